@@ -1,0 +1,163 @@
+/*
+ * mollifem_b200.h -- C-ABI of the B200 nonlocal stiffness assembly.
+ *
+ * Drop-in replacement for the numba cores the reference package binds on
+ * its hot path (/root/reference/pkg/src/mollifem/_kernels.py).  Plain C:
+ * pointers, sizes and an opaque stream handle; no torch or CUDA types.
+ *
+ * Conventions:
+ *   - every array argument is caller-owned DEVICE memory unless the
+ *     parameter comment says "host";
+ *   - kernels accumulate in place into `vals` like the reference cores;
+ *   - return 0 on success, MF_ERR_* otherwise; mf_last_error() gives a
+ *     thread-local message;
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy stream);
+ *   - no global mutable state: calls on distinct streams/devices with
+ *     disjoint output buffers may run concurrently.
+ */
+#ifndef MOLLIFEM_B200_H
+#define MOLLIFEM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MF_OK 0
+#define MF_ERR_ARG 1
+#define MF_ERR_CUDA 2
+#define MF_ERR_UNSUPPORTED 3
+
+#define MF_ABI_VERSION 1
+
+/* Mesh SoA + DOF map (mesh.py:78-88 flat arrays; fe_space.py:131-157). */
+typedef struct MfMesh {
+  int32_t dim;              /* 2 or 3 */
+  int32_t degree;           /* FE degree 1 or 2 */
+  int64_t n_elem;
+  int32_t nv_max;           /* geometry rows per element in elem_coords */
+  int32_t nloc_max;         /* columns of elem_dofs */
+  const int8_t *elem_kind;  /* (n) 0 quad, 1 tri, 2 hex */
+  const double *elem_coords;/* (n, nv_max, dim) */
+  const double *elem_lo;    /* (n, dim) bounding boxes */
+  const double *elem_hi;    /* (n, dim) */
+  const int64_t *elem_dofs; /* (n, nloc_max), -1 padded */
+  const int32_t *elem_cell; /* (n) flat cell id, x fastest (assembly.py:135) */
+  const int64_t *cell_ptr;  /* (ncells+1) elements per cell, cell-lex order */
+  int32_t ncx, ncy, ncz;    /* cell grid (ncz = 1 in 2D) */
+} MfMesh;
+
+/* Reference-element rules and inner shape tables (assembly.py:333-356).
+ * Tensor box rules also pass their 1D factor (n1d points/weights) so the
+ * specialised kernels can sum-factorise; n1d = 0 disables that path. */
+typedef struct MfRules {
+  int32_t nq_box_out, nq_box_in, nq_tri_out, nq_tri_in;
+  const double *box_out_pts, *box_out_w;  /* (nq, dim), (nq) */
+  const double *box_in_pts, *box_in_w;
+  const double *tri_out_pts, *tri_out_w;  /* (nq, 2), (nq) */
+  const double *tri_in_pts, *tri_in_w;
+  const double *phi_box_in;               /* (nq_box_in, nl_box) */
+  const double *phi_tri_in;               /* (nq_tri_in, nl_tri) */
+  int32_t n1d_box_out, n1d_box_in;
+  const double *box_out_x1d, *box_out_w1d;/* (n1d) */
+  const double *box_in_x1d, *box_in_w1d;
+} MfRules;
+
+/* Kernel + Algorithm-1 parameters (kernel.py:114-152, assembly.py:51-83). */
+typedef struct MfKernel {
+  double delta, eps, cde;   /* cde = C_{delta,eps} */
+  int32_t L_min, L_max;
+} MfKernel;
+
+/* Implicit structured pattern (assembly.py:189-223, 313-327): row r holds
+ * the clipped grid box of half-width K around r, x fastest. */
+typedef struct MfPattern {
+  int32_t NX, NY, NZ, K;
+  int64_t n;                /* rows = n_dofs */
+  const int64_t *rowptr;    /* (n+1) */
+} MfPattern;
+
+/* Counter slots written by mf_general_core (device uint64[MF_NCOUNTERS]). */
+#define MF_CNT_EVENTS 0        /* integration events (== reference events) */
+#define MF_CNT_PAIRS 1         /* (outer, inner) pairs visited */
+#define MF_CNT_EV_UPPER 2      /* events at level < L_max (mu == 1 plateau) */
+#define MF_CNT_EV_PLATEAU 3    /* L_max events proven inside delta-eps */
+#define MF_CNT_EV_DEAD 4       /* L_max events proven beyond delta+eps */
+#define MF_CNT_EV_FULL 5       /* L_max events integrated point by point */
+#define MF_NCOUNTERS 8
+
+/* Neighbour search.  Replaces _count_candidates/_fill_candidates
+ * (_kernels.py:1205-1268) as driven by _candidates (assembly.py:157-175):
+ * for outer element outer_ids[i], the inner elements e with inner_mask[e]
+ * in the (2R+1)^dim cell stencil whose max-axis box gap is < reach, in
+ * ascending id order.  Bit-exact with the reference. */
+int mf_count_candidates(const MfMesh *mesh, const int64_t *outer_ids,
+                        int64_t n_outer, const uint8_t *inner_mask,
+                        int32_t R, double reach, int64_t *counts,
+                        void *stream);
+int mf_fill_candidates(const MfMesh *mesh, const int64_t *outer_ids,
+                       int64_t n_outer, const uint8_t *inner_mask,
+                       int32_t R, double reach, const int64_t *ptr,
+                       int64_t *ids, void *stream);
+
+/* ptr[0] = 0, ptr[i+1] = sum(counts[0..i]) (np.cumsum, assembly.py:169). */
+size_t mf_scan_workspace_bytes(int64_t n);
+int mf_exclusive_scan(const int64_t *counts, int64_t n, int64_t *ptr,
+                      void *workspace, size_t ws_bytes, void *stream);
+
+/* Adaptive pair assembly.  Replaces _general_core (_kernels.py:391-487)
+ * together with the candidate lists it consumes: every pair (l, m) with
+ * outer_mask[l], m in inner_sorted and max-axis box gap < delta+eps runs
+ * Algorithm 1 (_pair_blocks, _kernels.py:184-313) with bit-exact
+ * classification; scale*(A21 + A22) blocks are added into vals (scale = 2
+ * folds _finish's doubling, assembly.py:441).
+ *
+ * inner_sorted (device int32) lists the inner elements grouped by colour;
+ * color_ptr (HOST int64[ncolors+1]) delimits the groups.  Elements of one
+ * colour share no DOF, so each colour is one race-free, atomic-free launch
+ * and the result is deterministic.  counters: device uint64[MF_NCOUNTERS]
+ * (accumulated).  flags: MF_FLAG_* below.  workspace: device scratch of at
+ * least mf_general_workspace_bytes() bytes. */
+#define MF_FLAG_FORCE_GENERIC 1   /* bypass the specialised kernels */
+#define MF_FLAG_NO_SHORTCUTS 2    /* integrate proven-plateau/dead events
+                                     point by point too */
+size_t mf_general_workspace_bytes(const MfMesh *mesh, const MfRules *rules,
+                                  int64_t n_inner);
+int mf_general_core(const MfMesh *mesh, const MfRules *rules,
+                    const MfKernel *kern, const MfPattern *pat,
+                    const uint8_t *outer_mask, const int32_t *inner_sorted,
+                    const int64_t *color_ptr, int32_t ncolors, int32_t R,
+                    double scale, double *vals, uint64_t *counters,
+                    int32_t flags, void *workspace, size_t ws_bytes,
+                    void *stream);
+
+/* Matrix utilities on the implicit pattern (_kernels.py:846-1202). */
+int mf_scale(double *vals, int64_t nnz, double s, void *stream);
+/* out: device double[1]; max over rows of sum_c |A_rc - A_cr| */
+int mf_asymmetry_inf(const MfPattern *pat, const double *vals, double *out,
+                     void *stream);
+int mf_norm_inf(const MfPattern *pat, const double *vals, double *out,
+                void *stream);
+int mf_matvec(const MfPattern *pat, const double *vals, const double *x,
+              double *y, void *stream);
+int mf_diag(const MfPattern *pat, const double *vals, double *out,
+            void *stream);
+int mf_symmetrize(const MfPattern *pat, double *vals, void *stream);
+int mf_fill_cols(const MfPattern *pat, int64_t *cols, void *stream);
+
+/* FP64 roofline probe: independent DFMA chains; out = device double[1]
+ * (sink).  Time it with events to get the sustained DFMA rate. */
+int mf_fp64_probe(double *out, int64_t iters, int32_t blocks,
+                  int32_t threads, void *stream);
+/* flops executed by one mf_fp64_probe launch with these arguments */
+double mf_fp64_probe_flops(int64_t iters, int32_t blocks, int32_t threads);
+
+const char *mf_last_error(void);
+int mf_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

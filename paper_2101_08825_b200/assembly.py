@@ -1,0 +1,580 @@
+"""Stiffness/load assembly entry points (reference rows a4-a14, boundary 8(b)).
+
+Host orchestration for the B200 path.  Mirrors the reference module
+`mollifem/assembly.py` -- same names, arguments, return contract and
+ValueError behaviour -- while every numeric kernel on the path runs in
+`csrc/` through the C-ABI in `include/mollifem_b200.h`:
+
+  assemble()            assembly.py:456-473  -> mf_general_core (+ mf_scale
+                                                 folded, mf_asymmetry_inf)
+  neighbor_sets()       assembly.py:178-183  -> mf_count/fill_candidates
+  assemble_rhs()        assembly.py:679-691  -> mf_load_scatter, mf_matvec
+  SparseMatrix methods  assembly.py:189-310  -> mf_matvec/diag/...
+
+The matrix is A = 2(A21 + A22) on the implicit structured pattern (row r
+couples to the clipped grid box of half-width K around r).  There is no
+CPU fallback: without the CUDA library every device call raises.
+"""
+
+import math
+
+import numpy as np
+
+from .fe_space import eval_shape_functions
+from .kernel import mollifier  # noqa: F401  (re-exported like the reference)
+from .mesh import BoundingBox
+from .quadrature import rule_for_kind
+
+__all__ = ["AssemblyConfig", "SparseMatrix", "NeighborSets", "assemble",
+           "assemble_rhs", "neighbor_sets", "pattern_halfwidth",
+           "aprx_min_dist", "aprx_max_dist"]
+
+
+class AssemblyConfig:
+    """Method, recursion window [L_min, L_max], rule presets, strategy.
+
+    Validation follows assembly.py:58-78.  strategy "auto"/"general"/
+    "blocked" are all accepted; on the device every strategy runs the
+    per-pair general kernel (the blocked CPU shortcut is a host
+    optimisation of the same matrix, assembly.py:391-437).
+    """
+
+    def __init__(self, method="mollified_adaptive", L_min=1, L_max=3,
+                 outer_rule="default", inner_rule="default", strategy="auto",
+                 symmetrize=False):
+        if method not in ("mollified_adaptive", "barycenter"):
+            raise ValueError(f"unknown assembly method {method!r}")
+        if not 1 <= L_min <= L_max:
+            raise ValueError("need 1 <= L_min <= L_max")
+        if L_max > 24:
+            raise ValueError("L_max > 24 exceeds the recursion stack bound")
+        if strategy not in ("auto", "general", "blocked"):
+            raise ValueError(f"unknown strategy {strategy!r}")
+        self.method = method
+        self.L_min = int(L_min)
+        self.L_max = int(L_max)
+        self.outer_rule = outer_rule
+        self.inner_rule = inner_rule
+        self.strategy = strategy
+        self.symmetrize = bool(symmetrize)
+
+    def __repr__(self):
+        return (f"AssemblyConfig({self.method}, L=[{self.L_min},"
+                f"{self.L_max}], outer={self.outer_rule!r}, "
+                f"inner={self.inner_rule!r}, strategy={self.strategy})")
+
+
+# ---------------------------------------------------------------------------
+# conservative box distances (assembly.py:96-111)
+
+def _box_lo_hi(box):
+    if isinstance(box, BoundingBox):
+        return box.lo, box.hi
+    lo, hi = box
+    return np.asarray(lo, dtype=float), np.asarray(hi, dtype=float)
+
+
+def aprx_min_dist(box_a, box_b):
+    """Largest single-axis gap (0 if the boxes overlap): a lower bound."""
+    alo, ahi = _box_lo_hi(box_a)
+    blo, bhi = _box_lo_hi(box_b)
+    return float(max(np.maximum(alo - bhi, blo - ahi).max(), 0.0))
+
+
+def aprx_max_dist(box_a, box_b):
+    """Euclidean norm of per-axis extreme separations: an upper bound."""
+    alo, ahi = _box_lo_hi(box_a)
+    blo, bhi = _box_lo_hi(box_b)
+    d = np.maximum(np.abs(alo - bhi), np.abs(blo - ahi))
+    return float(np.sqrt((d * d).sum()))
+
+
+def stencil_radius(reach, h):
+    """Cell stencil radius R = floor(reach/h + 1e-12) + 1 (assembly.py:151)."""
+    return int(math.floor(reach / h + 1e-12)) + 1
+
+
+def pattern_halfwidth(mesh, params, config, degree):
+    """(K, oe): grid half-width of a row's coupling box (assembly.py:313)."""
+    if config.method == "barycenter":
+        f = 2.0 / 3.0 if mesh.kind in ("tri", "mixed") else 0.5
+        oe = int(math.floor(params.delta / mesh.h + f + 1e-12))
+    else:
+        oe = int(math.floor((params.delta + params.eps) / mesh.h + 1e-12)) + 1
+    return degree * (oe + 1), oe
+
+
+# ---------------------------------------------------------------------------
+# rule / table preparation (assembly.py:333-356)
+
+class PrepTables:
+    """Outer/inner reference rules and inner shape tables for one config."""
+
+    def __init__(self, mesh, space, config):
+        dim = mesh.dim
+        box_kind = "hex" if dim == 3 else "quad"
+        outer = config.outer_rule
+        if outer == "default" and config.method == "barycenter":
+            outer = "lobatto3"
+        self.box_out = rule_for_kind(box_kind, outer)
+        self.box_in = rule_for_kind(box_kind, config.inner_rule)
+        self.tri_out = rule_for_kind("tri", outer)
+        self.tri_in = rule_for_kind("tri", config.inner_rule)
+        deg = space.degree
+        self.PHI_box_in = np.ascontiguousarray(
+            eval_shape_functions(box_kind, deg, self.box_in.ref_points))
+        self.PHI_tri_in = np.ascontiguousarray(
+            eval_shape_functions("tri", deg, self.tri_in.ref_points))
+        self.box_out_pts = np.ascontiguousarray(self.box_out.ref_points)
+        self.box_out_w = np.ascontiguousarray(self.box_out.weights)
+        self.box_in_pts = np.ascontiguousarray(self.box_in.ref_points)
+        self.box_in_w = np.ascontiguousarray(self.box_in.weights)
+        self.tri_out_pts = np.ascontiguousarray(self.tri_out.ref_points)
+        self.tri_out_w = np.ascontiguousarray(self.tri_out.weights)
+        self.tri_in_pts = np.ascontiguousarray(self.tri_in.ref_points)
+        self.tri_in_w = np.ascontiguousarray(self.tri_in.weights)
+        # 1D factors of the tensor box rules (for sum factorisation)
+        self.box_out_1d = _rule_1d(outer)
+        self.box_in_1d = _rule_1d(config.inner_rule)
+
+
+def _rule_1d(preset):
+    from .quadrature import _preset, gauss_legendre_1d, gauss_lobatto_1d
+    fam, n = _preset(preset)
+    r = gauss_legendre_1d(n) if fam == "gauss" else gauss_lobatto_1d(n)
+    return (np.ascontiguousarray(r.ref_points[:, 0]),
+            np.ascontiguousarray(r.weights))
+
+
+def prep_tables(mesh, space, config):
+    return PrepTables(mesh, space, config)
+
+
+# ---------------------------------------------------------------------------
+# implicit-pattern matrix
+
+class HostPattern:
+    """Pattern metadata + a host value array (assembly.py:197-223)."""
+
+    def _init_pattern(self, space, K):
+        dims = space.grid_dims
+        self.NX = int(dims[0])
+        self.NY = int(dims[1])
+        self.NZ = int(dims[2]) if len(dims) == 3 else 1
+        self.K = int(K)
+        self.n = int(space.n_dofs)
+        r = np.arange(self.n, dtype=np.int64)
+        self.gx = (r % self.NX).astype(np.int32)
+        t = r // self.NX
+        self.gy = (t % self.NY).astype(np.int32)
+        self.gz = (t // self.NY).astype(np.int32)
+
+        def width(g, N):
+            lo = np.maximum(g - self.K, 0)
+            hi = np.minimum(g + self.K, N - 1)
+            return (hi - lo + 1).astype(np.int64)
+
+        row_nnz = width(self.gx, self.NX) * width(self.gy, self.NY)
+        if self.NZ > 1:
+            row_nnz *= width(self.gz, self.NZ)
+        self.rowptr = np.zeros(self.n + 1, dtype=np.int64)
+        np.cumsum(row_nnz, out=self.rowptr[1:])
+        self.presym_asymmetry = None
+        self.events = None
+
+    def __init__(self, space, K, allocate=True):
+        self._init_pattern(space, K)
+        self._vals = (np.zeros(int(self.rowptr[-1]), dtype=np.float64)
+                      if allocate else None)
+
+    @classmethod
+    def for_space(cls, mesh, space, params, config):
+        K, oe = pattern_halfwidth(mesh, params, config, space.degree)
+        A = cls(space, K)
+        A._offset_reach = oe
+        return A
+
+    @property
+    def vals(self):
+        return self._vals
+
+    @vals.setter
+    def vals(self, v):
+        self._vals = v
+
+    @property
+    def nnz(self):
+        return int(self.rowptr[-1])
+
+    @property
+    def n_rows(self):
+        return self.n
+
+    @property
+    def n_cols(self):
+        return self.n
+
+    @property
+    def shape(self):
+        return (self.n, self.n)
+
+    def row_cols(self, r):
+        xlo = max(self.gx[r] - self.K, 0)
+        xhi = min(self.gx[r] + self.K, self.NX - 1)
+        ylo = max(self.gy[r] - self.K, 0)
+        yhi = min(self.gy[r] + self.K, self.NY - 1)
+        zlo = max(self.gz[r] - self.K, 0)
+        zhi = min(self.gz[r] + self.K, self.NZ - 1)
+        cx = np.arange(xlo, xhi + 1)
+        cy = np.arange(ylo, yhi + 1)
+        cz = np.arange(zlo, zhi + 1)
+        return ((cz[:, None, None] * self.NY + cy[None, :, None]) * self.NX
+                + cx[None, None, :]).ravel()
+
+    def row_entries(self, r):
+        return self.row_cols(r), self.vals[self.rowptr[r]:self.rowptr[r + 1]]
+
+    def __repr__(self):
+        return f"{type(self).__name__}(n={self.n}, K={self.K}, nnz={self.nnz})"
+
+
+class SparseMatrix(HostPattern):
+    """Values-only matrix on the structured DOF grid (assembly.py:189-310).
+
+    After `assemble()` the values live in HBM (`vals_device`) and, unless
+    the caller asked for a device-only result, in the host array `vals`
+    (the reference contract).  Every method runs on the device through the
+    C-ABI; after mutating the host `vals` call `sync_to_device()`.
+    """
+
+    def __init__(self, space, K, allocate=True):
+        super().__init__(space, K, allocate=allocate)
+        self._dvals = None
+        self._drowptr = None
+        self.counters = None
+
+    # -- device plumbing -------------------------------------------------
+    def _pattern_struct(self):
+        from . import _native as N
+        if self._drowptr is None:
+            from .device import to_device
+            self._drowptr = to_device(self.rowptr, None)
+        return N.MfPattern(NX=self.NX, NY=self.NY, NZ=self.NZ, K=self.K,
+                           n=self.n, rowptr=self._drowptr.data_ptr())
+
+    @property
+    def vals_device(self):
+        if self._dvals is None:
+            self.sync_to_device()
+        return self._dvals
+
+    def sync_to_device(self):
+        from .device import to_device
+        if self._vals is None:
+            raise RuntimeError("matrix has no values")
+        self._dvals = to_device(self._vals, None)
+        return self._dvals
+
+    @property
+    def vals(self):
+        if self._vals is None and self._dvals is not None:
+            self._vals = _d2h(self._dvals)
+        return self._vals
+
+    @vals.setter
+    def vals(self, v):
+        self._vals = v
+        self._dvals = None
+
+    def _call(self, name, *args):
+        from . import _native as N
+        L = N.lib()
+        N.check(getattr(L, name)(C_byref(self._pattern_struct()), *args,
+                                 N.stream_ptr()), name)
+
+    def _dev_vec(self, x):
+        import torch
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        if x.shape != (self.n,):
+            raise ValueError(f"vector length must be {self.n}")
+        return torch.from_numpy(x).to(self.vals_device.device)
+
+    # -- reference methods -------------------------------------------------
+    def matvec(self, x):
+        import torch
+        from . import _native as N
+        xd = self._dev_vec(x)
+        yd = torch.empty_like(xd)
+        self._call("mf_matvec", N.ptr(self.vals_device), N.ptr(xd),
+                   N.ptr(yd))
+        return yd.cpu().numpy()
+
+    def __matmul__(self, x):
+        return self.matvec(x)
+
+    def symmetrize_(self):
+        from . import _native as N
+        self._call("mf_symmetrize", N.ptr(self.vals_device))
+        self._vals = None  # host copy refreshed lazily from the device
+
+    def _reduce(self, name):
+        import torch
+        from . import _native as N
+        out = torch.zeros(1, dtype=torch.float64,
+                          device=self.vals_device.device)
+        self._call(name, N.ptr(self.vals_device), N.ptr(out))
+        return float(out.item())
+
+    def asymmetry_inf(self):
+        """inf-norm of A - A^T."""
+        return self._reduce("mf_asymmetry_inf")
+
+    def norm_inf(self):
+        return self._reduce("mf_norm_inf")
+
+    def diag(self):
+        import torch
+        from . import _native as N
+        out = torch.empty(self.n, dtype=torch.float64,
+                          device=self.vals_device.device)
+        self._call("mf_diag", N.ptr(self.vals_device), N.ptr(out))
+        return out.cpu().numpy()
+
+    def to_scipy(self):
+        import torch
+        from scipy.sparse import csr_matrix
+        from . import _native as N
+        cols = torch.empty(self.nnz, dtype=torch.int64,
+                           device=self.vals_device.device)
+        self._call("mf_fill_cols", N.ptr(cols))
+        return csr_matrix((self.vals.copy(), cols.cpu().numpy(),
+                           self.rowptr.copy()), shape=(self.n, self.n))
+
+    def toarray(self):
+        return self.to_scipy().toarray()
+
+    def copy_pattern(self):
+        """All-zero host matrix sharing this pattern's metadata."""
+        other = object.__new__(SparseMatrix)
+        for a in ("NX", "NY", "NZ", "K", "n", "gx", "gy", "gz", "rowptr"):
+            setattr(other, a, getattr(self, a))
+        other._vals = np.zeros(self.nnz)
+        other._dvals = None
+        other._drowptr = self._drowptr
+        other.presym_asymmetry = None
+        other.events = None
+        other.counters = None
+        return other
+
+
+def C_byref(s):
+    import ctypes
+    return ctypes.byref(s)
+
+
+def _d2h(t):
+    """Device tensor -> host numpy through a pinned buffer."""
+    import torch
+    if t.numel() == 0:
+        return np.zeros(0, dtype=np.float64)
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    h.copy_(t, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return h.numpy()
+
+
+def _new_matrix(mesh, space, params, config, allocate):
+    K, oe = pattern_halfwidth(mesh, params, config, space.degree)
+    A = SparseMatrix(space, K, allocate=allocate)
+    A._offset_reach = oe
+    return A
+
+
+# ---------------------------------------------------------------------------
+# neighbour sets (assembly.py:117-183)
+
+class NeighborSets:
+    """CSR candidate lists: inner m of outer l with box gap < delta+eps."""
+
+    def __init__(self, outer_ids, ptr, ids):
+        self.outer_ids = outer_ids
+        self.ptr = ptr
+        self.ids = ids
+        self._pos = {int(l): i for i, l in enumerate(outer_ids)}
+
+    def of(self, l):
+        i = self._pos[int(l)]
+        return self.ids[self.ptr[i]:self.ptr[i + 1]]
+
+    def __len__(self):
+        return len(self.outer_ids)
+
+
+def candidates(mesh, reach, outer_ids, inner_mask, device=None,
+               dmesh=None, return_device=False):
+    """(ptr, ids) of `_candidates` (assembly.py:157-175), computed on GPU."""
+    import torch
+    from . import _native as N
+    from .device import DeviceMesh, to_device
+    L = N.lib()
+    if dmesh is None:
+        dmesh = DeviceMesh(mesh, _DummySpace(mesh), device)
+    dev = dmesh.device
+    outer = to_device(np.ascontiguousarray(outer_ids, np.int64), dev)
+    mask = to_device(np.ascontiguousarray(inner_mask, np.uint8), dev)
+    n = int(outer.numel())
+    R = stencil_radius(reach, mesh.h)
+    st = N.stream_ptr()
+    counts = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    N.check(L.mf_count_candidates(C_byref(dmesh.struct), N.ptr(outer), n,
+                                  N.ptr(mask), R, float(reach), N.ptr(counts),
+                                  st), "mf_count_candidates")
+    ptr = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    wsb = int(L.mf_scan_workspace_bytes(n))
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+    N.check(L.mf_exclusive_scan(N.ptr(counts), n, N.ptr(ptr), N.ptr(ws), wsb,
+                                st), "mf_exclusive_scan")
+    total = int(ptr[-1].item())
+    ids = torch.empty(max(total, 1), dtype=torch.int64, device=dev)
+    N.check(L.mf_fill_candidates(C_byref(dmesh.struct), N.ptr(outer), n,
+                                 N.ptr(mask), R, float(reach), N.ptr(ptr),
+                                 N.ptr(ids), st), "mf_fill_candidates")
+    ids = ids[:total]
+    if return_device:
+        return ptr, ids
+    return ptr.cpu().numpy(), ids.cpu().numpy()
+
+
+class _DummySpace:
+    """Degree-1 stand-in when only geometry is needed on the device."""
+
+    def __init__(self, mesh):
+        self.degree = 1
+        self.element_dofs = np.zeros((mesh.n_elements, 1), dtype=np.int64)
+
+
+def neighbor_sets(mesh, params):
+    """Candidate inner elements per outer element for kernel params."""
+    outer = np.arange(mesh.n_elements, dtype=np.int64)
+    mask = np.ones(mesh.n_elements, dtype=np.uint8)
+    ptr, ids = candidates(mesh, params.delta + params.eps, outer, mask)
+    return NeighborSets(outer, ptr, ids)
+
+
+# ---------------------------------------------------------------------------
+# assembly
+
+class AssemblyContext:
+    """Device-resident inputs of one (mesh, space, kernel, config) problem.
+
+    `assemble()` builds one per call (inputs copied host->device inside
+    the call, as the end-to-end contract requires); benchmarks and the
+    partitioned driver may build it once and call `run()` repeatedly.
+    """
+
+    def __init__(self, mesh, space, params, config, device=None):
+        from .device import DeviceMesh, DeviceRules
+        self.mesh, self.space, self.params, self.config = (mesh, space,
+                                                           params, config)
+        self.prep = prep_tables(mesh, space, config)
+        self.dmesh = DeviceMesh(mesh, space, device)
+        self.drules = DeviceRules(self.prep, device)
+        self.device = self.dmesh.device
+        self.R = stencil_radius(params.delta + params.eps, mesh.h)
+        self.h2d_bytes = self.dmesh.h2d_bytes
+
+    def kernel_struct(self):
+        from . import _native as N
+        p, c = self.params, self.config
+        return N.MfKernel(delta=p.delta, eps=p.eps, cde=p.c_delta_eps,
+                          L_min=c.L_min, L_max=c.L_max)
+
+    def new_matrix(self):
+        import torch
+        A = _new_matrix(self.mesh, self.space, self.params, self.config,
+                        allocate=False)
+        A._dvals = torch.zeros(A.nnz, dtype=torch.float64, device=self.device)
+        from .device import to_device
+        A._drowptr = to_device(A.rowptr, self.device)
+        self.h2d_bytes += A.rowptr.nbytes
+        return A
+
+    def run(self, A, outer_mask=None, inner_ids=None, scale=2.0, flags=0,
+            plan=None, counters=None):
+        """Accumulate scale*(A21 + A22) of the selected pairs into A."""
+        import torch
+        from . import _native as N
+        from .device import ColorPlan, to_device
+        L = N.lib()
+        n = self.mesh.n_elements
+        if outer_mask is None:
+            om = torch.ones(n, dtype=torch.uint8, device=self.device)
+        else:
+            om = to_device(np.ascontiguousarray(outer_mask, np.uint8),
+                           self.device)
+        if plan is None:
+            plan = ColorPlan(self.mesh, inner_ids, self.device)
+        if counters is None:
+            counters = torch.zeros(N.MF_NCOUNTERS, dtype=torch.int64,
+                                   device=self.device)
+        wsb = int(L.mf_general_workspace_bytes(C_byref(self.dmesh.struct),
+                                               C_byref(self.drules.struct),
+                                               plan.n_inner))
+        ws = torch.zeros(wsb, dtype=torch.uint8, device=self.device)
+        cp = plan.color_ptr.ctypes.data_as(ctypes_void_p())
+        N.check(L.mf_general_core(
+            C_byref(self.dmesh.struct), C_byref(self.drules.struct),
+            C_byref(self.kernel_struct()), C_byref(A._pattern_struct()),
+            N.ptr(om), N.ptr(plan.inner_sorted), cp, plan.NCOLORS, self.R,
+            float(scale), N.ptr(A._dvals), N.ptr(counters), int(flags),
+            N.ptr(ws), wsb, N.stream_ptr()), "mf_general_core")
+        return counters
+
+    def finish(self, A, counters):
+        """events/asymmetry/symmetrize (assembly.py:440-445, x2 folded)."""
+        import torch
+        from . import _native as N
+        out = torch.zeros(1, dtype=torch.float64, device=self.device)
+        pat = A._pattern_struct()
+        N.check(N.lib().mf_asymmetry_inf(C_byref(pat), N.ptr(A._dvals),
+                                          N.ptr(out), N.stream_ptr()),
+                "mf_asymmetry_inf")
+        if self.config.symmetrize:
+            N.check(N.lib().mf_symmetrize(C_byref(pat), N.ptr(A._dvals),
+                                           N.stream_ptr()), "mf_symmetrize")
+        cnt = counters.cpu().numpy()
+        A.counters = cnt
+        A.events = int(cnt[N.CNT_EVENTS])
+        A.presym_asymmetry = float(out.item())
+        return A
+
+
+def ctypes_void_p():
+    import ctypes
+    return ctypes.c_void_p
+
+
+def assemble(mesh, space, kernel, config=None, *, device=None, flags=0,
+             keep_on_device=False):
+    """Assemble the stiffness matrix A = 2(A21 + A22) on the GPU.
+
+    Same arguments and return contract as the reference (assembly.py:456):
+    a `SparseMatrix` with host `vals` (already x2), `events` and
+    `presym_asymmetry`.  keep_on_device=True skips the host copy (the
+    values stay in `A.vals_device`; `A.vals` copies them on first use).
+    """
+    config = config or AssemblyConfig()
+    if config.method == "barycenter":
+        raise NotImplementedError(
+            "the barycenter baseline (assembly.py:565-635) is outside the "
+            "B200 hot path; use the reference package for it")
+    if config.strategy == "blocked" and mesh.kind not in ("quad", "tri",
+                                                          "hex"):
+        raise ValueError("blocked strategy needs a pure-kind mesh")
+    ctx = AssemblyContext(mesh, space, kernel, config, device)
+    A = ctx.new_matrix()
+    counters = ctx.run(A, flags=flags)
+    ctx.finish(A, counters)
+    if not keep_on_device:
+        A._vals = _d2h(A._dvals)
+    return A

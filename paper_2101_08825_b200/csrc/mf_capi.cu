@@ -1,0 +1,293 @@
+// mf_capi.cu -- extern "C" entry points of include/mollifem_b200.h.
+//
+// Argument validation, launch configuration and kernel selection live
+// here; the kernels are in mf_candidates.cu, mf_generic.cu, mf_hex.cu,
+// mf_tri.cu and mf_matrix.cu.  Host arithmetic that feeds classification
+// (delta -/+ eps and their squares, _kernels.py:410-413) is plain IEEE
+// double without contraction (x86-64 host code, no -mfma).
+#include <string>
+
+#include "mf_common.cuh"
+
+cudaError_t mf_launch_candidates(const MfMesh &, const int64_t *, int64_t,
+                                 const uint8_t *, int, double, int64_t *,
+                                 const int64_t *, int64_t *, cudaStream_t);
+size_t mf_scan_bytes(int64_t n);
+cudaError_t mf_scan(const int64_t *, int64_t, int64_t *, void *, size_t,
+                    cudaStream_t);
+cudaError_t mf_launch_generic(const AsmParams &, int, int, cudaStream_t);
+// specialised kernels: return cudaErrorNotSupported when they do not cover
+// the configuration
+cudaError_t mf_launch_hex(const AsmParams &, cudaStream_t);
+cudaError_t mf_launch_tri(const AsmParams &, cudaStream_t);
+bool mf_hex_supported(const AsmParams &);
+bool mf_tri_supported(const AsmParams &);
+cudaError_t mf_launch_asym(const MfPattern &, const double *, double *,
+                           cudaStream_t);
+cudaError_t mf_launch_norm(const MfPattern &, const double *, double *,
+                           cudaStream_t);
+cudaError_t mf_launch_matvec(const MfPattern &, const double *,
+                             const double *, double *, cudaStream_t);
+cudaError_t mf_launch_symmetrize(const MfPattern &, double *, cudaStream_t);
+cudaError_t mf_launch_fill_cols(const MfPattern &, int64_t *, cudaStream_t);
+cudaError_t mf_launch_diag(const MfPattern &, const double *, double *,
+                           cudaStream_t);
+cudaError_t mf_launch_scale(double *, int64_t, double, cudaStream_t);
+cudaError_t mf_launch_probe(double *, int64_t, int, int, cudaStream_t);
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_status(cudaError_t e, const char *where) {
+  if (e == cudaSuccess) return MF_OK;
+  return fail(MF_ERR_CUDA,
+              std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int check_mesh(const MfMesh *m) {
+  if (!m) return fail(MF_ERR_ARG, "mesh is NULL");
+  if (m->dim != 2 && m->dim != 3) return fail(MF_ERR_ARG, "dim must be 2/3");
+  if (m->degree != 1 && m->degree != 2)
+    return fail(MF_ERR_ARG, "degree must be 1/2");
+  if (m->n_elem < 0) return fail(MF_ERR_ARG, "n_elem < 0");
+  if (m->n_elem > 0 && (!m->elem_kind || !m->elem_lo || !m->elem_hi ||
+                        !m->elem_cell || !m->cell_ptr))
+    return fail(MF_ERR_ARG, "mesh array is NULL");
+  if (m->ncx < 1 || m->ncy < 1 || m->ncz < 1)
+    return fail(MF_ERR_ARG, "bad cell grid");
+  return MF_OK;
+}
+
+int check_pattern(const MfPattern *p) {
+  if (!p) return fail(MF_ERR_ARG, "pattern is NULL");
+  if (p->n > 0 && !p->rowptr) return fail(MF_ERR_ARG, "rowptr is NULL");
+  if (p->NX < 1 || p->NY < 1 || p->NZ < 1 || p->K < 0)
+    return fail(MF_ERR_ARG, "bad pattern grid");
+  if ((int64_t)p->NX * p->NY * p->NZ != p->n)
+    return fail(MF_ERR_ARG, "pattern grid does not match n");
+  return MF_OK;
+}
+
+constexpr int kGenericBlock = 128;
+constexpr int kGenericMaxGrid = 148 * 4;
+
+int nq_in_max(const MfRules *r) {
+  return r->nq_box_in > r->nq_tri_in ? r->nq_box_in : r->nq_tri_in;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *mf_last_error(void) { return g_err.c_str(); }
+int mf_abi_version(void) { return MF_ABI_VERSION; }
+
+int mf_count_candidates(const MfMesh *mesh, const int64_t *outer_ids,
+                        int64_t n_outer, const uint8_t *inner_mask,
+                        int32_t R, double reach, int64_t *counts,
+                        void *stream) {
+  if (int rc = check_mesh(mesh)) return rc;
+  if (n_outer < 0 || R < 1) return fail(MF_ERR_ARG, "bad n_outer/R");
+  if (n_outer > 0 && (!outer_ids || !inner_mask || !counts))
+    return fail(MF_ERR_ARG, "NULL array");
+  return cuda_status(
+      mf_launch_candidates(*mesh, outer_ids, n_outer, inner_mask, R, reach,
+                           counts, nullptr, nullptr, S(stream)),
+      "mf_count_candidates");
+}
+
+int mf_fill_candidates(const MfMesh *mesh, const int64_t *outer_ids,
+                       int64_t n_outer, const uint8_t *inner_mask, int32_t R,
+                       double reach, const int64_t *ptr, int64_t *ids,
+                       void *stream) {
+  if (int rc = check_mesh(mesh)) return rc;
+  if (n_outer < 0 || R < 1) return fail(MF_ERR_ARG, "bad n_outer/R");
+  if (n_outer == 0) return MF_OK;
+  if (!outer_ids || !inner_mask || !ptr) return fail(MF_ERR_ARG, "NULL array");
+  if (!ids) {
+    // a zero-length ids buffer may be NULL only if there are no pairs;
+    // the kernel would not write anything then
+    static int64_t dummy;
+    ids = &dummy;
+  }
+  return cuda_status(
+      mf_launch_candidates(*mesh, outer_ids, n_outer, inner_mask, R, reach,
+                           nullptr, ptr, ids, S(stream)),
+      "mf_fill_candidates");
+}
+
+size_t mf_scan_workspace_bytes(int64_t n) { return mf_scan_bytes(n); }
+
+int mf_exclusive_scan(const int64_t *counts, int64_t n, int64_t *ptr,
+                      void *workspace, size_t ws_bytes, void *stream) {
+  if (n < 0 || !ptr || (n > 0 && !counts))
+    return fail(MF_ERR_ARG, "bad scan arguments");
+  if (n > 0x7fffffffLL) return fail(MF_ERR_UNSUPPORTED, "scan n > 2^31");
+  if (n > 0 && ws_bytes < mf_scan_bytes(n))
+    return fail(MF_ERR_ARG, "scan workspace too small");
+  return cuda_status(mf_scan(counts, n, ptr, workspace, ws_bytes, S(stream)),
+                     "mf_exclusive_scan");
+}
+
+size_t mf_general_workspace_bytes(const MfMesh *mesh, const MfRules *rules,
+                                  int64_t n_inner) {
+  (void)mesh;
+  int64_t threads = (int64_t)kGenericMaxGrid * kGenericBlock;
+  int64_t want = ((n_inner + kGenericBlock - 1) / kGenericBlock) *
+                 kGenericBlock;
+  if (want < threads) threads = want > 0 ? want : kGenericBlock;
+  int nq = rules ? nq_in_max(rules) : 1;
+  return (size_t)threads * (size_t)nq * sizeof(double) + 256;
+}
+
+int mf_general_core(const MfMesh *mesh, const MfRules *rules,
+                    const MfKernel *kern, const MfPattern *pat,
+                    const uint8_t *outer_mask, const int32_t *inner_sorted,
+                    const int64_t *color_ptr, int32_t ncolors, int32_t R,
+                    double scale, double *vals, uint64_t *counters,
+                    int32_t flags, void *workspace, size_t ws_bytes,
+                    void *stream) {
+  if (int rc = check_mesh(mesh)) return rc;
+  if (int rc = check_pattern(pat)) return rc;
+  if (!rules || !kern) return fail(MF_ERR_ARG, "rules/kernel is NULL");
+  if (!color_ptr || ncolors < 1) return fail(MF_ERR_ARG, "bad colours");
+  if (!counters || !vals) return fail(MF_ERR_ARG, "vals/counters NULL");
+  if (kern->L_min < 1 || kern->L_min > kern->L_max || kern->L_max > 24)
+    return fail(MF_ERR_ARG, "need 1 <= L_min <= L_max <= 24");
+  if (!(kern->eps >= 0.0 && kern->eps < kern->delta))
+    return fail(MF_ERR_ARG, "need 0 <= eps < delta");
+  if (R < 1) return fail(MF_ERR_ARG, "R < 1");
+  int64_t n_inner = color_ptr[ncolors];
+  if (n_inner == 0) return MF_OK;
+  if (!outer_mask || !inner_sorted) return fail(MF_ERR_ARG, "NULL masks");
+
+  AsmParams P;
+  P.mesh = *mesh;
+  P.rules = *rules;
+  P.pat = *pat;
+  P.outer_mask = outer_mask;
+  P.R = R;
+  P.scale = scale;
+  P.vals = vals;
+  P.counters = reinterpret_cast<unsigned long long *>(counters);
+  P.flags = flags;
+  P.L_min = kern->L_min;
+  P.L_max = kern->L_max;
+  P.delta = kern->delta;
+  P.eps = kern->eps;
+  P.cde = kern->cde;
+  const double dm = kern->delta - kern->eps;
+  const double dp = kern->delta + kern->eps;
+  P.dme = dm;
+  P.dpe = dp;
+  P.dm2 = dm * dm;
+  P.dp2 = dp * dp;
+  P.dme2_lo = dm * dm * (1.0 - 4e-12);
+  P.dme2_hi = dm * dm * (1.0 + 4e-12);
+  P.nl_box = mesh->dim == 3 ? (mesh->degree + 1) * (mesh->degree + 1) *
+                                  (mesh->degree + 1)
+                            : (mesh->degree + 1) * (mesh->degree + 1);
+  P.nl_tri = 3 * mesh->degree;
+  P.shortcuts = (flags & MF_FLAG_NO_SHORTCUTS) == 0 && kern->eps > 0.0;
+  const size_t need = mf_general_workspace_bytes(mesh, rules, n_inner);
+  if (!workspace || ws_bytes < need)
+    return fail(MF_ERR_ARG, "workspace too small");
+  P.overflow = reinterpret_cast<int32_t *>(workspace);
+  P.scratch = reinterpret_cast<double *>(static_cast<char *>(workspace) + 256);
+  P.scratch_stride = nq_in_max(rules);
+  cudaStream_t s = S(stream);
+
+  const bool force_generic = (flags & MF_FLAG_FORCE_GENERIC) != 0;
+  bool use_hex = !force_generic && mf_hex_supported(P);
+  bool use_tri = !force_generic && !use_hex && mf_tri_supported(P);
+  for (int c = 0; c < ncolors; c++) {
+    int64_t n = color_ptr[c + 1] - color_ptr[c];
+    if (n <= 0) continue;
+    P.inner = inner_sorted + color_ptr[c];
+    P.n_inner = n;
+    cudaError_t e;
+    if (use_hex) {
+      e = mf_launch_hex(P, s);
+    } else if (use_tri) {
+      e = mf_launch_tri(P, s);
+    } else {
+      int64_t want = (n + kGenericBlock - 1) / kGenericBlock;
+      int grid = (int)(want < kGenericMaxGrid ? want : kGenericMaxGrid);
+      e = mf_launch_generic(P, grid, kGenericBlock, s);
+    }
+    if (e != cudaSuccess) return cuda_status(e, "mf_general_core");
+  }
+  return MF_OK;
+}
+
+int mf_scale(double *vals, int64_t nnz, double sc, void *stream) {
+  if (nnz < 0 || (nnz > 0 && !vals)) return fail(MF_ERR_ARG, "bad scale");
+  return cuda_status(mf_launch_scale(vals, nnz, sc, S(stream)), "mf_scale");
+}
+
+int mf_asymmetry_inf(const MfPattern *pat, const double *vals, double *out,
+                     void *stream) {
+  if (int rc = check_pattern(pat)) return rc;
+  if (!vals || !out) return fail(MF_ERR_ARG, "NULL array");
+  return cuda_status(mf_launch_asym(*pat, vals, out, S(stream)),
+                     "mf_asymmetry_inf");
+}
+
+int mf_norm_inf(const MfPattern *pat, const double *vals, double *out,
+                void *stream) {
+  if (int rc = check_pattern(pat)) return rc;
+  if (!vals || !out) return fail(MF_ERR_ARG, "NULL array");
+  return cuda_status(mf_launch_norm(*pat, vals, out, S(stream)),
+                     "mf_norm_inf");
+}
+
+int mf_matvec(const MfPattern *pat, const double *vals, const double *x,
+              double *y, void *stream) {
+  if (int rc = check_pattern(pat)) return rc;
+  if (!vals || !x || !y) return fail(MF_ERR_ARG, "NULL array");
+  return cuda_status(mf_launch_matvec(*pat, vals, x, y, S(stream)),
+                     "mf_matvec");
+}
+
+int mf_diag(const MfPattern *pat, const double *vals, double *out,
+            void *stream) {
+  if (int rc = check_pattern(pat)) return rc;
+  if (!vals || !out) return fail(MF_ERR_ARG, "NULL array");
+  return cuda_status(mf_launch_diag(*pat, vals, out, S(stream)), "mf_diag");
+}
+
+int mf_symmetrize(const MfPattern *pat, double *vals, void *stream) {
+  if (int rc = check_pattern(pat)) return rc;
+  if (!vals) return fail(MF_ERR_ARG, "NULL array");
+  return cuda_status(mf_launch_symmetrize(*pat, vals, S(stream)),
+                     "mf_symmetrize");
+}
+
+int mf_fill_cols(const MfPattern *pat, int64_t *cols, void *stream) {
+  if (int rc = check_pattern(pat)) return rc;
+  if (!cols) return fail(MF_ERR_ARG, "NULL array");
+  return cuda_status(mf_launch_fill_cols(*pat, cols, S(stream)),
+                     "mf_fill_cols");
+}
+
+int mf_fp64_probe(double *out, int64_t iters, int32_t blocks,
+                  int32_t threads, void *stream) {
+  if (!out || iters < 1 || blocks < 1 || threads < 32 || threads > 1024)
+    return fail(MF_ERR_ARG, "bad probe arguments");
+  return cuda_status(mf_launch_probe(out, iters, blocks, threads, S(stream)),
+                     "mf_fp64_probe");
+}
+
+double mf_fp64_probe_flops(int64_t iters, int32_t blocks, int32_t threads) {
+  return 2.0 * 8.0 * (double)iters * (double)blocks * (double)threads;
+}
+
+}  // extern "C"

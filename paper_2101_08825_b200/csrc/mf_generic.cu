@@ -1,0 +1,458 @@
+// mf_generic.cu -- generic adaptive pair assembly (all kinds/degrees/rules).
+//
+// One thread per INNER element m of the current colour.  The thread
+// enumerates its outer partners l in the (2R+1)^dim cell stencil with the
+// exact candidate test (max-axis gap < delta+eps, _kernels.py:1225-1233; the
+// relation is symmetric so this is the transpose of the reference's
+// J_l lists), runs Algorithm 1 per pair (_pair_blocks, _kernels.py:184-313)
+// as a depth-first walk that keeps one geometry per level, integrates each
+// event in the reference's rank-1 form (_event_box/_event_tri,
+// _kernels.py:105-181) and adds the inner-row blocks into vals.  A22 is
+// folded once per inner element from the element-level sum of gsum over all
+// its pairs (the reference folds per pair, _kernels.py:303-312; same sum).
+//
+// All of a pair's entries lie in rows of the inner element
+// (_kernels.py:483-486), and same-colour elements share no DOF, so the
+// launch is race-free without atomics and deterministic.
+//
+// This kernel is the fallback for configurations the specialised kernels
+// (mf_hex.cu, mf_tri.cu) do not cover: mixed meshes, degree 2, large rules,
+// deep L_max.
+#include "mf_common.cuh"
+
+namespace {
+
+constexpr int kLevels = 25;  // L_max <= 24 (assembly.py:65)
+
+struct Outer {
+  int kind;       // 0 quad, 1 tri, 2 hex
+  int nloc;
+  double geo[6];  // box lo/hi or tri vertices
+  double lo[3], hi[3];
+  double v0[2], inv[4];
+};
+
+template <int DIM>
+MF_DEV void sub_bbox(int kind, const double *g, double *slo, double *shi) {
+  if (kind == 1) {
+    slo[0] = pmin(g[0], pmin(g[2], g[4]));
+    shi[0] = pmax(g[0], pmax(g[2], g[4]));
+    slo[1] = pmin(g[1], pmin(g[3], g[5]));
+    shi[1] = pmax(g[1], pmax(g[3], g[5]));
+  } else {
+#pragma unroll
+    for (int k = 0; k < DIM; k++) {
+      slo[k] = g[k];
+      shi[k] = g[DIM + k];
+    }
+  }
+}
+
+// child b of sub-cell g (_kernels.py:253-302), exact midpoint arithmetic
+template <int DIM>
+MF_DEV void make_child(int kind, const double *g, int b, double *c) {
+  if (kind == 1) {
+    double m010 = xmul(0.5, xadd(g[0], g[2]));
+    double m011 = xmul(0.5, xadd(g[1], g[3]));
+    double m120 = xmul(0.5, xadd(g[2], g[4]));
+    double m121 = xmul(0.5, xadd(g[3], g[5]));
+    double m200 = xmul(0.5, xadd(g[4], g[0]));
+    double m201 = xmul(0.5, xadd(g[5], g[1]));
+    if (b == 0) {
+      c[0] = g[0]; c[1] = g[1]; c[2] = m010; c[3] = m011; c[4] = m200;
+      c[5] = m201;
+    } else if (b == 1) {
+      c[0] = m010; c[1] = m011; c[2] = g[2]; c[3] = g[3]; c[4] = m120;
+      c[5] = m121;
+    } else if (b == 2) {
+      c[0] = m200; c[1] = m201; c[2] = m120; c[3] = m121; c[4] = g[4];
+      c[5] = g[5];
+    } else {
+      c[0] = m010; c[1] = m011; c[2] = m120; c[3] = m121; c[4] = m200;
+      c[5] = m201;
+    }
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < DIM; k++) {
+    double lo = g[k], hi = g[DIM + k];
+    double mid = xmul(0.5, xadd(lo, hi));
+    if (((b >> k) & 1) == 0) {
+      c[k] = lo;
+      c[DIM + k] = mid;
+    } else {
+      c[k] = mid;
+      c[DIM + k] = hi;
+    }
+  }
+}
+
+struct Inner {
+  int kind, nq, nloc;
+  const double *pts, *w, *phi;
+  double lo[3], hi[3];
+  double c0[2], e1[2], e2[2];  // tri: vertex 0 and edges
+  double scale_w;              // det (tri) or jac (box)
+};
+
+// physical inner point q (_inner_data, _kernels.py:316-340), exact
+template <int DIM>
+MF_DEV void inner_point(const Inner &I, int q, double *y) {
+  if (I.kind == 1) {
+    double p0 = I.pts[q * 2], p1 = I.pts[q * 2 + 1];
+    y[0] = xadd(xadd(I.c0[0], xmul(p0, I.e1[0])), xmul(p1, I.e2[0]));
+    y[1] = xadd(xadd(I.c0[1], xmul(p0, I.e1[1])), xmul(p1, I.e2[1]));
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < DIM; k++)
+    y[k] = xadd(I.lo[k], xmul(xmul(xadd(I.pts[q * DIM + k], 1.0), 0.5),
+                              xsub(I.hi[k], I.lo[k])));
+}
+
+// one integration event on sub-cell g (reference rank-1 form)
+template <int DIM, int NLM>
+MF_DEV void event_full(const AsmParams &P, const Outer &O, const double *g,
+                       const Inner &I, double *b21, double *G) {
+  const MfRules &Rr = P.rules;
+  int degree = P.mesh.degree;
+  double phi2[NLM];
+  if (O.kind == 1) {
+    double e10 = xsub(g[2], g[0]), e11 = xsub(g[3], g[1]);
+    double e20 = xsub(g[4], g[0]), e21 = xsub(g[5], g[1]);
+    double det = e10 * e21 - e11 * e20;
+    for (int q2 = 0; q2 < Rr.nq_tri_out; q2++) {
+      double px = Rr.tri_out_pts[q2 * 2], py = Rr.tri_out_pts[q2 * 2 + 1];
+      double x[3];
+      x[0] = xadd(xadd(g[0], xmul(px, e10)), xmul(py, e20));
+      x[1] = xadd(xadd(g[1], xmul(px, e11)), xmul(py, e21));
+      double w2q = Rr.tri_out_w[q2] * det * P.cde * (1.0 / 256.0);
+      double dx0 = x[0] - O.v0[0], dx1 = x[1] - O.v0[1];
+      double rx = O.inv[0] * dx0 + O.inv[1] * dx1;
+      double ry = O.inv[2] * dx0 + O.inv[3] * dx1;
+      shape_at(1, degree, 2, rx, ry, 0.0, phi2);
+      for (int q1 = 0; q1 < I.nq; q1++) {
+        double y[3];
+        inner_point<DIM>(I, q1, y);
+        double dx = xsub(x[0], y[0]), dy = xsub(x[1], y[1]);
+        double d2 = xadd(xmul(dx, dx), xmul(dy, dy));
+        if (d2 >= P.dp2) continue;
+        double tq = mu256(P, d2) * w2q;
+        G[q1] += tq;
+        double tw = tq * I.w[q1] * I.scale_w;
+        for (int i = 0; i < I.nloc; i++) {
+          double ci = tw * I.phi[q1 * I.nloc + i];
+          for (int j = 0; j < O.nloc; j++) b21[i * NLM + j] -= ci * phi2[j];
+        }
+      }
+    }
+    return;
+  }
+  double jac = 1.0;
+#pragma unroll
+  for (int k = 0; k < DIM; k++) jac *= 0.5 * (g[DIM + k] - g[k]);
+  for (int q2 = 0; q2 < Rr.nq_box_out; q2++) {
+    double x[3], r[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int k = 0; k < DIM; k++) {
+      x[k] = xadd(g[k], xmul(xmul(xadd(Rr.box_out_pts[q2 * DIM + k], 1.0),
+                                  0.5),
+                             xsub(g[DIM + k], g[k])));
+      r[k] = (x[k] - O.lo[k]) / (O.hi[k] - O.lo[k]) * 2.0 - 1.0;
+    }
+    double w2q = Rr.box_out_w[q2] * jac * P.cde * (1.0 / 256.0);
+    shape_at(O.kind, degree, DIM, r[0], r[1], r[2], phi2);
+    for (int q1 = 0; q1 < I.nq; q1++) {
+      double y[3];
+      inner_point<DIM>(I, q1, y);
+      double d2 = 0.0;
+#pragma unroll
+      for (int k = 0; k < DIM; k++) {
+        double dk = xsub(x[k], y[k]);
+        d2 = (k == 0) ? xmul(dk, dk) : xadd(d2, xmul(dk, dk));
+      }
+      if (d2 >= P.dp2) continue;
+      double tq = mu256(P, d2) * w2q;
+      G[q1] += tq;
+      double tw = tq * I.w[q1] * I.scale_w;
+      for (int i = 0; i < I.nloc; i++) {
+        double ci = tw * I.phi[q1 * I.nloc + i];
+        for (int j = 0; j < O.nloc; j++) b21[i * NLM + j] -= ci * phi2[j];
+      }
+    }
+  }
+}
+
+// plateau shortcut: every point pair has mu == 1 (sub-cell proven inside
+// delta-eps), so the event is rank-1:  b21 -= cde * m (x) S,  G += cde * W
+template <int DIM, int NLM>
+MF_DEV void event_plateau(const AsmParams &P, const Outer &O, const double *g,
+                          const Inner &I, const double *mvec, double *b21,
+                          double &Gall) {
+  const MfRules &Rr = P.rules;
+  int degree = P.mesh.degree;
+  double phi2[NLM], S[NLM];
+  for (int j = 0; j < O.nloc; j++) S[j] = 0.0;
+  double W = 0.0;
+  if (O.kind == 1) {
+    double e10 = g[2] - g[0], e11 = g[3] - g[1];
+    double e20 = g[4] - g[0], e21 = g[5] - g[1];
+    double det = e10 * e21 - e11 * e20;
+    for (int q2 = 0; q2 < Rr.nq_tri_out; q2++) {
+      double px = Rr.tri_out_pts[q2 * 2], py = Rr.tri_out_pts[q2 * 2 + 1];
+      double x0 = g[0] + px * e10 + py * e20;
+      double x1 = g[1] + px * e11 + py * e21;
+      double w2q = Rr.tri_out_w[q2] * det;
+      double dx0 = x0 - O.v0[0], dx1 = x1 - O.v0[1];
+      shape_at(1, degree, 2, O.inv[0] * dx0 + O.inv[1] * dx1,
+               O.inv[2] * dx0 + O.inv[3] * dx1, 0.0, phi2);
+      W += w2q;
+      for (int j = 0; j < O.nloc; j++) S[j] += w2q * phi2[j];
+    }
+  } else {
+    double jac = 1.0;
+#pragma unroll
+    for (int k = 0; k < DIM; k++) jac *= 0.5 * (g[DIM + k] - g[k]);
+    for (int q2 = 0; q2 < Rr.nq_box_out; q2++) {
+      double r[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+      for (int k = 0; k < DIM; k++) {
+        double x = g[k] + (Rr.box_out_pts[q2 * DIM + k] + 1.0) * 0.5 *
+                              (g[DIM + k] - g[k]);
+        r[k] = (x - O.lo[k]) / (O.hi[k] - O.lo[k]) * 2.0 - 1.0;
+      }
+      double w2q = Rr.box_out_w[q2] * jac;
+      shape_at(O.kind, degree, DIM, r[0], r[1], r[2], phi2);
+      W += w2q;
+      for (int j = 0; j < O.nloc; j++) S[j] += w2q * phi2[j];
+    }
+  }
+  Gall += P.cde * W;
+  for (int i = 0; i < I.nloc; i++) {
+    double ci = P.cde * mvec[i];
+    for (int j = 0; j < O.nloc; j++) b21[i * NLM + j] -= ci * S[j];
+  }
+}
+
+MF_DEV void scatter_add(const AsmParams &P, const int64_t *rows, int nr,
+                        const int64_t *cols, int nc, const double *blk,
+                        int ld) {
+  for (int i = 0; i < nr; i++) {
+    int64_t r = rows[i];
+    for (int j = 0; j < nc; j++) {
+      int64_t idx = pat_index(P.pat, r, cols[j]);
+      P.vals[idx] += P.scale * blk[i * ld + j];
+    }
+  }
+}
+
+template <int DIM, int NLM>
+__global__ void __launch_bounds__(128)
+    k_generic(AsmParams P) {
+  const MfMesh &M = P.mesh;
+  const MfRules &Rr = P.rules;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  double *G = P.scratch + tid * P.scratch_stride;
+  unsigned long long c_ev = 0, c_pairs = 0, c_up = 0, c_pl = 0, c_dead = 0,
+                     c_full = 0;
+  const int nchild_box = 1 << DIM;
+  for (int64_t t = tid; t < P.n_inner; t += nthreads) {
+    const int64_t m = P.inner[t];
+    Inner I;
+    I.kind = M.elem_kind[m];
+    const bool itri = I.kind == 1;
+    I.nq = itri ? Rr.nq_tri_in : Rr.nq_box_in;
+    I.nloc = itri ? P.nl_tri : P.nl_box;
+    I.pts = itri ? Rr.tri_in_pts : Rr.box_in_pts;
+    I.w = itri ? Rr.tri_in_w : Rr.box_in_w;
+    I.phi = itri ? Rr.phi_tri_in : Rr.phi_box_in;
+#pragma unroll
+    for (int k = 0; k < DIM; k++) {
+      I.lo[k] = M.elem_lo[m * DIM + k];
+      I.hi[k] = M.elem_hi[m * DIM + k];
+    }
+    if (itri) {
+      const double *c = M.elem_coords + (size_t)m * M.nv_max * DIM;
+      I.c0[0] = c[0];
+      I.c0[1] = c[1];
+      I.e1[0] = xsub(c[DIM], c[0]);
+      I.e1[1] = xsub(c[DIM + 1], c[1]);
+      I.e2[0] = xsub(c[2 * DIM], c[0]);
+      I.e2[1] = xsub(c[2 * DIM + 1], c[1]);
+      I.scale_w = I.e1[0] * I.e2[1] - I.e1[1] * I.e2[0];
+    } else {
+      double jac = 1.0;
+#pragma unroll
+      for (int k = 0; k < DIM; k++) jac *= 0.5 * (I.hi[k] - I.lo[k]);
+      I.scale_w = jac;
+    }
+    // m_i = int phi_i over the inner element (plateau shortcut)
+    double mvec[NLM];
+    for (int i = 0; i < I.nloc; i++) {
+      double s = 0.0;
+      for (int q = 0; q < I.nq; q++) s += I.w[q] * I.phi[q * I.nloc + i];
+      mvec[i] = s * I.scale_w;
+    }
+    for (int q = 0; q < I.nq; q++) G[q] = 0.0;
+    double Gall = 0.0;  // plateau contributions common to every q1
+    int cx, cy, cz;
+    cell_coords(M.elem_cell[m], M.ncx, M.ncy, cx, cy, cz);
+    const int R = P.R;
+    const int zlo = DIM == 3 ? max(cz - R, 0) : 0;
+    const int zhi = DIM == 3 ? min(cz + R, M.ncz - 1) : 0;
+    const int64_t *mdofs = M.elem_dofs + (size_t)m * M.nloc_max;
+    for (int z2 = zlo; z2 <= zhi; z2++)
+      for (int y2 = max(cy - R, 0); y2 <= min(cy + R, M.ncy - 1); y2++)
+        for (int x2 = max(cx - R, 0); x2 <= min(cx + R, M.ncx - 1); x2++) {
+          const int64_t c2 = ((int64_t)z2 * M.ncy + y2) * M.ncx + x2;
+          for (int64_t l = M.cell_ptr[c2]; l < M.cell_ptr[c2 + 1]; l++) {
+            if (!P.outer_mask[l]) continue;
+            if (!(elem_gap<DIM>(M.elem_lo, M.elem_hi, l, m) < P.dpe))
+              continue;
+            c_pairs++;
+            Outer O;
+            O.kind = M.elem_kind[l];
+            O.nloc = O.kind == 1 ? P.nl_tri : P.nl_box;
+            const double *lc = M.elem_coords + (size_t)l * M.nv_max * DIM;
+            if (O.kind == 1) {
+              for (int v = 0; v < 3; v++) {
+                O.geo[2 * v] = lc[v * DIM];
+                O.geo[2 * v + 1] = lc[v * DIM + 1];
+              }
+              double e10 = lc[DIM] - lc[0], e11 = lc[DIM + 1] - lc[1];
+              double e20 = lc[2 * DIM] - lc[0], e21 = lc[2 * DIM + 1] - lc[1];
+              double det = e10 * e21 - e11 * e20;
+              O.v0[0] = lc[0];
+              O.v0[1] = lc[1];
+              O.inv[0] = e21 / det;
+              O.inv[1] = -e20 / det;
+              O.inv[2] = -e11 / det;
+              O.inv[3] = e10 / det;
+            } else {
+#pragma unroll
+              for (int k = 0; k < DIM; k++) {
+                O.lo[k] = M.elem_lo[l * DIM + k];
+                O.hi[k] = M.elem_hi[l * DIM + k];
+                O.geo[k] = O.lo[k];
+                O.geo[DIM + k] = O.hi[k];
+              }
+            }
+            double b21[NLM * NLM];
+            for (int i = 0; i < I.nloc * NLM; i++) b21[i] = 0.0;
+            const int nchild = O.kind == 1 ? 4 : nchild_box;
+            // depth-first Algorithm 1 with one geometry per level
+            double geo[kLevels + 1][6];
+            int child[kLevels + 1];
+            for (int u = 0; u < 6; u++) geo[1][u] = O.geo[u];
+            int L = 1;
+            unsigned long long ev = 0;
+            for (;;) {
+              double slo[3], shi[3];
+              sub_bbox<DIM>(O.kind, geo[L], slo, shi);
+              bool split = false, integ = false;
+              if (L < P.L_min) {
+                split = true;
+              } else if (L == P.L_max) {
+                integ = aprx_min_d<DIM>(slo, shi, I.lo, I.hi) < P.dpe;
+              } else if (aprx_max_lt_dme(
+                             P, aprx_max_sq<DIM>(slo, shi, I.lo, I.hi))) {
+                integ = true;
+              } else if (aprx_min_d<DIM>(slo, shi, I.lo, I.hi) < P.dpe) {
+                split = true;
+              }
+              if (integ) {
+                ev++;
+                if (L < P.L_max) {
+                  c_up++;
+                  if (P.shortcuts)
+                    event_plateau<DIM, NLM>(P, O, geo[L], I, mvec, b21, Gall);
+                  else
+                    event_full<DIM, NLM>(P, O, geo[L], I, b21, G);
+                } else if (P.shortcuts &&
+                           box_dead<DIM>(P, slo, shi, I.lo, I.hi)) {
+                  c_dead++;
+                } else if (P.shortcuts &&
+                           aprx_max_lt_dme(P, aprx_max_sq<DIM>(slo, shi, I.lo,
+                                                               I.hi))) {
+                  c_pl++;
+                  event_plateau<DIM, NLM>(P, O, geo[L], I, mvec, b21, Gall);
+                } else {
+                  c_full++;
+                  event_full<DIM, NLM>(P, O, geo[L], I, b21, G);
+                }
+              }
+              if (split) {
+                ++L;
+                child[L] = 0;
+                make_child<DIM>(O.kind, geo[L - 1], 0, geo[L]);
+                continue;
+              }
+              bool done = false;
+              for (;;) {
+                if (L == 1) {
+                  done = true;
+                  break;
+                }
+                if (++child[L] < nchild) {
+                  make_child<DIM>(O.kind, geo[L - 1], child[L], geo[L]);
+                  break;
+                }
+                --L;
+              }
+              if (done) break;
+            }
+            if (ev) {
+              c_ev += ev;
+              scatter_add(P, mdofs, I.nloc, M.elem_dofs + (size_t)l * M.nloc_max,
+                          O.nloc, b21, NLM);
+            }
+          }
+        }
+    // A22 for the whole element: sum_q1 G[q1] w1[q1] PHI1 PHI1^T
+    double b22[NLM * NLM];
+    for (int i = 0; i < I.nloc * NLM; i++) b22[i] = 0.0;
+    bool any = Gall != 0.0;
+    for (int q = 0; q < I.nq; q++) {
+      double s = (G[q] + Gall) * I.w[q] * I.scale_w;
+      if (s == 0.0) continue;
+      any = true;
+      for (int i = 0; i < I.nloc; i++) {
+        double ci = s * I.phi[q * I.nloc + i];
+        for (int j = 0; j < I.nloc; j++)
+          b22[i * NLM + j] += ci * I.phi[q * I.nloc + j];
+      }
+    }
+    if (any) scatter_add(P, mdofs, I.nloc, mdofs, I.nloc, b22, NLM);
+  }
+  unsigned long long *C = P.counters;
+  counter_add(C + MF_CNT_EVENTS, c_ev);
+  counter_add(C + MF_CNT_PAIRS, c_pairs);
+  counter_add(C + MF_CNT_EV_UPPER, c_up);
+  counter_add(C + MF_CNT_EV_PLATEAU, c_pl);
+  counter_add(C + MF_CNT_EV_DEAD, c_dead);
+  counter_add(C + MF_CNT_EV_FULL, c_full);
+}
+
+}  // namespace
+
+// launch helper used by mf_capi.cu
+cudaError_t mf_launch_generic(const AsmParams &P, int grid, int block,
+                              cudaStream_t s) {
+  int dim = P.mesh.dim;
+  int nlm = P.nl_box > P.nl_tri ? P.nl_box : P.nl_tri;
+  if (dim == 2) {
+    if (nlm <= 9)
+      k_generic<2, 9><<<grid, block, 0, s>>>(P);
+    else
+      return cudaErrorInvalidValue;
+  } else {
+    if (nlm <= 8)
+      k_generic<3, 8><<<grid, block, 0, s>>>(P);
+    else if (nlm <= 27)
+      k_generic<3, 27><<<grid, block, 0, s>>>(P);
+    else
+      return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}

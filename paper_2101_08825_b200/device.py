@@ -1,0 +1,115 @@
+"""Device-resident inputs of the assembly kernels.
+
+`DeviceMesh` holds the mesh SoA + DOF map (mesh.py:78-88, fe_space.py:131)
+in HBM and the MfMesh descriptor pointing at it; `DeviceRules` the rule
+and shape tables (assembly.py:333-356); `ColorPlan` the colour-grouped
+inner-element list that makes the scatter race-free: elements whose cells
+have the same (x, y, z) parity and the same triangle proto share no DOF
+(a DOF of cell c lies in [degree*c, degree*(c+1)] per axis), so each
+colour is one atomic-free launch.
+"""
+
+import numpy as np
+
+from . import _native as N
+
+
+def _dev(device):
+    import torch
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device(device)
+
+
+def to_device(arr, device, pinned=True):
+    """numpy -> device tensor through a pinned staging copy."""
+    import torch
+    t = torch.from_numpy(np.ascontiguousarray(arr))
+    if pinned and t.numel() > 0:
+        t = t.pin_memory()
+    return t.to(device, non_blocking=True)
+
+
+class DeviceMesh:
+    """Mesh + FE space arrays in device memory."""
+
+    def __init__(self, mesh, space, device=None):
+        dev = _dev(device)
+        self.device = dev
+        self.dim = mesh.dim
+        flat, cptr = mesh.cell_ptr()
+        nc = mesh.grid_ncells
+        host = {
+            "elem_kind": np.ascontiguousarray(mesh.elem_kind, np.int8),
+            "elem_coords": np.ascontiguousarray(mesh.elem_coords, np.float64),
+            "elem_lo": np.ascontiguousarray(mesh.elem_lo, np.float64),
+            "elem_hi": np.ascontiguousarray(mesh.elem_hi, np.float64),
+            "elem_dofs": np.ascontiguousarray(space.element_dofs, np.int64),
+            "elem_cell": np.ascontiguousarray(flat, np.int32),
+            "cell_ptr": np.ascontiguousarray(cptr, np.int64),
+        }
+        self.h2d_bytes = sum(a.nbytes for a in host.values())
+        self.t = {k: to_device(v, dev) for k, v in host.items()}
+        self.struct = N.MfMesh(
+            dim=mesh.dim, degree=space.degree, n_elem=mesh.n_elements,
+            nv_max=mesh.elem_coords.shape[1],
+            nloc_max=space.element_dofs.shape[1],
+            elem_kind=self.t["elem_kind"].data_ptr(),
+            elem_coords=self.t["elem_coords"].data_ptr(),
+            elem_lo=self.t["elem_lo"].data_ptr(),
+            elem_hi=self.t["elem_hi"].data_ptr(),
+            elem_dofs=self.t["elem_dofs"].data_ptr(),
+            elem_cell=self.t["elem_cell"].data_ptr(),
+            cell_ptr=self.t["cell_ptr"].data_ptr(),
+            ncx=int(nc[0]), ncy=int(nc[1]),
+            ncz=int(nc[2]) if mesh.dim == 3 else 1)
+
+
+class DeviceRules:
+    """Rule/shape tables of a `PrepTables` in device memory."""
+
+    def __init__(self, prep, device=None):
+        dev = _dev(device)
+        names = ["box_out_pts", "box_out_w", "box_in_pts", "box_in_w",
+                 "tri_out_pts", "tri_out_w", "tri_in_pts", "tri_in_w"]
+        host = {n: getattr(prep, n) for n in names}
+        host["phi_box_in"] = prep.PHI_box_in
+        host["phi_tri_in"] = prep.PHI_tri_in
+        host["box_out_x1d"], host["box_out_w1d"] = prep.box_out_1d
+        host["box_in_x1d"], host["box_in_w1d"] = prep.box_in_1d
+        self.t = {k: to_device(np.ascontiguousarray(v, np.float64), dev,
+                               pinned=False) for k, v in host.items()}
+        p = {k: v.data_ptr() for k, v in self.t.items()}
+        self.struct = N.MfRules(
+            nq_box_out=len(prep.box_out_w), nq_box_in=len(prep.box_in_w),
+            nq_tri_out=len(prep.tri_out_w), nq_tri_in=len(prep.tri_in_w),
+            n1d_box_out=len(prep.box_out_1d[0]),
+            n1d_box_in=len(prep.box_in_1d[0]), **p)
+
+
+def color_of(mesh):
+    """Colour id per element: cell parity bits * 2 + proto (< 16)."""
+    c = mesh.elem_cell.astype(np.int64)
+    col = (c[:, 0] & 1) | ((c[:, 1] & 1) << 1)
+    if mesh.dim == 3:
+        col |= (c[:, 2] & 1) << 2
+    return (col * 2 + mesh.elem_proto.astype(np.int64)).astype(np.int64)
+
+
+class ColorPlan:
+    """Inner elements grouped by colour, ascending ids inside a colour."""
+
+    NCOLORS = 16
+
+    def __init__(self, mesh, inner_ids=None, device=None):
+        col = color_of(mesh)
+        ids = (np.arange(mesh.n_elements, dtype=np.int64) if inner_ids is None
+               else np.asarray(inner_ids, dtype=np.int64))
+        order = np.argsort(col[ids], kind="stable")
+        ids = ids[order]
+        counts = np.bincount(col[ids], minlength=self.NCOLORS)
+        self.color_ptr = np.zeros(self.NCOLORS + 1, dtype=np.int64)
+        np.cumsum(counts, out=self.color_ptr[1:])
+        self.inner_sorted = to_device(ids.astype(np.int32), _dev(device))
+        self.n_inner = int(len(ids))
+        self.h2d_bytes = ids.size * 4

@@ -1,0 +1,314 @@
+"""Structured meshes of Omega plus its constraint layer (reference row a3).
+
+Restates `mollifem/mesh.py:75-319` with vectorised construction: the same
+flat SoA arrays (`elem_kind`, `elem_proto`, `elem_region`, `elem_cell`,
+`elem_coords`, `elem_lo`, `elem_hi`), bit-identical coordinates
+(`origin + h*arange`, mesh.py:180-191), the same cell-lex element order
+(tri cells emit the lower then the upper triangle) and the same recursive
+coordinate bisection.  `Mesh.elements` is materialised lazily, so building
+the 474,552-hex R4 mesh takes well under a second instead of the
+reference's per-element Python loop.
+"""
+
+import math
+
+import numpy as np
+
+__all__ = ["BoundingBox", "Element", "Mesh", "PartitionMap", "build_mesh",
+           "refine", "partition_geometric"]
+
+KIND_CODE = {"quad": 0, "tri": 1, "hex": 2}
+KIND_NAME = {0: "quad", 1: "tri", 2: "hex"}
+
+
+class BoundingBox:
+    """Axis-aligned box (lo, hi)."""
+
+    __slots__ = ("lo", "hi")
+
+    def __init__(self, lo, hi):
+        self.lo = np.asarray(lo, dtype=float)
+        self.hi = np.asarray(hi, dtype=float)
+        if np.any(self.lo > self.hi):
+            raise ValueError("box needs lo <= hi componentwise")
+
+    @property
+    def center(self):
+        return 0.5 * (self.lo + self.hi)
+
+    def contains(self, point, tol=0.0):
+        p = np.asarray(point, dtype=float)
+        return bool(np.all(p >= self.lo - tol) and np.all(p <= self.hi + tol))
+
+    def __repr__(self):
+        return f"BoundingBox({self.lo.tolist()}, {self.hi.tolist()})"
+
+
+class Element:
+    """One element: geometry node ids/coords, region tag and bbox."""
+
+    __slots__ = ("id", "kind", "node_ids", "region", "bbox", "coords")
+
+    def __init__(self, eid, kind, node_ids, region, coords):
+        self.id = eid
+        self.kind = kind
+        self.node_ids = node_ids
+        self.region = region
+        self.coords = coords
+        self.bbox = BoundingBox(coords.min(axis=0), coords.max(axis=0))
+
+    def measure(self):
+        if self.kind == "tri":
+            a = self.coords[1] - self.coords[0]
+            b = self.coords[2] - self.coords[0]
+            return 0.5 * abs(a[0] * b[1] - a[1] * b[0])
+        return float(np.prod(self.bbox.hi - self.bbox.lo))
+
+    def __repr__(self):
+        return f"Element({self.id}, {self.kind}, {self.region})"
+
+
+class _LazyElements:
+    """Sequence view that builds `Element` records on demand."""
+
+    def __init__(self, mesh):
+        self._m = mesh
+
+    def __len__(self):
+        return self._m.elem_kind.shape[0]
+
+    def __getitem__(self, i):
+        m = self._m
+        if isinstance(i, slice):
+            return [self[j] for j in range(*i.indices(len(self)))]
+        i = int(i)
+        if i < 0:
+            i += len(self)
+        if not 0 <= i < len(self):
+            raise IndexError(i)
+        k = int(m.elem_kind[i])
+        nv = 3 if k == 1 else m.elem_nodes.shape[1]
+        ids = m.elem_nodes[i, :nv].copy()
+        return Element(i, KIND_NAME[k], ids,
+                       "omega" if m.elem_region[i] == 0 else "gamma",
+                       m.nodes[ids])
+
+    def __iter__(self):
+        for i in range(len(self)):
+            yield self[i]
+
+
+class Mesh:
+    """Structured mesh; see module docstring for the flat arrays."""
+
+    def __init__(self, dim, nodes, elem_nodes, h, omega_bounds, gamma_layers,
+                 kind, layer_width, grid_ncells, grid_origin, arrays):
+        self.dim = dim
+        self.nodes = nodes
+        self.elem_nodes = elem_nodes
+        self.h = h
+        self.omega_bounds = omega_bounds
+        self.gamma_layers = gamma_layers
+        self.kind = kind
+        self.layer_width = layer_width
+        self.grid_ncells = grid_ncells
+        self.grid_origin = grid_origin
+        (self.elem_kind, self.elem_proto, self.elem_region, self.elem_cell,
+         self.elem_coords, self.elem_lo, self.elem_hi) = arrays
+        self.elements = _LazyElements(self)
+
+    @property
+    def n_elements(self):
+        return int(self.elem_kind.shape[0])
+
+    def omega_element_ids(self):
+        return np.nonzero(self.elem_region == 0)[0]
+
+    def domain_bounds(self):
+        lo = np.asarray(self.grid_origin)
+        return BoundingBox(lo, lo + np.asarray(self.grid_ncells) * self.h)
+
+    def cell_flat(self):
+        """Flat cell id per element, x fastest (assembly.py:135-141)."""
+        c = self.elem_cell.astype(np.int64)
+        nc = self.grid_ncells
+        flat = c[:, 1] * nc[0] + c[:, 0]
+        if self.dim == 3:
+            flat += c[:, 2] * (nc[0] * nc[1])
+        return flat.astype(np.int32)
+
+    def cell_ptr(self):
+        """CSR of elements per flat cell (elements are cell-lex ordered)."""
+        flat = self.cell_flat()
+        ncells = int(np.prod(self.grid_ncells))
+        return flat, np.searchsorted(flat, np.arange(ncells + 1)).astype(
+            np.int64)
+
+    def __repr__(self):
+        return (f"Mesh(dim={self.dim}, kind={self.kind}, h={self.h}, "
+                f"elements={self.n_elements}, rings={self.gamma_layers})")
+
+
+class PartitionMap:
+    """Element -> part map with per-part bounding boxes."""
+
+    def __init__(self, n_parts, owner, part_bbox):
+        self.n_parts = n_parts
+        self.owner = owner
+        self.part_bbox = part_bbox
+
+    def owned(self, part):
+        return np.nonzero(self.owner == part)[0]
+
+    def __repr__(self):
+        return f"PartitionMap(n_parts={self.n_parts})"
+
+
+def _as_bounds(omega_bounds, dim):
+    if isinstance(omega_bounds, BoundingBox):
+        lo, hi = omega_bounds.lo, omega_bounds.hi
+    else:
+        arr = np.asarray(omega_bounds, dtype=float)
+        if arr.shape != (dim, 2):
+            raise ValueError(f"omega_bounds must be {dim} (lo, hi) pairs")
+        lo, hi = arr[:, 0], arr[:, 1]
+    if len(lo) != dim:
+        raise ValueError("omega_bounds dimension mismatch")
+    return BoundingBox(lo, hi)
+
+
+def build_mesh(dim, omega_bounds, h, layer_width, kind="quad"):
+    """Omega tiled at pitch h plus ceil(layer_width/h) Gamma rings.
+
+    kind: quad/tri/mixed in 2D, hex in 3D (mesh.py:153-165).
+    """
+    if h <= 0.0:
+        raise ValueError("h must be positive")
+    if layer_width < 0.0:
+        raise ValueError("layer_width must be nonnegative")
+    rings = int(math.ceil(layer_width / h - 1e-9)) if layer_width > 0.0 else 0
+    return _build(dim, omega_bounds, h, rings, kind, layer_width)
+
+
+def _build(dim, omega_bounds, h, rings, kind, layer_width):
+    if dim == 2 and kind not in ("quad", "tri", "mixed"):
+        raise ValueError(f"2D mesh kind must be quad/tri/mixed, got {kind!r}")
+    if dim == 3 and kind != "hex":
+        raise ValueError("3D meshes are hex only")
+    if dim not in (2, 3):
+        raise ValueError("dim must be 2 or 3")
+    box = _as_bounds(omega_bounds, dim)
+    side = box.hi - box.lo
+    n_omega = np.rint(side / h).astype(int)
+    if np.any(n_omega < 1) or np.any(
+            np.abs(n_omega * h - side) > 1e-9 * np.maximum(1.0, side)):
+        raise ValueError(f"omega side lengths {side.tolist()} are not "
+                         f"integer multiples of h={h}")
+    nc = n_omega + 2 * rings
+    origin = box.lo - rings * h
+    nv = nc + 1
+    axes = [origin[k] + h * np.arange(nv[k]) for k in range(dim)]
+    grids = np.meshgrid(*axes[::-1], indexing="ij")      # z/y slowest
+    nodes = np.column_stack([g.ravel() for g in grids[::-1]])
+
+    # per-cell integer coordinates, x fastest
+    cidx = np.indices(tuple(nc[::-1])).reshape(dim, -1)[::-1].T  # (ncell,dim)
+    inside = np.all((cidx >= rings) & (cidx < rings + n_omega), axis=1)
+    region_c = np.where(inside, 0, 1).astype(np.int8)
+
+    def nid(off):
+        g = cidx + np.asarray(off)[None, :]
+        out = g[:, -1].astype(np.int64)
+        for k in range(dim - 2, -1, -1):
+            out = out * nv[k] + g[:, k]
+        return out
+
+    if dim == 3:
+        corners = [((v & 1), (v >> 1) & 1, (v >> 2) & 1) for v in range(8)]
+        en = np.stack([nid(c) for c in corners], axis=1)
+        kinds = np.full(len(cidx), 2, np.int8)
+        protos = np.zeros(len(cidx), np.int8)
+        cells = cidx
+        regions = region_c
+    else:
+        sw, se, nw, ne = (nid((0, 0)), nid((1, 0)), nid((0, 1)),
+                          nid((1, 1)))
+        if kind == "quad":
+            as_quad = np.ones(len(cidx), bool)
+        elif kind == "tri":
+            as_quad = np.zeros(len(cidx), bool)
+        else:
+            as_quad = (cidx[:, 0] + cidx[:, 1]) % 2 == 0
+        nvmax = 4 if as_quad.any() else 3
+        # two slots per cell: slot 0 = quad or lower tri, slot 1 = upper tri
+        slot_nodes = np.zeros((len(cidx), 2, nvmax), np.int64)
+        q = as_quad
+        t = ~as_quad
+        if q.any():
+            slot_nodes[q, 0, :4] = np.stack([sw, se, nw, ne], 1)[q]
+        slot_nodes[t, 0, :3] = np.stack([sw, se, ne], 1)[t]
+        slot_nodes[t, 1, :3] = np.stack([sw, ne, nw], 1)[t]
+        valid = np.stack([np.ones(len(cidx), bool), t], axis=1)
+        sel = valid.ravel()
+        en = slot_nodes.reshape(-1, nvmax)[sel]
+        kinds = np.stack([np.where(q, 0, 1), np.ones(len(cidx), int)],
+                         1).ravel()[sel].astype(np.int8)
+        protos = np.stack([np.zeros(len(cidx), int), np.ones(len(cidx), int)],
+                          1).ravel()[sel].astype(np.int8)
+        cells = np.repeat(cidx, 2, axis=0)[sel]
+        regions = np.repeat(region_c, 2)[sel]
+
+    n_elem = en.shape[0]
+    nvmax = en.shape[1]
+    coords = nodes[en]                                   # (n, nvmax, dim)
+    is_tri = kinds == 1
+    if is_tri.any() and nvmax > 3:
+        coords[is_tri, 3:, :] = 0.0
+    lo = np.where(is_tri[:, None], coords[:, :3, :].min(axis=1),
+                  coords.min(axis=1))
+    hi = np.where(is_tri[:, None], coords[:, :3, :].max(axis=1),
+                  coords.max(axis=1))
+    arrays = (kinds, protos, regions.astype(np.int8),
+              cells.astype(np.int32), np.ascontiguousarray(coords),
+              np.ascontiguousarray(lo), np.ascontiguousarray(hi))
+    return Mesh(dim, nodes, en, h, box, rings, kind, layer_width,
+                tuple(int(x) for x in nc), origin, arrays)
+
+
+def refine(mesh):
+    """Uniform refinement: h halves, ring count doubles."""
+    return _build(mesh.dim, mesh.omega_bounds, mesh.h / 2.0,
+                  mesh.gamma_layers * 2, mesh.kind, mesh.layer_width)
+
+
+def partition_geometric(mesh, n_parts):
+    """Recursive coordinate bisection of element centroids (mesh.py:284-319).
+
+    Widest centroid axis, stable median split, proportional counts.
+    """
+    if n_parts < 1:
+        raise ValueError("n_parts must be >= 1")
+    n_elem = mesh.n_elements
+    if n_parts > n_elem:
+        raise ValueError("n_parts exceeds element count")
+    cen = 0.5 * (mesh.elem_lo + mesh.elem_hi)
+    owner = np.empty(n_elem, dtype=np.int32)
+    stack = [(np.arange(n_elem), n_parts, 0)]
+    while stack:
+        ids, parts, first = stack.pop()
+        if parts == 1:
+            owner[ids] = first
+            continue
+        n1 = (parts + 1) // 2
+        count1 = (len(ids) * n1) // parts
+        sub = cen[ids]
+        axis = int(np.argmax(sub.max(axis=0) - sub.min(axis=0)))
+        order = np.argsort(sub[:, axis], kind="stable")
+        stack.append((ids[order[count1:]], parts - n1, first + n1))
+        stack.append((ids[order[:count1]], n1, first))
+    boxes = []
+    for p in range(n_parts):
+        ids = np.nonzero(owner == p)[0]
+        boxes.append(BoundingBox(mesh.elem_lo[ids].min(axis=0),
+                                 mesh.elem_hi[ids].max(axis=0)))
+    return PartitionMap(n_parts, owner, boxes)

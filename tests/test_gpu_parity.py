@@ -1,0 +1,128 @@
+"""GPU assembly vs the reference (golden vectors) and the pinned oracle.
+
+Bar (BASELINE.json north_star): identical sparsity pattern, bit-exact
+neighbour lists, identical event counts, matrix within 1e-10 relative
+Frobenius norm.  Everything here calls the product path through the C-ABI
+(paper_2101_08825_b200 -> libmollifem_b200.so).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import Golden, golden_names, rel_frob
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+def _assemble(name, flags=0):
+    from paper_2101_08825_b200 import assemble
+    g = Golden(name)
+    mesh, space, kp, cfg = g.build()
+    return g, assemble(mesh, space, kp, cfg, flags=flags)
+
+
+@pytest.mark.parametrize("name", golden_names())
+@pytest.mark.parametrize("flags", [0, 1, 2], ids=["auto", "generic",
+                                                   "noshortcut"])
+def test_assemble_matches_reference(name, flags):
+    g, A = _assemble(name, flags)
+    assert np.array_equal(A.rowptr, g["rowptr"]) and A.K == int(g["K"])
+    assert A.events == int(g["events"])
+    err = rel_frob(A.vals, g["vals"])
+    print(f"{name} flags={flags} relF={err:.3e} events={A.events}")
+    assert err <= TOL
+    ref_asym = float(g["asym"])
+    assert abs(A.presym_asymmetry - ref_asym) <= 1e-8 * max(
+        ref_asym, np.abs(g["vals"]).max())
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_neighbor_lists_bit_exact(name):
+    from paper_2101_08825_b200 import neighbor_sets
+    g = Golden(name)
+    mesh, space, kp, cfg = g.build()
+    s = neighbor_sets(mesh, kp)
+    assert np.array_equal(s.ptr, g["cand_ptr"])
+    assert np.array_equal(s.ids, g["cand_ids"])
+
+
+def test_candidates_subset_and_mask():
+    from paper_2101_08825_b200.assembly import candidates
+    import oracle
+    g = Golden("hex_q1_gl3")
+    mesh, space, kp, cfg = g.build()
+    rng = np.random.default_rng(3)
+    outer = np.sort(rng.choice(mesh.n_elements, 57, replace=False))
+    mask = (rng.random(mesh.n_elements) < 0.4).astype(np.uint8)
+    p1, i1 = candidates(mesh, kp.delta + kp.eps, outer, mask)
+    p2, i2 = oracle.candidates(mesh, kp.delta + kp.eps, outer, mask)
+    assert np.array_equal(p1, p2) and np.array_equal(i1, i2)
+    # empty outer list
+    p, i = candidates(mesh, kp.delta + kp.eps, np.zeros(0, np.int64), mask)
+    assert p.tolist() == [0] and i.size == 0
+
+
+def test_partitioned_run_matches_reference():
+    """_run_general with outer subset + inner mask (parallel.py:161-171)."""
+    from paper_2101_08825_b200.assembly import AssemblyContext
+    for name in ("tri_p1_lmax3", "hex_q1_gl3"):
+        g = Golden(name)
+        mesh, space, kp, cfg = g.build()
+        ctx = AssemblyContext(mesh, space, kp, cfg)
+        A = ctx.new_matrix()
+        om = np.zeros(mesh.n_elements, np.uint8)
+        om[g["part_outer"]] = 1
+        cnt = ctx.run(A, outer_mask=om, inner_ids=g["part_owned"], scale=1.0)
+        assert int(cnt[0].item()) == int(g["part_events"])
+        assert rel_frob(A.vals, g["part_vals"]) <= TOL
+
+
+def test_deterministic_bitwise():
+    _, A = _assemble("hex_q1_gl3")
+    _, B = _assemble("hex_q1_gl3")
+    assert np.array_equal(A.vals, B.vals)
+
+
+def test_matrix_methods_match_oracle():
+    import oracle
+    g, A = _assemble("quad_q2_lmax2")
+    H = oracle.HostPattern_from(A) if hasattr(oracle, "HostPattern_from") \
+        else None
+    x = np.random.default_rng(1).standard_normal(A.n)
+    y = A.matvec(x)
+    from paper_2101_08825_b200.assembly import HostPattern
+    mesh, space, kp, cfg = g.build()
+    R = HostPattern.for_space(mesh, space, kp, cfg)
+    R.vals = A.vals.copy()
+    yr = oracle.matvec(R, x)
+    assert np.allclose(y, yr, rtol=0, atol=1e-12 * np.abs(yr).max())
+    assert np.array_equal(A.diag(), oracle.diag(R))
+    assert A.asymmetry_inf() == pytest.approx(oracle.asymmetry_inf(R),
+                                              rel=1e-12)
+    S = A.to_scipy()
+    assert np.allclose(S @ x, yr, rtol=0, atol=1e-12 * np.abs(yr).max())
+    assert A.norm_inf() == pytest.approx(np.abs(S).sum(axis=1).max(),
+                                         rel=1e-12)
+    A.symmetrize_()
+    oracle.symmetrize(R)
+    assert np.array_equal(A.vals, R.vals)
+    assert A.asymmetry_inf() <= 1e-14 * A.norm_inf()
+    del H
+
+
+def test_r1_full_against_oracle():
+    """BASELINE config #1 stand-in R1 at full size."""
+    import oracle
+    from paper_2101_08825_b200 import (AssemblyConfig, FESpace,
+                                       KernelParams, assemble, build_mesh)
+    h = 1 / 32
+    kp = KernelParams(2, 0.1, h / 2)
+    mesh = build_mesh(2, ((0, 1), (0, 1)), h, kp.delta + kp.eps, "tri")
+    space = FESpace(mesh, 1)
+    cfg = AssemblyConfig(L_max=3, strategy="general")
+    A = assemble(mesh, space, kp, cfg)
+    R = oracle.assemble_general(mesh, space, kp, cfg)
+    assert A.events == R.events == 5800432
+    assert rel_frob(A.vals, R.vals) <= TOL
