@@ -1,0 +1,489 @@
+"""Benchmark: interacting element pairs/s of the nonlocal stiffness assembly.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config R4]
+                    [--impl ours|reference]
+
+Metric (BASELINE.json): interacting element-pairs/sec and full assembly
+time, FP64 roofline fraction.  A *pair* is one (outer l, inner m) entry of
+the reference candidate lists (`_candidates`, assembly.py:157-175), the
+numerator for both the GPU and the CPU; a *step* is one full assembly of
+A = 2(A21 + A22) for the workload.
+
+  value  inputs resident in HBM: zero vals, mf_general_core over all
+         colours (neighbour search fused), asymmetry diagnostic.
+  e2e    the public API `assemble(mesh, space, kernel, config)` from host
+         arrays to a populated host SparseMatrix: mesh/DOF upload, the
+         same kernels, D2H of the 8-byte values.
+
+Default workload R4 = BASELINE config #4 stand-in (3D hex Q1, 64^3 cells,
+delta=0.1, eps=h/2, kappa=2, GL3, L_max=2).  Multi-GPU:
+inner elements are split into z-slabs balanced by pair count, one per rank;
+each rank assembles the rows its slab owns (no data-path collective; the
+slab partial matrices are exchanged only by the row-block gather of
+`parallel.py`, outside the timed kernel region).
+
+The CPU leg (cpu_baseline / --impl reference) times the oracle
+(oracle/mf_oracle.c, the C restatement of the reference numba cores) on a
+seeded sample of outer elements with all host threads.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (dim, omega, h, delta, eps, kappa, kind, L_max, rule)
+    "R1": (2, ((0.0, 1.0),) * 2, 1 / 32, 0.1, 1 / 64, 1.0, "tri", 3,
+           "default"),
+    "R3-2h": (2, ((0.0, 1.0),) * 2, 1 / 512, 2 / 512, 1 / 1024, 1.0, "tri",
+              3, "default"),
+    "R3-4h": (2, ((0.0, 1.0),) * 2, 1 / 512, 4 / 512, 1 / 1024, 1.0, "tri",
+              3, "default"),
+    "R3-8h": (2, ((0.0, 1.0),) * 2, 1 / 512, 8 / 512, 1 / 1024, 1.0, "tri",
+              3, "default"),
+    "R3-16h": (2, ((0.0, 1.0),) * 2, 1 / 512, 16 / 512, 1 / 1024, 1.0, "tri",
+               3, "default"),
+    "R4": (3, ((0.0, 1.0),) * 3, 1 / 64, 0.1, 1 / 128, 2.0, "hex", 2,
+           "default"),
+    "R4-gauss2": (3, ((0.0, 1.0),) * 3, 1 / 64, 0.1, 1 / 128, 2.0, "hex", 2,
+                  "gauss2"),
+    "R4-small": (3, ((0.0, 0.25),) * 3, 1 / 64, 0.1, 1 / 128, 2.0, "hex", 2,
+                 "default"),
+    "R5": (3, ((0.0, 1.0),) * 3, 1 / 128, 4 / 128, 1 / 512, 2.0, "hex", 2,
+           "default"),
+}
+
+METRIC = "interacting element-pairs/sec (full nonlocal stiffness assembly)"
+
+
+def build_problem(name):
+    from paper_2101_08825_b200 import (AssemblyConfig, FESpace, KernelParams,
+                                       build_mesh)
+    dim, om, h, delta, eps, kappa, kind, lmax, rule = CONFIGS[name]
+    kp = KernelParams(dim, delta, eps, kappa)
+    mesh = build_mesh(dim, om, h, delta + eps, kind)
+    space = FESpace(mesh, 1)
+    cfg = AssemblyConfig(L_max=lmax, outer_rule=rule, inner_rule=rule,
+                         strategy="general")
+    return mesh, space, kp, cfg
+
+
+def config_json(name, mesh, space, n_gpus, slab_info=None):
+    dim, om, h, delta, eps, kappa, kind, lmax, rule = CONFIGS[name]
+    d = {"workload": name, "dim": dim, "mesh": f"{kind} structured",
+         "cells": list(mesh.grid_ncells), "elements": mesh.n_elements,
+         "n_dofs": space.n_dofs, "fe_degree": 1, "h": h, "delta": delta,
+         "eps": eps, "kappa": kappa, "L_max": lmax,
+         "rule": "dunavant7" if kind == "tri" else rule,
+         "parallelism": f"z-slab x{n_gpus}" if n_gpus > 1 else "single",
+         "l2": "value array > L2 (rewritten every step)"}
+    if slab_info:
+        d.update(slab_info)
+    return d
+
+
+# --------------------------------------------------------------------------
+# clocks sampling during the timed region
+
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,"
+         "clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}",
+                 f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": mx, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+# --------------------------------------------------------------------------
+# flop model: executed arithmetic of the kernels
+
+def flop_model(name, counters):
+    """(executed_flops, canonical_flops) for one assembly.
+
+    canonical = SURVEY.md 8(d) (reference rank-1 form, every event);
+    executed  = what mf_hex.cu / mf_2d.cu actually issue per event class
+    (sum-factorised full events, rank-1 plateau events, dead events 0),
+    counting mul/add/sub as 1 and FMA as 2, sqrt/div/shell polynomial
+    not counted (same convention as the canonical count)."""
+    from paper_2101_08825_b200 import _native as N
+    dim = CONFIGS[name][0]
+    ev = int(counters[N.CNT_EVENTS])
+    pairs = int(counters[N.CNT_PAIRS])
+    full = int(counters[N.CNT_EV_FULL])
+    plat = int(counters[N.CNT_EV_PLATEAU]) + int(counters[N.CNT_EV_UPPER])
+    rule = CONFIGS[name][8]
+    if dim == 3:
+        no = ni = 2 if rule == "gauss2" else 3
+        nq1, nq2, nl = ni ** 3, no ** 3, 8
+        canon_ev = nq2 * nq1 * (3 * dim - 1 + 3) + 2 * nq2 * nq1 * nl \
+            + 2 * nq2 * nl * nl
+        canon_pair = 2 * nq1 * nl * nl
+        # per lane: sq (2*3NO), sxy (NO^2), d2 (NO^3), x-contraction
+        # (2 FMA per point), y (4*NO FMA per c), z (8 FMA per c)
+        lane = 6 * no + no * no + no ** 3 + 4 * no ** 3 + 8 * no * no \
+            + 16 * no
+        f_full = nq1 * lane + 3 * no * 8
+        f_plat = 3 * no * 8 + 6 * no + 16
+        f_pair = 2 * 2 * nq1 * 64 + 8 * nq1
+    else:
+        nq1 = nq2 = 7
+        nl = 3
+        canon_ev = nq2 * nq1 * (3 * dim - 1 + 3) + 2 * nq2 * nq1 * nl \
+            + 2 * nq2 * nl * nl
+        canon_pair = 2 * nq1 * nl * nl
+        # per point pair: 2 sub, 2 mul, 1 add, 3 FMA; per q2: ~14
+        f_full = nq2 * (nq1 * (5 + 6) + 14)
+        f_plat = nq2 * 16
+        f_pair = 2 * nl * nl * nq1 + nq1 * nl
+    executed = full * f_full + plat * f_plat + pairs * f_pair
+    canonical = ev * canon_ev + pairs * canon_pair
+    return executed, canonical
+
+
+def fp64_peak(device):
+    """Measured sustained DFMA rate (TF/s) with mf_fp64_probe."""
+    import torch
+    from paper_2101_08825_b200 import _native as N
+    L = N.lib()
+    out = torch.zeros(1, dtype=torch.float64, device=device)
+    blocks, threads, iters = 148 * 8, 256, 40000
+    st = N.stream_ptr()
+    N.check(L.mf_fp64_probe(N.ptr(out), iters, blocks, threads, st), "probe")
+    best = 0.0
+    for _ in range(3):
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record()
+        N.check(L.mf_fp64_probe(N.ptr(out), iters, blocks, threads, st),
+                "probe")
+        e.record()
+        e.synchronize()
+        ms = s.elapsed_time(e)
+        best = max(best, L.mf_fp64_probe_flops(iters, blocks, threads) /
+                   (ms * 1e-3) / 1e12)
+    return best
+
+
+# --------------------------------------------------------------------------
+# CPU leg (oracle port on the host cores)
+
+def cpu_sample(name, mesh, space, kp, cfg, budget_s=20.0, seed=0):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+    from paper_2101_08825_b200.assembly import HostPattern
+    oracle.build()
+    threads = os.cpu_count() or 1
+    rng = np.random.default_rng(seed)
+    n = mesh.n_elements
+    A = HostPattern.for_space(mesh, space, kp, cfg)
+    private = A.nnz * 8 * threads < 8e9
+    # calibrate on a small sample, then size the timed one to the budget
+    probe = np.sort(rng.choice(n, min(n, 4 * threads), replace=False))
+    p_ptr, _ = oracle.candidates(mesh, kp.delta + kp.eps, probe,
+                                 np.ones(n, np.uint8))
+    _, dt = oracle.run_general_threads(mesh, space, kp, cfg, A, probe,
+                                       threads, private=False, blk=1)
+    rate = max(p_ptr[-1] / max(dt, 1e-6), 1.0)
+    want_pairs = rate * budget_s
+    per_el = max(p_ptr[-1] / len(probe), 1.0)
+    k = int(min(n, max(threads, want_pairs / per_el)))
+    sample = np.sort(rng.choice(n, k, replace=False))
+    ptr, _ = oracle.candidates(mesh, kp.delta + kp.eps, sample,
+                               np.ones(n, np.uint8))
+    A.vals[:] = 0.0
+    ev, dt = oracle.run_general_threads(mesh, space, kp, cfg, A, sample,
+                                        threads, private=private, blk=1)
+    pairs = int(ptr[-1])
+    return {"value": pairs / dt, "unit": "pairs/s", "cores": threads,
+            "kind": "port", "seconds": dt,
+            "sample": (f"{k} seeded outer elements (rng 0) of {name} "
+                       f"= {pairs} pairs, {ev} events, "
+                       f"{'private' if private else 'shared'} value "
+                       "buffers, oracle/mf_oracle.c (C restatement of "
+                       "_general_core, no FMA) on all host threads")}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    name = args.config
+    mesh, space, kp, cfg = build_problem(name)
+    n = mesh.n_elements
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+    ptr, _ = oracle.candidates(mesh, kp.delta + kp.eps, np.arange(n),
+                               np.ones(n, np.uint8))
+    total_pairs = int(ptr[-1])
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_sample(name, mesh, space, kp, cfg, budget_s=args.cpu_budget,
+                       seed=i)
+        if i >= args.warmup:
+            vals.append(r)
+    v = statistics.median(x["value"] for x in vals)
+    line = {"metric": METRIC, "value": v, "unit": "pairs/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_pairs / v * 1e3,
+            "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": config_json(name, mesh, space, 1),
+            "cpu_baseline": {"value": v, "unit": "pairs/s",
+                             "cores": vals[0]["cores"], "kind": "port",
+                             "sample": vals[0]["sample"]},
+            "e2e": {"value": v, "unit": "pairs/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "note": ("ms_per_step = projected full-assembly time at the "
+                     "sampled rate")}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------
+# GPU leg
+
+def slab_inner_ids(mesh, rank, world, pairs_per_elem):
+    """z-slab (y-slab in 2D) of inner elements balanced by pair count."""
+    axis = mesh.dim - 1
+    layer = mesh.elem_cell[:, axis]
+    nl = int(layer.max()) + 1
+    w = np.bincount(layer, weights=pairs_per_elem, minlength=nl)
+    cum = np.cumsum(w) / w.sum()
+    cuts = [0] + [int(np.searchsorted(cum, (r + 1) / world, side="left")) + 1
+                  for r in range(world - 1)] + [nl]
+    lo, hi = cuts[rank], cuts[rank + 1]
+    return np.nonzero((layer >= lo) & (layer < hi))[0], (lo, hi)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2101_08825_b200 import _native as N
+    from paper_2101_08825_b200 import assemble
+    from paper_2101_08825_b200.assembly import AssemblyContext
+    from paper_2101_08825_b200.device import ColorPlan
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    name = args.config
+    mesh, space, kp, cfg = build_problem(name)
+    ctx = AssemblyContext(mesh, space, kp, cfg, dev)
+    A = ctx.new_matrix()
+    n = mesh.n_elements
+    slab = None
+    if world > 1:
+        # per-element pair counts (GPU neighbour search) for balancing
+        from paper_2101_08825_b200.assembly import candidates
+        ptr, _ = candidates(mesh, kp.delta + kp.eps, np.arange(n),
+                            np.ones(n, np.uint8), dmesh=ctx.dmesh)
+        inner, (zlo, zhi) = slab_inner_ids(mesh, rank, world, np.diff(ptr))
+        slab = {"slab_layers": [zlo, zhi]}
+    else:
+        inner = None
+    plan = ColorPlan(mesh, inner, dev)
+    counters = torch.zeros(N.MF_NCOUNTERS, dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        A._dvals.zero_()
+        counters.zero_()
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        ctx.run(A, plan=plan, counters=counters)
+        e.record(stream)
+        ctx.finish(A, counters)
+        return s, e
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    kern_ms = []
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        evs = [step() for _ in range(args.steps)]
+        t1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = t0.elapsed_time(t1) / args.steps
+    kern_ms = [s.elapsed_time(e) for s, e in evs]
+    cnt = A.counters
+    pairs = int(cnt[N.CNT_PAIRS])
+    if world > 1:
+        t = torch.tensor([ms, float(pairs)], dtype=torch.float64, device=dev)
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = t.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        ms_all, pairs_all = float(mx[0]), int(sm[1])
+    else:
+        ms_all, pairs_all = ms, pairs
+    value = pairs_all / (ms_all * 1e-3)
+
+    # ---- end to end through the public API (host in, host out) --------
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        for _ in range(1):
+            B = assemble(mesh, space, kp, cfg, device=dev)
+        del B
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        e2e_steps = max(1, min(args.steps, args.e2e_steps))
+        for _ in range(e2e_steps):
+            B = assemble(mesh, space, kp, cfg, device=dev)
+            _ = B.vals[-1]
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t) / e2e_steps
+        h2d = ctx.h2d_bytes + plan.h2d_bytes
+        e2e = {"value": pairs_all / e2e_s, "unit": "pairs/s",
+               "seconds_per_assembly": e2e_s,
+               "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(B.nnz * 8 + 8 * N.MF_NCOUNTERS)}
+        del B
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    peak = fp64_peak(dev)
+    executed, canonical = flop_model(name, cnt)
+    kms = statistics.mean(kern_ms)
+    achieved = executed / (kms * 1e-3) / 1e12
+    prof = load_traffic(name)
+    line = {
+        "metric": METRIC, "value": value, "unit": "pairs/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_all, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (structured mesh, reference-realisable stand-in)",
+        "config": config_json(name, mesh, space, world, slab),
+        "events": int(cnt[N.CNT_EVENTS]), "pairs": pairs_all,
+        "event_classes": {"upper_plateau": int(cnt[N.CNT_EV_UPPER]),
+                          "lmax_plateau": int(cnt[N.CNT_EV_PLATEAU]),
+                          "lmax_dead": int(cnt[N.CNT_EV_DEAD]),
+                          "lmax_full": int(cnt[N.CNT_EV_FULL])},
+        "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak,
+                     "unit": "TFLOP/s", "frac": achieved / peak,
+                     "traffic": prof,
+                     "peak_source": "measured DFMA probe (mf_fp64_probe) "
+                                    "in this run",
+                     "kernel_ms": kms,
+                     "executed_flops": executed,
+                     "canonical_flops": canonical,
+                     "canonical_tflops_equiv": canonical / (kms * 1e-3)
+                     / 1e12},
+        "gpu_launches": int(args.steps * (np.count_nonzero(
+            np.diff(plan.color_ptr)) + 1)),
+        "clocks": clk.summary(),
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_sample(name, mesh, space, kp, cfg,
+                                          budget_s=args.cpu_budget)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def load_traffic(name):
+    """dram bytes per launch of the dominant kernel from profiles/."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(name)
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="R4", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -47,6 +47,7 @@ typedef struct MfMesh {
   const int32_t *elem_cell; /* (n) flat cell id, x fastest (assembly.py:135) */
   const int64_t *cell_ptr;  /* (ncells+1) elements per cell, cell-lex order */
   int32_t ncx, ncy, ncz;    /* cell grid (ncz = 1 in 2D) */
+  int32_t kinds_present;    /* bit k set if some element has kind k */
 } MfMesh;
 
 /* Reference-element rules and inner shape tables (assembly.py:333-356).

@@ -25,7 +25,8 @@ class MfMesh(C.Structure):
                 ("elem_coords", C.c_void_p), ("elem_lo", C.c_void_p),
                 ("elem_hi", C.c_void_p), ("elem_dofs", C.c_void_p),
                 ("elem_cell", C.c_void_p), ("cell_ptr", C.c_void_p),
-                ("ncx", C.c_int32), ("ncy", C.c_int32), ("ncz", C.c_int32)]
+                ("ncx", C.c_int32), ("ncy", C.c_int32), ("ncz", C.c_int32),
+                ("kinds_present", C.c_int32)]
 
 
 class MfRules(C.Structure):

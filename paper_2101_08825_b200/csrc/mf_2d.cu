@@ -1,0 +1,526 @@
+// mf_2d.cu -- specialised adaptive assembly for pure 2D meshes of degree 1.
+//
+// Covers BASELINE config #1/#3 stand-ins: right
+// triangle P1 with the Dunavant-7 rule (quadrature.py:141-142), and quad Q1
+// with tensor Gauss/Lobatto rules of <= 4 (outer) / 3 (inner) points per
+// axis; L_max <= 6.
+//
+// One thread per INNER element m of the current colour.  A 2D event is
+// small (49 point pairs for triangles), so a whole pair fits one thread:
+// the inner points y_q1, the per-pair accumulators
+//   V[q1][j] = sum_events sum_q2 gamma(x_q2, y_q1) w_q2 phi_j(x_q2)
+// and the element-level G[q1] = sum_pairs sum_j V[q1][j] live in registers.
+// The partner loop walks the full, unclipped (2R+1)^2 stencil in the same
+// order in every thread; same-colour elements handled by one warp have the
+// same proto and nearby cells, so they visit partners at identical offsets
+// and take identical Algorithm-1 paths (translation invariance), keeping
+// the warp converged.  Algorithm 1 is the reference's depth-first walk
+// (_pair_blocks, _kernels.py:184-313) with one geometry per level and the
+// reference's midpoint arithmetic; L_max events are split into dead /
+// plateau / full exactly as in mf_hex.cu.
+#include "mf_common.cuh"
+
+namespace {
+
+constexpr int kMaxLevels = 6;
+
+template <int KIND>
+struct Cfg;
+template <>
+struct Cfg<1> {  // triangle P1
+  static constexpr int NL = 3;
+  static constexpr int NCHILD = 4;
+};
+template <>
+struct Cfg<0> {  // quad Q1
+  static constexpr int NL = 4;
+  static constexpr int NCHILD = 4;
+};
+
+// sub-cell bbox (_kernels.py:214-222)
+template <int KIND>
+MF_DEV void sub_bbox(const double *g, double *lo, double *hi) {
+  if (KIND == 1) {
+    lo[0] = pmin(g[0], pmin(g[2], g[4]));
+    hi[0] = pmax(g[0], pmax(g[2], g[4]));
+    lo[1] = pmin(g[1], pmin(g[3], g[5]));
+    hi[1] = pmax(g[1], pmax(g[3], g[5]));
+  } else {
+    lo[0] = g[0];
+    lo[1] = g[1];
+    hi[0] = g[2];
+    hi[1] = g[3];
+  }
+}
+
+template <int KIND>
+MF_DEV void make_child(const double *g, int b, double *c) {
+  if (KIND == 1) {
+    const double m010 = xmul(0.5, xadd(g[0], g[2]));
+    const double m011 = xmul(0.5, xadd(g[1], g[3]));
+    const double m120 = xmul(0.5, xadd(g[2], g[4]));
+    const double m121 = xmul(0.5, xadd(g[3], g[5]));
+    const double m200 = xmul(0.5, xadd(g[4], g[0]));
+    const double m201 = xmul(0.5, xadd(g[5], g[1]));
+    switch (b) {
+      case 0:
+        c[0] = g[0]; c[1] = g[1]; c[2] = m010; c[3] = m011; c[4] = m200;
+        c[5] = m201;
+        break;
+      case 1:
+        c[0] = m010; c[1] = m011; c[2] = g[2]; c[3] = g[3]; c[4] = m120;
+        c[5] = m121;
+        break;
+      case 2:
+        c[0] = m200; c[1] = m201; c[2] = m120; c[3] = m121; c[4] = g[4];
+        c[5] = g[5];
+        break;
+      default:
+        c[0] = m010; c[1] = m011; c[2] = m120; c[3] = m121; c[4] = m200;
+        c[5] = m201;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+      const double lo = g[k], hi = g[2 + k];
+      const double mid = xmul(0.5, xadd(lo, hi));
+      if ((b >> k) & 1) {
+        c[k] = mid;
+        c[2 + k] = hi;
+      } else {
+        c[k] = lo;
+        c[2 + k] = mid;
+      }
+    }
+    c[4] = 0.0;
+    c[5] = 0.0;
+  }
+}
+
+struct OuterTri {
+  double v0[2], inv[4];
+};
+struct OuterBox {
+  double lo[2], inv[2];
+};
+
+// ---- triangle events (Dunavant outer rule in shared memory) ----
+template <int NQ1>
+MF_DEV void tri_full(const AsmParams &P, const double *g, const OuterTri &O,
+                     const double (*y)[2], const double *s_pts,
+                     const double *s_w, double (*V)[3]) {
+  const double e10 = xsub(g[2], g[0]), e11 = xsub(g[3], g[1]);
+  const double e20 = xsub(g[4], g[0]), e21 = xsub(g[5], g[1]);
+  const double det = e10 * e21 - e11 * e20;
+  const double f = det * P.cde * (1.0 / 256.0);
+#pragma unroll 1
+  for (int q2 = 0; q2 < 7; q2++) {
+    const double px = s_pts[2 * q2], py = s_pts[2 * q2 + 1];
+    const double x0 = xadd(xadd(g[0], xmul(px, e10)), xmul(py, e20));
+    const double x1 = xadd(xadd(g[1], xmul(px, e11)), xmul(py, e21));
+    const double w2 = s_w[q2] * f;
+    const double dx0 = x0 - O.v0[0], dx1 = x1 - O.v0[1];
+    const double rx = O.inv[0] * dx0 + O.inv[1] * dx1;
+    const double ry = O.inv[2] * dx0 + O.inv[3] * dx1;
+    const double p1 = rx * w2, p2 = ry * w2, p0 = w2 - p1 - p2;
+#pragma unroll
+    for (int q1 = 0; q1 < NQ1; q1++) {
+      const double dx = xsub(x0, y[q1][0]), dy = xsub(x1, y[q1][1]);
+      const double d2 = xadd(xmul(dx, dx), xmul(dy, dy));
+      double mu = (d2 <= P.dm2) ? 256.0 : 0.0;
+      if (d2 > P.dm2 && d2 < P.dp2) mu = xi_shell_256(P, d2);
+      V[q1][0] = fma(mu, p0, V[q1][0]);
+      V[q1][1] = fma(mu, p1, V[q1][1]);
+      V[q1][2] = fma(mu, p2, V[q1][2]);
+    }
+  }
+}
+
+MF_DEV void tri_plateau(const AsmParams &P, const double *g,
+                        const OuterTri &O, const double *s_pts,
+                        const double *s_w, double *SP) {
+  const double e10 = g[2] - g[0], e11 = g[3] - g[1];
+  const double e20 = g[4] - g[0], e21 = g[5] - g[1];
+  const double det = e10 * e21 - e11 * e20;
+  const double f = det * P.cde;
+#pragma unroll 1
+  for (int q2 = 0; q2 < 7; q2++) {
+    const double px = s_pts[2 * q2], py = s_pts[2 * q2 + 1];
+    const double x0 = g[0] + px * e10 + py * e20;
+    const double x1 = g[1] + px * e11 + py * e21;
+    const double w2 = s_w[q2] * f;
+    const double dx0 = x0 - O.v0[0], dx1 = x1 - O.v0[1];
+    const double rx = O.inv[0] * dx0 + O.inv[1] * dx1;
+    const double ry = O.inv[2] * dx0 + O.inv[3] * dx1;
+    SP[0] += w2 * (1.0 - rx - ry);
+    SP[1] += w2 * rx;
+    SP[2] += w2 * ry;
+  }
+}
+
+// ---- quad events (tensor outer rule, sum-factorised) ----
+template <int NO>
+MF_DEV void box_axes(const AsmParams &P, const double *g, const OuterBox &O,
+                     const double *s_t, const double *s_w, double X[2][NO],
+                     double sh[2][2][NO]) {
+  const double jac = (0.5 * (g[2] - g[0])) * (0.5 * (g[3] - g[1]));
+  const double f0 = P.cde * jac * (1.0 / 256.0);
+#pragma unroll
+  for (int k = 0; k < 2; k++) {
+    const double wk = xsub(g[2 + k], g[k]);
+#pragma unroll
+    for (int a = 0; a < NO; a++) {
+      const double x = xadd(g[k], xmul(s_t[a], wk));
+      X[k][a] = x;
+      const double s1 = (x - O.lo[k]) * O.inv[k];
+      const double wa = s_w[a] * (k == 0 ? f0 : 1.0);
+      sh[k][0][a] = (1.0 - s1) * wa;
+      sh[k][1][a] = s1 * wa;
+    }
+  }
+}
+
+template <int NO, int NQ1>
+MF_DEV void quad_full(const AsmParams &P, const double *g, const OuterBox &O,
+                      const double (*y)[2], const double *s_t,
+                      const double *s_w, double (*V)[4]) {
+  double X[2][NO], sh[2][2][NO];
+  box_axes<NO>(P, g, O, s_t, s_w, X, sh);
+#pragma unroll 1
+  for (int q1 = 0; q1 < NQ1; q1++) {
+    double sqx[NO], sqy[NO];
+#pragma unroll
+    for (int a = 0; a < NO; a++) {
+      const double dx = xsub(X[0][a], y[q1][0]);
+      const double dy = xsub(X[1][a], y[q1][1]);
+      sqx[a] = xmul(dx, dx);
+      sqy[a] = xmul(dy, dy);
+    }
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+#pragma unroll
+    for (int b = 0; b < NO; b++) {
+      double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+      for (int a = 0; a < NO; a++) {
+        const double d2 = xadd(sqx[a], sqy[b]);
+        double mu = (d2 <= P.dm2) ? 256.0 : 0.0;
+        if (d2 > P.dm2 && d2 < P.dp2) mu = xi_shell_256(P, d2);
+        t0 = fma(mu, sh[0][0][a], t0);
+        t1 = fma(mu, sh[0][1][a], t1);
+      }
+      v0 = fma(t0, sh[1][0][b], v0);
+      v1 = fma(t1, sh[1][0][b], v1);
+      v2 = fma(t0, sh[1][1][b], v2);
+      v3 = fma(t1, sh[1][1][b], v3);
+    }
+    // dynamic q1 index: V lives in local memory for this path
+    V[q1][0] += v0;
+    V[q1][1] += v1;
+    V[q1][2] += v2;
+    V[q1][3] += v3;
+  }
+}
+
+template <int NO>
+MF_DEV void quad_plateau(const AsmParams &P, const double *g,
+                         const OuterBox &O, const double *s_t,
+                         const double *s_w, double *SP) {
+  double X[2][NO], sh[2][2][NO];
+  box_axes<NO>(P, g, O, s_t, s_w, X, sh);
+  double S[2][2];
+#pragma unroll
+  for (int k = 0; k < 2; k++)
+#pragma unroll
+    for (int j = 0; j < 2; j++) {
+      double s = 0.0;
+#pragma unroll
+      for (int a = 0; a < NO; a++) s += sh[k][j][a];
+      S[k][j] = s;
+    }
+#pragma unroll
+  for (int jy = 0; jy < 2; jy++)
+#pragma unroll
+    for (int jx = 0; jx < 2; jx++) SP[jx + 2 * jy] += 256.0 * S[0][jx] * S[1][jy];
+}
+
+enum : int { ACT_NONE = 0, ACT_SPLIT = 1, ACT_UPPER = 2, ACT_PLAT = 3,
+             ACT_DEAD = 4, ACT_FULL = 5 };
+
+// KIND 1: tri P1 with Dunavant (NO = NI = 7 points, unused template args)
+// KIND 0: quad Q1 with NO / NI points per axis
+template <int KIND, int NO, int NI>
+__global__ void __launch_bounds__(128, 4) k_2d(AsmParams P) {
+  constexpr int NL = Cfg<KIND>::NL;
+  constexpr int NQ1 = KIND == 1 ? 7 : NI * NI;
+  constexpr int NQO = KIND == 1 ? 7 : NO;  // per-axis (quad) / total (tri)
+  __shared__ double s_phiw[NQ1][NL], s_phi[NQ1][NL];
+  __shared__ double s_opts[2 * NQO], s_ow[NQO];
+  const MfMesh &M = P.mesh;
+  const MfRules &Rr = P.rules;
+  for (int i = threadIdx.x; i < NQ1 * NL; i += blockDim.x) {
+    const int q = i / NL, j = i % NL;
+    const double ph = KIND == 1 ? Rr.phi_tri_in[q * NL + j]
+                                : Rr.phi_box_in[q * NL + j];
+    s_phi[q][j] = ph;
+    s_phiw[q][j] = (KIND == 1 ? Rr.tri_in_w[q] : Rr.box_in_w[q]) * ph;
+  }
+  for (int i = threadIdx.x; i < NQO; i += blockDim.x) {
+    if (KIND == 1) {
+      s_opts[2 * i] = Rr.tri_out_pts[2 * i];
+      s_opts[2 * i + 1] = Rr.tri_out_pts[2 * i + 1];
+      s_ow[i] = Rr.tri_out_w[i];
+    } else {
+      s_opts[i] = xmul(xadd(Rr.box_out_x1d[i], 1.0), 0.5);
+      s_ow[i] = Rr.box_out_w1d[i];
+    }
+  }
+  __syncthreads();
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= P.n_inner) return;
+  const int64_t m = P.inner[t];
+
+  // inner element: exact points (_inner_data) and measure factor
+  double y[NQ1][2];
+  double ilo[2], ihi[2], scale_in;
+  ilo[0] = M.elem_lo[m * 2];
+  ilo[1] = M.elem_lo[m * 2 + 1];
+  ihi[0] = M.elem_hi[m * 2];
+  ihi[1] = M.elem_hi[m * 2 + 1];
+  if (KIND == 1) {
+    const double *c = M.elem_coords + m * M.nv_max * 2;
+    const double e10 = xsub(c[2], c[0]), e11 = xsub(c[3], c[1]);
+    const double e20 = xsub(c[4], c[0]), e21 = xsub(c[5], c[1]);
+    scale_in = e10 * e21 - e11 * e20;
+#pragma unroll
+    for (int q = 0; q < NQ1; q++) {
+      const double p0 = Rr.tri_in_pts[2 * q], p1 = Rr.tri_in_pts[2 * q + 1];
+      y[q][0] = xadd(xadd(c[0], xmul(p0, e10)), xmul(p1, e20));
+      y[q][1] = xadd(xadd(c[1], xmul(p0, e11)), xmul(p1, e21));
+    }
+  } else {
+    scale_in = (0.5 * (ihi[0] - ilo[0])) * (0.5 * (ihi[1] - ilo[1]));
+#pragma unroll
+    for (int q = 0; q < NQ1; q++)
+#pragma unroll
+      for (int k = 0; k < 2; k++)
+        y[q][k] = xadd(ilo[k], xmul(xmul(xadd(Rr.box_in_pts[2 * q + k], 1.0),
+                                         0.5),
+                                    xsub(ihi[k], ilo[k])));
+  }
+  double G[NQ1];
+#pragma unroll
+  for (int q = 0; q < NQ1; q++) G[q] = 0.0;
+  unsigned long long c_ev = 0, c_pairs = 0, c_up = 0, c_pl = 0, c_dead = 0,
+                     c_full = 0;
+  int cx, cy, cz;
+  cell_coords(M.elem_cell[m], M.ncx, M.ncy, cx, cy, cz);
+  const int64_t *mdofs = M.elem_dofs + m * M.nloc_max;
+  const int Rs = P.R;
+
+  for (int dy = -Rs; dy <= Rs; dy++) {
+    const int y2 = cy + dy;
+    if (y2 < 0 || y2 >= M.ncy) continue;
+    for (int dx = -Rs; dx <= Rs; dx++) {
+      const int x2 = cx + dx;
+      if (x2 < 0 || x2 >= M.ncx) continue;
+      const int64_t c2 = (int64_t)y2 * M.ncx + x2;
+      for (int64_t l = M.cell_ptr[c2]; l < M.cell_ptr[c2 + 1]; l++) {
+        if (!P.outer_mask[l]) continue;
+        if (!(elem_gap<2>(M.elem_lo, M.elem_hi, l, m) < P.dpe)) continue;
+        c_pairs++;
+        OuterTri OT;
+        OuterBox OB;
+        double root[6];
+        if (KIND == 1) {
+          const double *c = M.elem_coords + l * M.nv_max * 2;
+#pragma unroll
+          for (int u = 0; u < 6; u++) root[u] = c[u];
+          const double e10 = c[2] - c[0], e11 = c[3] - c[1];
+          const double e20 = c[4] - c[0], e21 = c[5] - c[1];
+          const double det = e10 * e21 - e11 * e20;
+          OT.v0[0] = c[0];
+          OT.v0[1] = c[1];
+          OT.inv[0] = e21 / det;
+          OT.inv[1] = -e20 / det;
+          OT.inv[2] = -e11 / det;
+          OT.inv[3] = e10 / det;
+        } else {
+#pragma unroll
+          for (int k = 0; k < 2; k++) {
+            root[k] = M.elem_lo[l * 2 + k];
+            root[2 + k] = M.elem_hi[l * 2 + k];
+            OB.lo[k] = root[k];
+            OB.inv[k] = 1.0 / (root[2 + k] - root[k]);
+          }
+          root[4] = root[5] = 0.0;
+        }
+        double V[NQ1][NL];
+#pragma unroll
+        for (int q = 0; q < NQ1; q++)
+#pragma unroll
+          for (int j = 0; j < NL; j++) V[q][j] = 0.0;
+        double SP[NL];
+#pragma unroll
+        for (int j = 0; j < NL; j++) SP[j] = 0.0;
+        unsigned long long ev = 0;
+        double geo[kMaxLevels + 1][6];
+        int child[kMaxLevels + 1];
+#pragma unroll
+        for (int u = 0; u < 6; u++) geo[1][u] = root[u];
+        int L = 1;
+        for (;;) {
+          double slo[2], shi[2];
+          sub_bbox<KIND>(geo[L], slo, shi);
+          int act = ACT_NONE;
+          if (L < P.L_min) {
+            act = ACT_SPLIT;
+          } else if (L == P.L_max) {
+            if (aprx_min_d<2>(slo, shi, ilo, ihi) < P.dpe) {
+              if (!P.shortcuts)
+                act = ACT_FULL;
+              else if (box_dead<2>(P, slo, shi, ilo, ihi))
+                act = ACT_DEAD;
+              else if (aprx_max_lt_dme(P, aprx_max_sq<2>(slo, shi, ilo, ihi)))
+                act = ACT_PLAT;
+              else
+                act = ACT_FULL;
+            }
+          } else if (aprx_max_lt_dme(P, aprx_max_sq<2>(slo, shi, ilo, ihi))) {
+            act = ACT_UPPER;
+          } else if (aprx_min_d<2>(slo, shi, ilo, ihi) < P.dpe) {
+            act = ACT_SPLIT;
+          }
+          if (act >= ACT_UPPER) {
+            ev++;
+            if (act == ACT_UPPER) c_up++;
+            if (act == ACT_DEAD) c_dead++;
+            if (act == ACT_PLAT) c_pl++;
+            if (act == ACT_FULL) c_full++;
+            const bool plateau =
+                act == ACT_PLAT || (act == ACT_UPPER && P.shortcuts);
+            const bool full = act == ACT_FULL || (act == ACT_UPPER &&
+                                                  !P.shortcuts);
+            if constexpr (KIND == 1) {
+              if (plateau)
+                tri_plateau(P, geo[L], OT, s_opts, s_ow, SP);
+              else if (full)
+                tri_full<NQ1>(P, geo[L], OT, y, s_opts, s_ow,
+                              reinterpret_cast<double(*)[3]>(V));
+            } else {
+              if (plateau)
+                quad_plateau<NO>(P, geo[L], OB, s_opts, s_ow, SP);
+              else if (full)
+                quad_full<NO, NQ1>(P, geo[L], OB, y, s_opts, s_ow,
+                                   reinterpret_cast<double(*)[4]>(V));
+            }
+          }
+          if (act == ACT_SPLIT) {
+            ++L;
+            child[L] = 0;
+            make_child<KIND>(geo[L - 1], 0, geo[L]);
+            continue;
+          }
+          bool done = false;
+          for (;;) {
+            if (L == 1) {
+              done = true;
+              break;
+            }
+            if (++child[L] < Cfg<KIND>::NCHILD) {
+              make_child<KIND>(geo[L - 1], child[L], geo[L]);
+              break;
+            }
+            --L;
+          }
+          if (done) break;
+        }
+        if (ev) {
+          c_ev += ev;
+          // plateau part is common to every q1
+          double spsum = 0.0;
+#pragma unroll
+          for (int j = 0; j < NL; j++) spsum += SP[j];
+          const int64_t *ldofs = M.elem_dofs + l * M.nloc_max;
+          const double sc = -P.scale * scale_in;
+#pragma unroll
+          for (int i = 0; i < NL; i++) {
+            double mi = 0.0;
+#pragma unroll
+            for (int q = 0; q < NQ1; q++) mi += s_phiw[q][i];
+            const int64_t r = mdofs[i];
+#pragma unroll
+            for (int j = 0; j < NL; j++) {
+              double b = mi * SP[j];
+#pragma unroll
+              for (int q = 0; q < NQ1; q++) b = fma(s_phiw[q][i], V[q][j], b);
+              P.vals[pat_index(P.pat, r, ldofs[j])] += sc * b;
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < NQ1; q++) {
+            double s = spsum;
+#pragma unroll
+            for (int j = 0; j < NL; j++) s += V[q][j];
+            G[q] += s;
+          }
+        }
+      }
+    }
+  }
+  // A22 of the element
+  const double sc = P.scale * scale_in;
+#pragma unroll
+  for (int i = 0; i < NL; i++) {
+    const int64_t r = mdofs[i];
+#pragma unroll
+    for (int j = 0; j < NL; j++) {
+      double b = 0.0;
+#pragma unroll
+      for (int q = 0; q < NQ1; q++) b = fma(G[q] * s_phiw[q][i], s_phi[q][j], b);
+      P.vals[pat_index(P.pat, r, mdofs[j])] += sc * b;
+    }
+  }
+  unsigned long long *C = P.counters;
+  counter_add(C + MF_CNT_EVENTS, c_ev);
+  counter_add(C + MF_CNT_PAIRS, c_pairs);
+  counter_add(C + MF_CNT_EV_UPPER, c_up);
+  counter_add(C + MF_CNT_EV_PLATEAU, c_pl);
+  counter_add(C + MF_CNT_EV_DEAD, c_dead);
+  counter_add(C + MF_CNT_EV_FULL, c_full);
+}
+
+template <int KIND, int NO, int NI>
+cudaError_t launch(const AsmParams &P, cudaStream_t s) {
+  const int block = 128;
+  const int64_t grid = (P.n_inner + block - 1) / block;
+  k_2d<KIND, NO, NI><<<(unsigned)grid, block, 0, s>>>(P);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool mf_2d_supported(const AsmParams &P) {
+  const MfMesh &M = P.mesh;
+  if (M.dim != 2 || M.degree != 1 || P.L_max > kMaxLevels) return false;
+  const MfRules &R = P.rules;
+  if (M.kinds_present == 2) {  // pure triangle mesh
+    return M.nloc_max == 3 && R.nq_tri_out == 7 && R.nq_tri_in == 7;
+  }
+  if (M.kinds_present != 1) return false;  // mixed -> generic kernel
+  if (R.n1d_box_in < 1 || R.n1d_box_in > 3) return false;
+  if (R.n1d_box_out < 1 || R.n1d_box_out > 4) return false;
+  return R.nq_box_in == R.n1d_box_in * R.n1d_box_in &&
+         R.nq_box_out == R.n1d_box_out * R.n1d_box_out;
+}
+
+cudaError_t mf_launch_2d(const AsmParams &P, cudaStream_t s) {
+  if (P.mesh.kinds_present == 2) return launch<1, 7, 7>(P, s);
+  const int no = P.rules.n1d_box_out, ni = P.rules.n1d_box_in;
+#define MF_Q(NO_, NI_) \
+  if (no == NO_ && ni == NI_) return launch<0, NO_, NI_>(P, s);
+  MF_Q(1, 1) MF_Q(2, 1) MF_Q(3, 1) MF_Q(4, 1)
+  MF_Q(1, 2) MF_Q(2, 2) MF_Q(3, 2) MF_Q(4, 2)
+  MF_Q(1, 3) MF_Q(2, 3) MF_Q(3, 3) MF_Q(4, 3)
+#undef MF_Q
+  return cudaErrorNotSupported;
+}

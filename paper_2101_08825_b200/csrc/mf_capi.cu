@@ -2,7 +2,7 @@
 //
 // Argument validation, launch configuration and kernel selection live
 // here; the kernels are in mf_candidates.cu, mf_generic.cu, mf_hex.cu,
-// mf_tri.cu and mf_matrix.cu.  Host arithmetic that feeds classification
+// mf_2d.cu and mf_matrix.cu.  Host arithmetic that feeds classification
 // (delta -/+ eps and their squares, _kernels.py:410-413) is plain IEEE
 // double without contraction (x86-64 host code, no -mfma).
 #include <string>
@@ -19,9 +19,9 @@ cudaError_t mf_launch_generic(const AsmParams &, int, int, cudaStream_t);
 // specialised kernels: return cudaErrorNotSupported when they do not cover
 // the configuration
 cudaError_t mf_launch_hex(const AsmParams &, cudaStream_t);
-cudaError_t mf_launch_tri(const AsmParams &, cudaStream_t);
+cudaError_t mf_launch_2d(const AsmParams &, cudaStream_t);
 bool mf_hex_supported(const AsmParams &);
-bool mf_tri_supported(const AsmParams &);
+bool mf_2d_supported(const AsmParams &);
 cudaError_t mf_launch_asym(const MfPattern &, const double *, double *,
                            cudaStream_t);
 cudaError_t mf_launch_norm(const MfPattern &, const double *, double *,
@@ -207,7 +207,7 @@ int mf_general_core(const MfMesh *mesh, const MfRules *rules,
 
   const bool force_generic = (flags & MF_FLAG_FORCE_GENERIC) != 0;
   bool use_hex = !force_generic && mf_hex_supported(P);
-  bool use_tri = !force_generic && !use_hex && mf_tri_supported(P);
+  bool use_2d = !force_generic && !use_hex && mf_2d_supported(P);
   for (int c = 0; c < ncolors; c++) {
     int64_t n = color_ptr[c + 1] - color_ptr[c];
     if (n <= 0) continue;
@@ -216,8 +216,8 @@ int mf_general_core(const MfMesh *mesh, const MfRules *rules,
     cudaError_t e;
     if (use_hex) {
       e = mf_launch_hex(P, s);
-    } else if (use_tri) {
-      e = mf_launch_tri(P, s);
+    } else if (use_2d) {
+      e = mf_launch_2d(P, s);
     } else {
       int64_t want = (n + kGenericBlock - 1) / kGenericBlock;
       int grid = (int)(want < kGenericMaxGrid ? want : kGenericMaxGrid);

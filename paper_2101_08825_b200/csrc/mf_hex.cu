@@ -1,6 +1,473 @@
-// mf_hex.cu -- specialised 3D hex Q1 kernel (placeholder until written).
+// mf_hex.cu -- specialised adaptive assembly for hex Q1 meshes (3D).
+//
+// Covers BASELINE config #4/#5 stand-ins: pure hex
+// mesh, degree 1, tensor outer rule with NO points per axis (2..4), tensor
+// inner rule with NI^3 <= 32 points, L_max <= 4.
+//
+// Work decomposition (one warp per INNER element m of the current colour):
+//   lane q1 < NI^3 owns inner quadrature point y_q1 (_inner_data,
+//   _kernels.py:316-340) and two accumulators:
+//     V[q1][j] = sum over events of this pair of sum_q2 gamma(x_q2, y_q1)
+//                w_q2 phi_j(x_q2)                     (reset per pair)
+//     G[q1]    = sum over all pairs of sum_j V[q1][j] (= the reference's
+//                gsum, since the Q1 shapes sum to one)
+//   b21 = -PHI1w^T V is contracted once per pair and A22 once per element
+//   (the reference folds both per pair, _kernels.py:139-143, 303-312).
+//
+// Algorithm 1 (_pair_blocks, _kernels.py:184-313) runs level-synchronously:
+// the root sub-cell is classified by every lane, the 8^k children of level
+// k are classified one per lane, each child's box recomputed from the root
+// along its path with the reference's midpoint arithmetic, so the
+// classification is bit-identical.  Events are then integrated by the
+// whole warp.  L_max events are split three ways (counted identically):
+//   dead    -- exact box gap >= delta+eps: every point pair is skipped by
+//              the reference (_kernels.py:134-135); nothing to integrate
+//   plateau -- aprx_max < delta-eps: mu == 1 at every point pair, so the
+//              event is a rank-1 tensor product (3 x 1D sums)
+//   full    -- point pairs evaluated; the outer tensor rule is contracted
+//              by sum factorisation (x, then y, then z), 114 DFMA per lane
+//              for NO = 3 instead of 27*8.
+// Point coordinates and squared distances use the *_rn intrinsics so they
+// match the reference bit for bit (eps = 0 ties depend on it).
 #include "mf_common.cuh"
-bool mf_hex_supported(const AsmParams &) { return false; }
-cudaError_t mf_launch_hex(const AsmParams &, cudaStream_t) {
+
+namespace {
+
+constexpr int kWarpsPerBlock = 4;
+constexpr int kSplitCap = 64;  // split nodes per level (L_max <= 4)
+
+struct Box {
+  double lo[3], hi[3];
+};
+
+MF_DEV void child_box(const Box &p, int b, Box &c) {
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    double mid = xmul(0.5, xadd(p.lo[k], p.hi[k]));
+    if ((b >> k) & 1) {
+      c.lo[k] = mid;
+      c.hi[k] = p.hi[k];
+    } else {
+      c.lo[k] = p.lo[k];
+      c.hi[k] = mid;
+    }
+  }
+}
+
+// box of the node with path `code` (3 bits per level below the root)
+MF_DEV Box path_box(const Box &root, uint32_t code, int L) {
+  Box g = root;
+  for (int l = 2; l <= L; l++) {
+    Box c;
+    child_box(g, (code >> (3 * (l - 2))) & 7, c);
+    g = c;
+  }
+  return g;
+}
+
+enum : int { ACT_NONE = 0, ACT_SPLIT = 1, ACT_UPPER = 2, ACT_PLAT = 3,
+             ACT_DEAD = 4, ACT_FULL = 5 };
+
+MF_DEV int classify(const AsmParams &P, const Box &g, int L,
+                    const double *ilo, const double *ihi) {
+  if (L < P.L_min) return ACT_SPLIT;
+  if (L == P.L_max) {
+    if (!(aprx_min_d<3>(g.lo, g.hi, ilo, ihi) < P.dpe)) return ACT_NONE;
+    if (!P.shortcuts) return ACT_FULL;
+    if (box_dead<3>(P, g.lo, g.hi, ilo, ihi)) return ACT_DEAD;
+    if (aprx_max_lt_dme(P, aprx_max_sq<3>(g.lo, g.hi, ilo, ihi)))
+      return ACT_PLAT;
+    return ACT_FULL;
+  }
+  if (aprx_max_lt_dme(P, aprx_max_sq<3>(g.lo, g.hi, ilo, ihi)))
+    return P.shortcuts ? ACT_UPPER : -ACT_UPPER;  // negative: integrate full
+  if (aprx_min_d<3>(g.lo, g.hi, ilo, ihi) < P.dpe) return ACT_SPLIT;
+  return ACT_NONE;
+}
+
+template <int NO>
+struct OuterRule {
+  double t[NO];  // (p_a + 1) * 0.5, exact
+  double w[NO];
+};
+
+struct PairCtx {
+  double olo[3], ohi[3], oinv[3];
+};
+
+// per-axis data of an event: pullback shapes times weights
+template <int NO>
+MF_DEV void event_axes(const AsmParams &P, const OuterRule<NO> &R,
+                       const PairCtx &O, const Box &g, double X[3][NO],
+                       double sh[3][2][NO], bool want_x) {
+  double jac = 1.0;
+#pragma unroll
+  for (int k = 0; k < 3; k++) jac *= 0.5 * (g.hi[k] - g.lo[k]);
+  const double f0 = P.cde * jac * (1.0 / 256.0);
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    const double wk = xsub(g.hi[k], g.lo[k]);
+#pragma unroll
+    for (int a = 0; a < NO; a++) {
+      double x = xadd(g.lo[k], xmul(R.t[a], wk));
+      if (want_x) X[k][a] = x;
+      double s1 = (x - O.olo[k]) * O.oinv[k];
+      double wa = R.w[a] * (k == 0 ? f0 : 1.0);
+      sh[k][0][a] = (1.0 - s1) * wa;
+      sh[k][1][a] = s1 * wa;
+    }
+  }
+}
+
+// mu == 1 everywhere: V[j] += 256 * Sx[jx] Sy[jy] Sz[jz]
+template <int NO>
+MF_DEV void event_plateau(const AsmParams &P, const OuterRule<NO> &R,
+                          const PairCtx &O, const Box &g, double V[8]) {
+  double X[3][NO], sh[3][2][NO];
+  event_axes<NO>(P, R, O, g, X, sh, false);
+  double S[3][2];
+#pragma unroll
+  for (int k = 0; k < 3; k++)
+#pragma unroll
+    for (int j = 0; j < 2; j++) {
+      double s = 0.0;
+#pragma unroll
+      for (int a = 0; a < NO; a++) s += sh[k][j][a];
+      S[k][j] = s;
+    }
+#pragma unroll
+  for (int jz = 0; jz < 2; jz++)
+#pragma unroll
+    for (int jy = 0; jy < 2; jy++) {
+      double syz = 256.0 * S[1][jy] * S[2][jz];
+#pragma unroll
+      for (int jx = 0; jx < 2; jx++)
+        V[jx + 2 * jy + 4 * jz] = fma(S[0][jx], syz, V[jx + 2 * jy + 4 * jz]);
+    }
+}
+
+template <int NO>
+MF_DEV void event_full(const AsmParams &P, const OuterRule<NO> &R,
+                       const PairCtx &O, const Box &g, const double y[3],
+                       bool active, double V[8]) {
+  double X[3][NO], sh[3][2][NO];
+  event_axes<NO>(P, R, O, g, X, sh, true);
+  if (!active) return;
+  double sq[3][NO];
+#pragma unroll
+  for (int k = 0; k < 3; k++)
+#pragma unroll
+    for (int a = 0; a < NO; a++) {
+      double d = xsub(X[k][a], y[k]);
+      sq[k][a] = xmul(d, d);
+    }
+  double sxy[NO][NO];
+#pragma unroll
+  for (int a = 0; a < NO; a++)
+#pragma unroll
+    for (int b = 0; b < NO; b++) sxy[a][b] = xadd(sq[0][a], sq[1][b]);
+  // z outermost: for each outer z-node c contract x (2 DFMA per point),
+  // then y (4 x NO), then scatter into V along z (8)
+#pragma unroll
+  for (int c = 0; c < NO; c++) {
+    double Tb[2][NO];
+#pragma unroll
+    for (int b = 0; b < NO; b++) {
+      double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+      for (int a = 0; a < NO; a++) {
+        const double d2 = xadd(sxy[a][b], sq[2][c]);
+        double mu = (d2 <= P.dm2) ? 256.0 : 0.0;
+        if (d2 > P.dm2 && d2 < P.dp2) mu = xi_shell_256(P, d2);
+        t0 = fma(mu, sh[0][0][a], t0);
+        t1 = fma(mu, sh[0][1][a], t1);
+      }
+      Tb[0][b] = t0;
+      Tb[1][b] = t1;
+    }
+#pragma unroll
+    for (int jx = 0; jx < 2; jx++)
+#pragma unroll
+      for (int jy = 0; jy < 2; jy++) {
+        double t2 = 0.0;
+#pragma unroll
+        for (int b = 0; b < NO; b++) t2 = fma(Tb[jx][b], sh[1][jy][b], t2);
+        V[jx + 2 * jy] = fma(t2, sh[2][0][c], V[jx + 2 * jy]);
+        V[jx + 2 * jy + 4] = fma(t2, sh[2][1][c], V[jx + 2 * jy + 4]);
+      }
+  }
+}
+
+MF_DEV Box shfl_box(const Box &g, int src) {
+  Box r;
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    r.lo[k] = __shfl_sync(0xffffffffu, g.lo[k], src);
+    r.hi[k] = __shfl_sync(0xffffffffu, g.hi[k], src);
+  }
+  return r;
+}
+
+template <int NO, int NI>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
+    k_hex(AsmParams P) {
+  constexpr int NQ1 = NI * NI * NI;
+  __shared__ double s_phiw[NQ1][8];  // w_ref[q1] * PHI1[q1][i]
+  __shared__ double s_phi[NQ1][8];   // PHI1[q1][i]
+  __shared__ double s_buf[kWarpsPerBlock][NQ1][9];
+  __shared__ uint32_t s_split[kWarpsPerBlock][2][kSplitCap];
+
+  const MfMesh &M = P.mesh;
+  const MfRules &Rr = P.rules;
+  for (int i = threadIdx.x; i < NQ1 * 8; i += blockDim.x) {
+    int q = i / 8, j = i % 8;
+    double ph = Rr.phi_box_in[q * 8 + j];
+    s_phi[q][j] = ph;
+    s_phiw[q][j] = Rr.box_in_w[q] * ph;
+  }
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t t = (int64_t)blockIdx.x * kWarpsPerBlock + wib;
+  if (t >= P.n_inner) return;
+
+  OuterRule<NO> R;
+#pragma unroll
+  for (int a = 0; a < NO; a++) {
+    R.t[a] = xmul(xadd(Rr.box_out_x1d[a], 1.0), 0.5);
+    R.w[a] = Rr.box_out_w1d[a];
+  }
+
+  const int64_t m = P.inner[t];
+  double ilo[3], ihi[3];
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    ilo[k] = M.elem_lo[m * 3 + k];
+    ihi[k] = M.elem_hi[m * 3 + k];
+  }
+  const double jac_in = (0.5 * (ihi[0] - ilo[0])) * (0.5 * (ihi[1] - ilo[1])) *
+                        (0.5 * (ihi[2] - ilo[2]));
+  const bool active = lane < NQ1;
+  double y[3] = {0.0, 0.0, 0.0};
+  if (active) {
+#pragma unroll
+    for (int k = 0; k < 3; k++)
+      y[k] = xadd(ilo[k], xmul(xmul(xadd(Rr.box_in_pts[lane * 3 + k], 1.0),
+                                    0.5),
+                               xsub(ihi[k], ilo[k])));
+  }
+  double G = 0.0;
+  unsigned long long c_ev = 0, c_pairs = 0, c_up = 0, c_pl = 0, c_dead = 0,
+                     c_full = 0;
+  int cx, cy, cz;
+  cell_coords(M.elem_cell[m], M.ncx, M.ncy, cx, cy, cz);
+  const int Rs = P.R;
+  const int xlo = max(cx - Rs, 0), xhi = min(cx + Rs, M.ncx - 1);
+  const int ylo = max(cy - Rs, 0), yhi = min(cy + Rs, M.ncy - 1);
+  const int zlo = max(cz - Rs, 0), zhi = min(cz + Rs, M.ncz - 1);
+  const int nx = xhi - xlo + 1, ny = yhi - ylo + 1;
+  const int ncell = nx * ny * (zhi - zlo + 1);
+  const int64_t *mdofs = M.elem_dofs + m * M.nloc_max;
+  // this lane's two b21 outputs: (i0, j) and (i0 + 4, j)
+  const int oj = lane & 7, oi = lane >> 3;
+  const int64_t row0 = mdofs[oi], row1 = mdofs[oi + 4];
+  double(*buf)[9] = s_buf[wib];
+
+  for (int base = 0; base < ncell; base += 32) {
+    const int ci = base + lane;
+    int64_t cand = -1;
+    if (ci < ncell) {
+      const int x2 = xlo + ci % nx;
+      const int tt = ci / nx;
+      const int y2 = ylo + tt % ny;
+      const int z2 = zlo + tt / ny;
+      const int64_t c2 = ((int64_t)z2 * M.ncy + y2) * M.ncx + x2;
+      const int64_t l = M.cell_ptr[c2];
+      if (l < M.cell_ptr[c2 + 1] && P.outer_mask[l] &&
+          elem_gap<3>(M.elem_lo, M.elem_hi, l, m) < P.dpe)
+        cand = l;
+    }
+    unsigned mask = __ballot_sync(0xffffffffu, cand >= 0);
+    while (mask) {
+      const int src = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const int64_t l = __shfl_sync(0xffffffffu, cand, src);
+      c_pairs++;
+      PairCtx O;
+      Box root;
+#pragma unroll
+      for (int k = 0; k < 3; k++) {
+        O.olo[k] = M.elem_lo[l * 3 + k];
+        O.ohi[k] = M.elem_hi[l * 3 + k];
+        O.oinv[k] = 1.0 / (O.ohi[k] - O.olo[k]);
+        root.lo[k] = O.olo[k];
+        root.hi[k] = O.ohi[k];
+      }
+      double V[8];
+#pragma unroll
+      for (int j = 0; j < 8; j++) V[j] = 0.0;
+      unsigned long long ev = 0;
+      int act = classify(P, root, 1, ilo, ihi);
+      if (act == ACT_UPPER || act == ACT_PLAT) {
+        ev++;
+        (act == ACT_UPPER ? c_up : c_pl)++;
+        event_plateau<NO>(P, R, O, root, V);
+      } else if (act == ACT_FULL || act == -ACT_UPPER) {
+        ev++;
+        (act == ACT_FULL ? c_full : c_up)++;
+        event_full<NO>(P, R, O, root, y, active, V);
+      } else if (act == ACT_DEAD) {
+        ev++;
+        c_dead++;
+      } else if (act == ACT_SPLIT) {
+        uint32_t *cur = s_split[wib][0], *nxt = s_split[wib][1];
+        int nsplit = 1;
+        if (lane == 0) cur[0] = 0;
+        __syncwarp();
+        for (int L = 2; L <= P.L_max && nsplit > 0; L++) {
+          const int nchild = nsplit * 8;
+          int nnext = 0;
+          for (int rb = 0; rb < nchild; rb += 32) {
+            const int k = rb + lane;
+            Box g;
+            int a = ACT_NONE;
+            uint32_t code = 0;
+            if (k < nchild) {
+              code = cur[k >> 3] | ((uint32_t)(k & 7) << (3 * (L - 2)));
+              g = path_box(root, code, L);
+              a = classify(P, g, L, ilo, ihi);
+            }
+            const unsigned msplit = __ballot_sync(0xffffffffu, a == ACT_SPLIT);
+            if (msplit) {
+              const int pos = nnext + __popc(msplit & ((1u << lane) - 1));
+              if (a == ACT_SPLIT) {
+                if (pos < kSplitCap) nxt[pos] = code;
+              }
+              nnext += __popc(msplit);
+            }
+            const unsigned mplat =
+                __ballot_sync(0xffffffffu, a == ACT_UPPER || a == ACT_PLAT);
+            const unsigned mfull =
+                __ballot_sync(0xffffffffu, a == ACT_FULL || a == -ACT_UPPER);
+            const unsigned mdead = __ballot_sync(0xffffffffu, a == ACT_DEAD);
+            const unsigned mup = __ballot_sync(
+                0xffffffffu, a == ACT_UPPER || a == -ACT_UPPER);
+            ev += __popc(mplat) + __popc(mfull) + __popc(mdead);
+            c_dead += __popc(mdead);
+            c_up += __popc(mup);
+            c_pl += __popc(mplat & ~mup);
+            c_full += __popc(mfull & ~mup);
+            unsigned mm = mplat;
+            while (mm) {
+              const int s = __ffs(mm) - 1;
+              mm &= mm - 1;
+              Box e = shfl_box(g, s);
+              event_plateau<NO>(P, R, O, e, V);
+            }
+            mm = mfull;
+            while (mm) {
+              const int s = __ffs(mm) - 1;
+              mm &= mm - 1;
+              Box e = shfl_box(g, s);
+              event_full<NO>(P, R, O, e, y, active, V);
+            }
+          }
+          __syncwarp();
+          if (nnext > kSplitCap) {
+            if (lane == 0) atomicExch(P.overflow, 1);
+            nnext = 0;
+          }
+          uint32_t *tmp = cur;
+          cur = nxt;
+          nxt = tmp;
+          nsplit = nnext;
+        }
+      }
+      if (ev) {
+        c_ev += ev;
+        // b21[i][j] = -jac_in * sum_q1 phiw[q1][i] V[q1][j]
+        if (active) {
+#pragma unroll
+          for (int j = 0; j < 8; j++) buf[lane][j] = V[j];
+        }
+        double gs = 0.0;
+#pragma unroll
+        for (int j = 0; j < 8; j++) gs += V[j];
+        G += gs;
+        __syncwarp();
+        double b0 = 0.0, b1 = 0.0;
+#pragma unroll
+        for (int q = 0; q < NQ1; q++) {
+          const double v = buf[q][oj];
+          b0 = fma(s_phiw[q][oi], v, b0);
+          b1 = fma(s_phiw[q][oi + 4], v, b1);
+        }
+        __syncwarp();
+        const int64_t col = M.elem_dofs[l * M.nloc_max + oj];
+        const double sc = -P.scale * jac_in;
+        P.vals[pat_index(P.pat, row0, col)] += sc * b0;
+        P.vals[pat_index(P.pat, row1, col)] += sc * b1;
+      }
+    }
+  }
+  // A22 for the whole element: jac_in * sum_q1 G[q1] phiw[q1][i] phi[q1][j]
+  if (active) buf[lane][8] = G;
+  __syncwarp();
+  double b0 = 0.0, b1 = 0.0;
+#pragma unroll
+  for (int q = 0; q < NQ1; q++) {
+    const double gq = buf[q][8] * s_phi[q][oj];
+    b0 = fma(s_phiw[q][oi], gq, b0);
+    b1 = fma(s_phiw[q][oi + 4], gq, b1);
+  }
+  const int64_t col = mdofs[oj];
+  const double sc = P.scale * jac_in;
+  P.vals[pat_index(P.pat, row0, col)] += sc * b0;
+  P.vals[pat_index(P.pat, row1, col)] += sc * b1;
+  if (lane == 0) {
+    unsigned long long *C = P.counters;
+    counter_add(C + MF_CNT_EVENTS, c_ev);
+    counter_add(C + MF_CNT_PAIRS, c_pairs);
+    counter_add(C + MF_CNT_EV_UPPER, c_up);
+    counter_add(C + MF_CNT_EV_PLATEAU, c_pl);
+    counter_add(C + MF_CNT_EV_DEAD, c_dead);
+    counter_add(C + MF_CNT_EV_FULL, c_full);
+  }
+}
+
+template <int NO, int NI>
+cudaError_t launch(const AsmParams &P, cudaStream_t s) {
+  int64_t grid = (P.n_inner + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  k_hex<NO, NI><<<(unsigned)grid, kWarpsPerBlock * 32, 0, s>>>(P);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool mf_hex_supported(const AsmParams &P) {
+  const MfMesh &M = P.mesh;
+  if (M.dim != 3 || M.degree != 1 || M.nloc_max != 8) return false;
+  if (P.L_max > 4) return false;
+  const MfRules &R = P.rules;
+  if (R.n1d_box_in < 2 || R.n1d_box_in > 3) return false;
+  if (R.n1d_box_out < 2 || R.n1d_box_out > 4) return false;
+  if (R.nq_box_in != R.n1d_box_in * R.n1d_box_in * R.n1d_box_in) return false;
+  if (R.nq_box_out != R.n1d_box_out * R.n1d_box_out * R.n1d_box_out)
+    return false;
+  return M.kinds_present == 4;  // pure hex (mesh.py:168-178)
+}
+
+cudaError_t mf_launch_hex(const AsmParams &P, cudaStream_t s) {
+  const int no = P.rules.n1d_box_out, ni = P.rules.n1d_box_in;
+  if (ni == 3) {
+    if (no == 2) return launch<2, 3>(P, s);
+    if (no == 3) return launch<3, 3>(P, s);
+    if (no == 4) return launch<4, 3>(P, s);
+  } else if (ni == 2) {
+    if (no == 2) return launch<2, 2>(P, s);
+    if (no == 3) return launch<3, 2>(P, s);
+    if (no == 4) return launch<4, 2>(P, s);
+  }
   return cudaErrorNotSupported;
 }

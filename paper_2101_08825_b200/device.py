@@ -62,7 +62,9 @@ class DeviceMesh:
             elem_cell=self.t["elem_cell"].data_ptr(),
             cell_ptr=self.t["cell_ptr"].data_ptr(),
             ncx=int(nc[0]), ncy=int(nc[1]),
-            ncz=int(nc[2]) if mesh.dim == 3 else 1)
+            ncz=int(nc[2]) if mesh.dim == 3 else 1,
+            kinds_present=int(np.bitwise_or.reduce(
+                1 << np.unique(mesh.elem_kind).astype(np.int64))))
 
 
 class DeviceRules:
