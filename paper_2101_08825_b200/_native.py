@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libmollifem_b200.so")
+LIB_PATH = os.environ.get("MF_LIB_PATH") or os.path.join(
+    _HERE, "_lib", "libmollifem_b200.so")
 
 MF_NCOUNTERS = 8
 CNT_EVENTS, CNT_PAIRS, CNT_EV_UPPER, CNT_EV_PLATEAU, CNT_EV_DEAD, \

@@ -500,8 +500,11 @@ class AssemblyContext:
         return A
 
     def run(self, A, outer_mask=None, inner_ids=None, scale=2.0, flags=0,
-            plan=None, counters=None):
-        """Accumulate scale*(A21 + A22) of the selected pairs into A."""
+            plan=None, counters=None, vals_window=None):
+        """Accumulate scale*(A21 + A22) of the selected pairs into A.
+
+        vals_window: a `WindowedValues` when the caller only holds the
+        value range of the rows its inner elements touch (multi-GPU)."""
         import torch
         from . import _native as N
         from .device import ColorPlan, to_device
@@ -526,7 +529,9 @@ class AssemblyContext:
             C_byref(self.dmesh.struct), C_byref(self.drules.struct),
             C_byref(self.kernel_struct()), C_byref(A._pattern_struct()),
             N.ptr(om), N.ptr(plan.inner_sorted), cp, plan.NCOLORS, self.R,
-            float(scale), N.ptr(A._dvals), N.ptr(counters), int(flags),
+            float(scale),
+            (vals_window.pointer() if vals_window is not None
+             else N.ptr(A._dvals)), N.ptr(counters), int(flags),
             N.ptr(ws), wsb, N.stream_ptr()), "mf_general_core")
         return counters
 
@@ -547,6 +552,22 @@ class AssemblyContext:
         A.events = int(cnt[N.CNT_EVENTS])
         A.presym_asymmetry = float(out.item())
         return A
+
+
+class WindowedValues:
+    """A device tensor holding vals[base : base + n] of a larger pattern.
+
+    The kernels index vals with absolute pattern offsets, so they get the
+    tensor's address shifted back by `base` elements; every offset they
+    touch (rows of the caller's inner elements) lies inside the window."""
+
+    def __init__(self, tensor, base):
+        self.tensor = tensor
+        self.base = int(base)
+
+    def pointer(self):
+        import ctypes
+        return ctypes.c_void_p(self.tensor.data_ptr() - 8 * self.base)
 
 
 def ctypes_void_p():

@@ -105,7 +105,7 @@ struct OuterBox {
 };
 
 // ---- triangle events (Dunavant outer rule in shared memory) ----
-template <int NQ1>
+template <int NQ1, bool SHARP>
 MF_DEV void tri_full(const AsmParams &P, const double *g, const OuterTri &O,
                      const double (*y)[2], const double *s_pts,
                      const double *s_w, double (*V)[3]) {
@@ -123,15 +123,37 @@ MF_DEV void tri_full(const AsmParams &P, const double *g, const OuterTri &O,
     const double rx = O.inv[0] * dx0 + O.inv[1] * dx1;
     const double ry = O.inv[2] * dx0 + O.inv[3] * dx1;
     const double p1 = rx * w2, p2 = ry * w2, p0 = w2 - p1 - p2;
+    double mu[NQ1];
+    bool anysh = false;
+    unsigned shm = 0;
 #pragma unroll
     for (int q1 = 0; q1 < NQ1; q1++) {
       const double dx = xsub(x0, y[q1][0]), dy = xsub(x1, y[q1][1]);
       const double d2 = xadd(xmul(dx, dx), xmul(dy, dy));
-      double mu = (d2 <= P.dm2) ? 256.0 : 0.0;
-      if (d2 > P.dm2 && d2 < P.dp2) mu = xi_shell_256(P, d2);
-      V[q1][0] = fma(mu, p0, V[q1][0]);
-      V[q1][1] = fma(mu, p1, V[q1][1]);
-      V[q1][2] = fma(mu, p2, V[q1][2]);
+      if (SHARP) {
+        mu[q1] = d2 < P.dp2 ? 256.0 : 0.0;
+      } else {
+        // high-word classification + warp-voted shell (see mf_hex.cu)
+        const int hi = __double2hiint(d2);
+        const bool pl = hi < P.hi_dm2, sk = hi > P.hi_dp2;
+        const bool sh = !(pl || sk);
+        mu[q1] = sh ? d2 : (pl ? 256.0 : 0.0);
+        shm |= (unsigned)sh << q1;
+        anysh |= sh;
+      }
+    }
+    if (!SHARP && __any_sync(__activemask(), anysh)) {
+#pragma unroll
+      for (int q1 = 0; q1 < NQ1; q1++) {
+        const double v = xi256_unclamped(P, mu[q1]);
+        if ((shm >> q1) & 1u) mu[q1] = v;
+      }
+    }
+#pragma unroll
+    for (int q1 = 0; q1 < NQ1; q1++) {
+      V[q1][0] = fma(mu[q1], p0, V[q1][0]);
+      V[q1][1] = fma(mu[q1], p1, V[q1][1]);
+      V[q1][2] = fma(mu[q1], p2, V[q1][2]);
     }
   }
 }
@@ -180,7 +202,7 @@ MF_DEV void box_axes(const AsmParams &P, const double *g, const OuterBox &O,
   }
 }
 
-template <int NO, int NQ1>
+template <int NO, int NQ1, bool SHARP>
 MF_DEV void quad_full(const AsmParams &P, const double *g, const OuterBox &O,
                       const double (*y)[2], const double *s_t,
                       const double *s_w, double (*V)[4]) {
@@ -199,14 +221,33 @@ MF_DEV void quad_full(const AsmParams &P, const double *g, const OuterBox &O,
     double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
 #pragma unroll
     for (int b = 0; b < NO; b++) {
-      double t0 = 0.0, t1 = 0.0;
+      double mu[NO];
+      unsigned shm = 0;
 #pragma unroll
       for (int a = 0; a < NO; a++) {
         const double d2 = xadd(sqx[a], sqy[b]);
-        double mu = (d2 <= P.dm2) ? 256.0 : 0.0;
-        if (d2 > P.dm2 && d2 < P.dp2) mu = xi_shell_256(P, d2);
-        t0 = fma(mu, sh[0][0][a], t0);
-        t1 = fma(mu, sh[0][1][a], t1);
+        if (SHARP) {
+          mu[a] = d2 < P.dp2 ? 256.0 : 0.0;
+        } else {
+          const int hi = __double2hiint(d2);
+          const bool pl = hi < P.hi_dm2, sk = hi > P.hi_dp2;
+          const bool shl = !(pl || sk);
+          mu[a] = shl ? d2 : (pl ? 256.0 : 0.0);
+          shm |= (unsigned)shl << a;
+        }
+      }
+      if (!SHARP && __any_sync(__activemask(), shm != 0)) {
+#pragma unroll
+        for (int a = 0; a < NO; a++) {
+          const double v = xi256_unclamped(P, mu[a]);
+          if ((shm >> a) & 1u) mu[a] = v;
+        }
+      }
+      double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+      for (int a = 0; a < NO; a++) {
+        t0 = fma(mu[a], sh[0][0][a], t0);
+        t1 = fma(mu[a], sh[0][1][a], t1);
       }
       v0 = fma(t0, sh[1][0][b], v0);
       v1 = fma(t1, sh[1][0][b], v1);
@@ -340,17 +381,18 @@ __global__ void __launch_bounds__(128, 4) k_2d(AsmParams P) {
           const double det = e10 * e21 - e11 * e20;
           OT.v0[0] = c[0];
           OT.v0[1] = c[1];
-          OT.inv[0] = e21 / det;
-          OT.inv[1] = -e20 / det;
-          OT.inv[2] = -e11 / det;
-          OT.inv[3] = e10 / det;
+          const double idet = rcp_fast(det);
+          OT.inv[0] = e21 * idet;
+          OT.inv[1] = -e20 * idet;
+          OT.inv[2] = -e11 * idet;
+          OT.inv[3] = e10 * idet;
         } else {
 #pragma unroll
           for (int k = 0; k < 2; k++) {
             root[k] = M.elem_lo[l * 2 + k];
             root[2 + k] = M.elem_hi[l * 2 + k];
             OB.lo[k] = root[k];
-            OB.inv[k] = 1.0 / (root[2 + k] - root[k]);
+            OB.inv[k] = rcp_fast(root[2 + k] - root[k]);
           }
           root[4] = root[5] = 0.0;
         }
@@ -403,15 +445,21 @@ __global__ void __launch_bounds__(128, 4) k_2d(AsmParams P) {
             if constexpr (KIND == 1) {
               if (plateau)
                 tri_plateau(P, geo[L], OT, s_opts, s_ow, SP);
+              else if (full && P.eps > 0.0)
+                tri_full<NQ1, false>(P, geo[L], OT, y, s_opts, s_ow,
+                                     reinterpret_cast<double(*)[3]>(V));
               else if (full)
-                tri_full<NQ1>(P, geo[L], OT, y, s_opts, s_ow,
-                              reinterpret_cast<double(*)[3]>(V));
+                tri_full<NQ1, true>(P, geo[L], OT, y, s_opts, s_ow,
+                                    reinterpret_cast<double(*)[3]>(V));
             } else {
               if (plateau)
                 quad_plateau<NO>(P, geo[L], OB, s_opts, s_ow, SP);
+              else if (full && P.eps > 0.0)
+                quad_full<NO, NQ1, false>(P, geo[L], OB, y, s_opts, s_ow,
+                                          reinterpret_cast<double(*)[4]>(V));
               else if (full)
-                quad_full<NO, NQ1>(P, geo[L], OB, y, s_opts, s_ow,
-                                   reinterpret_cast<double(*)[4]>(V));
+                quad_full<NO, NQ1, true>(P, geo[L], OB, y, s_opts, s_ow,
+                                         reinterpret_cast<double(*)[4]>(V));
             }
           }
           if (act == ACT_SPLIT) {

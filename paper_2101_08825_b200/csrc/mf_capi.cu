@@ -5,6 +5,7 @@
 // mf_2d.cu and mf_matrix.cu.  Host arithmetic that feeds classification
 // (delta -/+ eps and their squares, _kernels.py:410-413) is plain IEEE
 // double without contraction (x86-64 host code, no -mfma).
+#include <cstring>
 #include <string>
 
 #include "mf_common.cuh"
@@ -192,6 +193,15 @@ int mf_general_core(const MfMesh *mesh, const MfRules *rules,
   P.dp2 = dp * dp;
   P.dme2_lo = dm * dm * (1.0 - 4e-12);
   P.dme2_hi = dm * dm * (1.0 + 4e-12);
+  P.inv_eps = kern->eps > 0.0 ? 1.0 / kern->eps : 0.0;
+  P.alpha = kern->delta * P.inv_eps;
+  {
+    int64_t b;
+    memcpy(&b, &P.dm2, 8);
+    P.hi_dm2 = (int32_t)(b >> 32);
+    memcpy(&b, &P.dp2, 8);
+    P.hi_dp2 = (int32_t)(b >> 32);
+  }
   P.nl_box = mesh->dim == 3 ? (mesh->degree + 1) * (mesh->degree + 1) *
                                   (mesh->degree + 1)
                             : (mesh->degree + 1) * (mesh->degree + 1);

@@ -42,6 +42,9 @@ struct AsmParams {
   double dme, dpe;        // delta -/+ eps  (_kernels.py:410-411)
   double dm2, dp2;        // squared        (_kernels.py:412-413)
   double dme2_lo, dme2_hi;// sqrt-free decision band for aprx_max < dme
+  double inv_eps, alpha;  // 1/eps and delta/eps (eps > 0 kernels)
+  int32_t hi_dm2, hi_dp2; // high 32-bit words of dm2 / dp2 (non-negative
+                          // doubles order like their bit patterns)
   int32_t nl_box, nl_tri;
   int32_t shortcuts;      // plateau/dead event shortcuts enabled
   double *scratch;        // per-thread scratch (generic kernel)
@@ -114,6 +117,62 @@ MF_DEV double xi_shell_256(const AsmParams &P, double d2) {
   double p = fma(fma(fma(fma(35.0, r2, -180.0), r2, 378.0), r2, -420.0), r2,
                  315.0);
   return fma(p, r, 128.0);
+}
+
+// 1/sqrt(x) for normal x > 0 without the libdevice slow-path call:
+// MUFU.RSQ64H seed + two Newton steps (relative error ~1e-16)
+MF_DEV double rsqrt_fast(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double h = x * y;
+  double r = fma(-h, y, 1.0);
+  y = fma(0.5 * y, r, y);
+  h = x * y;
+  r = fma(-h, y, 1.0);
+  return fma(0.5 * y, r, y);
+}
+
+// 1/x for normal x without the IEEE-division slow path (Newton twice)
+MF_DEV double rcp_fast(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+
+// Branch-free 256*mu for eps > 0: r = clamp((delta - d)/eps, -1, 1) and
+// xi(+1) = 1, xi(-1) = 0 exactly, so the plateau and the cut-off need no
+// branch; d = d2 * rsqrt(d2) (d2 clamped away from 0, where r clamps to 1).
+// Matches the reference's piecewise mu (_kernels.py:18-29) to rounding.
+MF_DEV double mu256_smooth(const AsmParams &P, double d2) {
+  const double dd = fmax(d2, 1e-300);
+  const double d = dd * rsqrt_fast(dd);
+  double r = fma(-d, P.inv_eps, P.alpha);
+  r = fmin(fmax(r, -1.0), 1.0);
+  const double r2 = r * r;
+  const double p = fma(fma(fma(fma(35.0, r2, -180.0), r2, 378.0), r2, -420.0),
+                       r2, 315.0);
+  return fma(p, r, 128.0);
+}
+
+// shell mollifier without clamp: callers select it only for pairs whose
+// d2 shares its high 32-bit word with, or lies between, dm2 and dp2, so
+// |r| exceeds 1 by at most (delta/eps) 2^-21 and xi, flat to fourth order
+// at +-1, deviates from its end value by < 1e-24 there.
+MF_DEV double xi256_unclamped(const AsmParams &P, double d2) {
+  const double d = d2 * rsqrt_fast(d2);
+  const double r = fma(-d, P.inv_eps, P.alpha);
+  const double r2 = r * r;
+  const double p = fma(fma(fma(fma(35.0, r2, -180.0), r2, 378.0), r2, -420.0),
+                       r2, 315.0);
+  return fma(p, r, 128.0);
+}
+
+// eps = 0: the reference skips d2 >= delta^2 and takes mu = 1 below
+MF_DEV double mu256_sharp(const AsmParams &P, double d2) {
+  return d2 < P.dp2 ? 256.0 : 0.0;
 }
 
 MF_DEV double mu256(const AsmParams &P, double d2) {

@@ -35,6 +35,12 @@ namespace {
 
 constexpr int kWarpsPerBlock = 4;
 constexpr int kSplitCap = 64;  // split nodes per level (L_max <= 4)
+#ifndef MF_HEX_MINB
+#define MF_HEX_MINB 3
+#endif
+#ifndef MF_HEX_BATCH
+#define MF_HEX_BATCH 3
+#endif
 
 struct Box {
   double lo[3], hi[3];
@@ -43,7 +49,7 @@ struct Box {
 MF_DEV void child_box(const Box &p, int b, Box &c) {
 #pragma unroll
   for (int k = 0; k < 3; k++) {
-    double mid = xmul(0.5, xadd(p.lo[k], p.hi[k]));
+    const double mid = xmul(0.5, xadd(p.lo[k], p.hi[k]));
     if ((b >> k) & 1) {
       c.lo[k] = mid;
       c.hi[k] = p.hi[k];
@@ -54,7 +60,8 @@ MF_DEV void child_box(const Box &p, int b, Box &c) {
   }
 }
 
-// box of the node with path `code` (3 bits per level below the root)
+// box of the node with path `code` (3 bits per level below the root),
+// recomputed from the root with the reference's midpoint arithmetic
 MF_DEV Box path_box(const Box &root, uint32_t code, int L) {
   Box g = root;
   for (int l = 2; l <= L; l++) {
@@ -66,8 +73,10 @@ MF_DEV Box path_box(const Box &root, uint32_t code, int L) {
 }
 
 enum : int { ACT_NONE = 0, ACT_SPLIT = 1, ACT_UPPER = 2, ACT_PLAT = 3,
-             ACT_DEAD = 4, ACT_FULL = 5 };
+             ACT_DEAD = 4, ACT_FULL = 5, ACT_UPPER_FULL = 6 };
 
+// Algorithm-1 decision for one sub-cell (_kernels.py:224-251) plus the
+// dead/plateau proofs for L_max events
 MF_DEV int classify(const AsmParams &P, const Box &g, int L,
                     const double *ilo, const double *ihi) {
   if (L < P.L_min) return ACT_SPLIT;
@@ -80,51 +89,55 @@ MF_DEV int classify(const AsmParams &P, const Box &g, int L,
     return ACT_FULL;
   }
   if (aprx_max_lt_dme(P, aprx_max_sq<3>(g.lo, g.hi, ilo, ihi)))
-    return P.shortcuts ? ACT_UPPER : -ACT_UPPER;  // negative: integrate full
+    return P.shortcuts ? ACT_UPPER : ACT_UPPER_FULL;
   if (aprx_min_d<3>(g.lo, g.hi, ilo, ihi) < P.dpe) return ACT_SPLIT;
   return ACT_NONE;
 }
 
+// Per-warp uniform state kept in shared memory (not registers) so the
+// event code has the register file to itself.
 template <int NO>
-struct OuterRule {
-  double t[NO];  // (p_a + 1) * 0.5, exact
-  double w[NO];
+struct WarpCtx {
+  double ilo[3], ihi[3];           // inner element box
+  double olo[3], ohi[3], oinv[3];  // current outer element box
+  double blo[33][3], bhi[33][3];   // event boxes of the round (32 = root)
+  double X[3][NO];                 // event: outer 1D coordinates
+  double sh[3][2][NO];             // event: weighted pullback shapes
 };
 
-struct PairCtx {
-  double olo[3], ohi[3], oinv[3];
-};
-
-// per-axis data of an event: pullback shapes times weights
+// Phase 0 of an event: lanes (k, a) compute the outer 1D coordinate
+// (exact, like _event_box's x, _kernels.py:115-119) and the two weighted
+// pullback shapes (1-s, s) * w_a on axis k; the x axis also carries
+// cde * |sub-cell| / 8 / 256.
 template <int NO>
-MF_DEV void event_axes(const AsmParams &P, const OuterRule<NO> &R,
-                       const PairCtx &O, const Box &g, double X[3][NO],
-                       double sh[3][2][NO], bool want_x) {
-  double jac = 1.0;
-#pragma unroll
-  for (int k = 0; k < 3; k++) jac *= 0.5 * (g.hi[k] - g.lo[k]);
-  const double f0 = P.cde * jac * (1.0 / 256.0);
-#pragma unroll
-  for (int k = 0; k < 3; k++) {
-    const double wk = xsub(g.hi[k], g.lo[k]);
-#pragma unroll
-    for (int a = 0; a < NO; a++) {
-      double x = xadd(g.lo[k], xmul(R.t[a], wk));
-      if (want_x) X[k][a] = x;
-      double s1 = (x - O.olo[k]) * O.oinv[k];
-      double wa = R.w[a] * (k == 0 ? f0 : 1.0);
-      sh[k][0][a] = (1.0 - s1) * wa;
-      sh[k][1][a] = s1 * wa;
+MF_DEV void event_axes(const AsmParams &P, const double *s_rt,
+                       const double *s_rw, WarpCtx<NO> &C, int slot,
+                       int lane) {
+  if (lane < 3 * NO) {
+    const int k = lane / NO, a = lane - (lane / NO) * NO;
+    const double lo = C.blo[slot][k], hi = C.bhi[slot][k];
+    double wa = s_rw[a];
+    if (k == 0) {
+      const double jac = (0.5 * (C.bhi[slot][0] - C.blo[slot][0])) *
+                         (0.5 * (C.bhi[slot][1] - C.blo[slot][1])) *
+                         (0.5 * (C.bhi[slot][2] - C.blo[slot][2]));
+      wa *= P.cde * jac * (1.0 / 256.0);
     }
+    const double x = xadd(lo, xmul(s_rt[a], xsub(hi, lo)));
+    const double s1 = (x - C.olo[k]) * C.oinv[k];
+    C.X[k][a] = x;
+    C.sh[k][0][a] = (1.0 - s1) * wa;
+    C.sh[k][1][a] = s1 * wa;
   }
+  __syncwarp();
 }
 
-// mu == 1 everywhere: V[j] += 256 * Sx[jx] Sy[jy] Sz[jz]
+// mu == 1 at every point pair: V[j] += 256 Sx[jx] Sy[jy] Sz[jz]
 template <int NO>
-MF_DEV void event_plateau(const AsmParams &P, const OuterRule<NO> &R,
-                          const PairCtx &O, const Box &g, double V[8]) {
-  double X[3][NO], sh[3][2][NO];
-  event_axes<NO>(P, R, O, g, X, sh, false);
+MF_DEV void event_plateau(const AsmParams &P, const double *s_rt,
+                          const double *s_rw, WarpCtx<NO> &C, int slot,
+                          int lane, double V[8]) {
+  event_axes<NO>(P, s_rt, s_rw, C, slot, lane);
   double S[3][2];
 #pragma unroll
   for (int k = 0; k < 3; k++)
@@ -132,98 +145,146 @@ MF_DEV void event_plateau(const AsmParams &P, const OuterRule<NO> &R,
     for (int j = 0; j < 2; j++) {
       double s = 0.0;
 #pragma unroll
-      for (int a = 0; a < NO; a++) s += sh[k][j][a];
+      for (int a = 0; a < NO; a++) s += C.sh[k][j][a];
       S[k][j] = s;
     }
+  __syncwarp();
 #pragma unroll
   for (int jz = 0; jz < 2; jz++)
 #pragma unroll
     for (int jy = 0; jy < 2; jy++) {
-      double syz = 256.0 * S[1][jy] * S[2][jz];
+      const double syz = 256.0 * S[1][jy] * S[2][jz];
 #pragma unroll
       for (int jx = 0; jx < 2; jx++)
         V[jx + 2 * jy + 4 * jz] = fma(S[0][jx], syz, V[jx + 2 * jy + 4 * jz]);
     }
 }
 
-template <int NO>
-MF_DEV void event_full(const AsmParams &P, const OuterRule<NO> &R,
-                       const PairCtx &O, const Box &g, const double y[3],
-                       bool active, double V[8]) {
-  double X[3][NO], sh[3][2][NO];
-  event_axes<NO>(P, R, O, g, X, sh, true);
-  if (!active) return;
+// Full event: lane q1 evaluates its NO^3 point pairs and contracts them
+// by sum factorisation (x, then y, then z) into V.  Point pairs are
+// classified on the high word of the exact d2 (certainly inside delta-eps
+// -> mu = 1, certainly beyond delta+eps -> 0); the shell polynomial runs
+// for a group of BATCH points only when a lane of the warp needs it.
+template <int NO, bool SHARP, int BATCH>
+MF_DEV void event_full(const AsmParams &P, const double *s_rt,
+                       const double *s_rw, WarpCtx<NO> &C, int slot,
+                       const double y[3], int lane, bool active,
+                       double V[8]) {
+  event_axes<NO>(P, s_rt, s_rw, C, slot, lane);
   double sq[3][NO];
 #pragma unroll
   for (int k = 0; k < 3; k++)
 #pragma unroll
     for (int a = 0; a < NO; a++) {
-      double d = xsub(X[k][a], y[k]);
+      const double d = xsub(C.X[k][a], y[k]);
       sq[k][a] = xmul(d, d);
     }
-  double sxy[NO][NO];
+  double shx[2][NO];
 #pragma unroll
-  for (int a = 0; a < NO; a++)
+  for (int j = 0; j < 2; j++)
 #pragma unroll
-    for (int b = 0; b < NO; b++) sxy[a][b] = xadd(sq[0][a], sq[1][b]);
-  // z outermost: for each outer z-node c contract x (2 DFMA per point),
-  // then y (4 x NO), then scatter into V along z (8)
-#pragma unroll
+    for (int a = 0; a < NO; a++) shx[j][a] = C.sh[0][j][a];
+#pragma unroll 1
   for (int c = 0; c < NO; c++) {
     double Tb[2][NO];
 #pragma unroll
     for (int b = 0; b < NO; b++) {
+      double mu[NO];
+      bool shl[NO];
+      bool anysh = false;
+#pragma unroll
+      for (int a = 0; a < NO; a++) {
+        const double d2 = xadd(xadd(sq[0][a], sq[1][b]), sq[2][c]);
+        if (SHARP) {
+          mu[a] = d2 < P.dp2 ? 256.0 : 0.0;
+          shl[a] = false;
+        } else {
+          const int hi = __double2hiint(d2);
+          const bool pl = hi < P.hi_dm2;
+          const bool sk = hi > P.hi_dp2;
+          mu[a] = pl ? 256.0 : 0.0;
+          shl[a] = active && !(pl || sk);
+          anysh |= shl[a];
+          if (BATCH == 1) {
+            if (__any_sync(0xffffffffu, shl[a])) {
+              const double v = xi256_unclamped(P, d2);
+              if (shl[a]) mu[a] = v;
+            }
+          } else if (shl[a]) {
+            mu[a] = d2;
+          }
+        }
+      }
+      if (!SHARP && BATCH != 1) {
+        if (__any_sync(0xffffffffu, anysh)) {
+#pragma unroll
+          for (int a = 0; a < NO; a++) {
+            const double v = xi256_unclamped(P, mu[a]);
+            if (shl[a]) mu[a] = v;
+          }
+        }
+      }
       double t0 = 0.0, t1 = 0.0;
 #pragma unroll
       for (int a = 0; a < NO; a++) {
-        const double d2 = xadd(sxy[a][b], sq[2][c]);
-        double mu = (d2 <= P.dm2) ? 256.0 : 0.0;
-        if (d2 > P.dm2 && d2 < P.dp2) mu = xi_shell_256(P, d2);
-        t0 = fma(mu, sh[0][0][a], t0);
-        t1 = fma(mu, sh[0][1][a], t1);
+        t0 = fma(mu[a], shx[0][a], t0);
+        t1 = fma(mu[a], shx[1][a], t1);
       }
       Tb[0][b] = t0;
       Tb[1][b] = t1;
     }
+    const double z0 = C.sh[2][0][c], z1 = C.sh[2][1][c];
 #pragma unroll
-    for (int jx = 0; jx < 2; jx++)
+    for (int jy = 0; jy < 2; jy++) {
+      double t2x0 = 0.0, t2x1 = 0.0;
 #pragma unroll
-      for (int jy = 0; jy < 2; jy++) {
-        double t2 = 0.0;
-#pragma unroll
-        for (int b = 0; b < NO; b++) t2 = fma(Tb[jx][b], sh[1][jy][b], t2);
-        V[jx + 2 * jy] = fma(t2, sh[2][0][c], V[jx + 2 * jy]);
-        V[jx + 2 * jy + 4] = fma(t2, sh[2][1][c], V[jx + 2 * jy + 4]);
+      for (int b = 0; b < NO; b++) {
+        const double yb = C.sh[1][jy][b];
+        t2x0 = fma(Tb[0][b], yb, t2x0);
+        t2x1 = fma(Tb[1][b], yb, t2x1);
       }
+      V[2 * jy] = fma(t2x0, z0, V[2 * jy]);
+      V[2 * jy + 1] = fma(t2x1, z0, V[2 * jy + 1]);
+      V[2 * jy + 4] = fma(t2x0, z1, V[2 * jy + 4]);
+      V[2 * jy + 5] = fma(t2x1, z1, V[2 * jy + 5]);
+    }
   }
+  __syncwarp();
 }
 
-MF_DEV Box shfl_box(const Box &g, int src) {
-  Box r;
-#pragma unroll
-  for (int k = 0; k < 3; k++) {
-    r.lo[k] = __shfl_sync(0xffffffffu, g.lo[k], src);
-    r.hi[k] = __shfl_sync(0xffffffffu, g.hi[k], src);
-  }
-  return r;
+template <int NO>
+MF_DEV void run_full(const AsmParams &P, const double *s_rt,
+                     const double *s_rw, WarpCtx<NO> &C, int slot,
+                     const double y[3], int lane, bool active, double V[8]) {
+  if (P.eps == 0.0)
+    event_full<NO, true, 1>(P, s_rt, s_rw, C, slot, y, lane, active, V);
+  else
+    event_full<NO, false, (MF_HEX_BATCH == 1 ? 1 : NO)>(
+        P, s_rt, s_rw, C, slot, y, lane, active, V);
 }
 
 template <int NO, int NI>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, MF_HEX_MINB)
     k_hex(AsmParams P) {
   constexpr int NQ1 = NI * NI * NI;
   __shared__ double s_phiw[NQ1][8];  // w_ref[q1] * PHI1[q1][i]
   __shared__ double s_phi[NQ1][8];   // PHI1[q1][i]
+  __shared__ double s_rt[NO], s_rw[NO];
+  __shared__ WarpCtx<NO> s_ctx[kWarpsPerBlock];
   __shared__ double s_buf[kWarpsPerBlock][NQ1][9];
   __shared__ uint32_t s_split[kWarpsPerBlock][2][kSplitCap];
 
   const MfMesh &M = P.mesh;
   const MfRules &Rr = P.rules;
   for (int i = threadIdx.x; i < NQ1 * 8; i += blockDim.x) {
-    int q = i / 8, j = i % 8;
-    double ph = Rr.phi_box_in[q * 8 + j];
+    const int q = i / 8, j = i % 8;
+    const double ph = Rr.phi_box_in[q * 8 + j];
     s_phi[q][j] = ph;
     s_phiw[q][j] = Rr.box_in_w[q] * ph;
+  }
+  if (threadIdx.x < NO) {
+    s_rt[threadIdx.x] = xmul(xadd(Rr.box_out_x1d[threadIdx.x], 1.0), 0.5);
+    s_rw[threadIdx.x] = Rr.box_out_w1d[threadIdx.x];
   }
   __syncthreads();
 
@@ -231,35 +292,29 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
   const int wib = threadIdx.x >> 5;
   const int64_t t = (int64_t)blockIdx.x * kWarpsPerBlock + wib;
   if (t >= P.n_inner) return;
-
-  OuterRule<NO> R;
-#pragma unroll
-  for (int a = 0; a < NO; a++) {
-    R.t[a] = xmul(xadd(Rr.box_out_x1d[a], 1.0), 0.5);
-    R.w[a] = Rr.box_out_w1d[a];
-  }
+  WarpCtx<NO> &C = s_ctx[wib];
+  double(*buf)[9] = s_buf[wib];
 
   const int64_t m = P.inner[t];
-  double ilo[3], ihi[3];
-#pragma unroll
-  for (int k = 0; k < 3; k++) {
-    ilo[k] = M.elem_lo[m * 3 + k];
-    ihi[k] = M.elem_hi[m * 3 + k];
+  if (lane < 3) {
+    C.ilo[lane] = M.elem_lo[m * 3 + lane];
+    C.ihi[lane] = M.elem_hi[m * 3 + lane];
   }
-  const double jac_in = (0.5 * (ihi[0] - ilo[0])) * (0.5 * (ihi[1] - ilo[1])) *
-                        (0.5 * (ihi[2] - ilo[2]));
+  __syncwarp();
+  const double jac_in = (0.5 * (C.ihi[0] - C.ilo[0])) *
+                        (0.5 * (C.ihi[1] - C.ilo[1])) *
+                        (0.5 * (C.ihi[2] - C.ilo[2]));
   const bool active = lane < NQ1;
   double y[3] = {0.0, 0.0, 0.0};
   if (active) {
 #pragma unroll
     for (int k = 0; k < 3; k++)
-      y[k] = xadd(ilo[k], xmul(xmul(xadd(Rr.box_in_pts[lane * 3 + k], 1.0),
-                                    0.5),
-                               xsub(ihi[k], ilo[k])));
+      y[k] = xadd(C.ilo[k],
+                  xmul(xmul(xadd(Rr.box_in_pts[lane * 3 + k], 1.0), 0.5),
+                       xsub(C.ihi[k], C.ilo[k])));
   }
   double G = 0.0;
-  unsigned long long c_ev = 0, c_pairs = 0, c_up = 0, c_pl = 0, c_dead = 0,
-                     c_full = 0;
+  unsigned c_ev = 0, c_pairs = 0, c_up = 0, c_pl = 0, c_dead = 0, c_full = 0;
   int cx, cy, cz;
   cell_coords(M.elem_cell[m], M.ncx, M.ncy, cx, cy, cz);
   const int Rs = P.R;
@@ -268,11 +323,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
   const int zlo = max(cz - Rs, 0), zhi = min(cz + Rs, M.ncz - 1);
   const int nx = xhi - xlo + 1, ny = yhi - ylo + 1;
   const int ncell = nx * ny * (zhi - zlo + 1);
-  const int64_t *mdofs = M.elem_dofs + m * M.nloc_max;
-  // this lane's two b21 outputs: (i0, j) and (i0 + 4, j)
-  const int oj = lane & 7, oi = lane >> 3;
-  const int64_t row0 = mdofs[oi], row1 = mdofs[oi + 4];
-  double(*buf)[9] = s_buf[wib];
 
   for (int base = 0; base < ncell; base += 32) {
     const int ci = base + lane;
@@ -294,94 +344,105 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
       mask &= mask - 1;
       const int64_t l = __shfl_sync(0xffffffffu, cand, src);
       c_pairs++;
-      PairCtx O;
-      Box root;
-#pragma unroll
-      for (int k = 0; k < 3; k++) {
-        O.olo[k] = M.elem_lo[l * 3 + k];
-        O.ohi[k] = M.elem_hi[l * 3 + k];
-        O.oinv[k] = 1.0 / (O.ohi[k] - O.olo[k]);
-        root.lo[k] = O.olo[k];
-        root.hi[k] = O.ohi[k];
+      if (lane < 3) {
+        const double lo = M.elem_lo[l * 3 + lane];
+        const double hi = M.elem_hi[l * 3 + lane];
+        C.olo[lane] = lo;
+        C.ohi[lane] = hi;
+        C.oinv[lane] = rcp_fast(hi - lo);
+        C.blo[32][lane] = lo;
+        C.bhi[32][lane] = hi;
       }
+      __syncwarp();
       double V[8];
 #pragma unroll
       for (int j = 0; j < 8; j++) V[j] = 0.0;
-      unsigned long long ev = 0;
-      int act = classify(P, root, 1, ilo, ihi);
-      if (act == ACT_UPPER || act == ACT_PLAT) {
-        ev++;
-        (act == ACT_UPPER ? c_up : c_pl)++;
-        event_plateau<NO>(P, R, O, root, V);
-      } else if (act == ACT_FULL || act == -ACT_UPPER) {
-        ev++;
-        (act == ACT_FULL ? c_full : c_up)++;
-        event_full<NO>(P, R, O, root, y, active, V);
-      } else if (act == ACT_DEAD) {
-        ev++;
-        c_dead++;
-      } else if (act == ACT_SPLIT) {
-        uint32_t *cur = s_split[wib][0], *nxt = s_split[wib][1];
-        int nsplit = 1;
-        if (lane == 0) cur[0] = 0;
-        __syncwarp();
-        for (int L = 2; L <= P.L_max && nsplit > 0; L++) {
-          const int nchild = nsplit * 8;
-          int nnext = 0;
-          for (int rb = 0; rb < nchild; rb += 32) {
-            const int k = rb + lane;
-            Box g;
-            int a = ACT_NONE;
-            uint32_t code = 0;
-            if (k < nchild) {
-              code = cur[k >> 3] | ((uint32_t)(k & 7) << (3 * (L - 2)));
-              g = path_box(root, code, L);
-              a = classify(P, g, L, ilo, ihi);
-            }
-            const unsigned msplit = __ballot_sync(0xffffffffu, a == ACT_SPLIT);
-            if (msplit) {
-              const int pos = nnext + __popc(msplit & ((1u << lane) - 1));
-              if (a == ACT_SPLIT) {
-                if (pos < kSplitCap) nxt[pos] = code;
-              }
-              nnext += __popc(msplit);
-            }
-            const unsigned mplat =
-                __ballot_sync(0xffffffffu, a == ACT_UPPER || a == ACT_PLAT);
-            const unsigned mfull =
-                __ballot_sync(0xffffffffu, a == ACT_FULL || a == -ACT_UPPER);
-            const unsigned mdead = __ballot_sync(0xffffffffu, a == ACT_DEAD);
-            const unsigned mup = __ballot_sync(
-                0xffffffffu, a == ACT_UPPER || a == -ACT_UPPER);
-            ev += __popc(mplat) + __popc(mfull) + __popc(mdead);
-            c_dead += __popc(mdead);
-            c_up += __popc(mup);
-            c_pl += __popc(mplat & ~mup);
-            c_full += __popc(mfull & ~mup);
-            unsigned mm = mplat;
-            while (mm) {
-              const int s = __ffs(mm) - 1;
-              mm &= mm - 1;
-              Box e = shfl_box(g, s);
-              event_plateau<NO>(P, R, O, e, V);
-            }
-            mm = mfull;
-            while (mm) {
-              const int s = __ffs(mm) - 1;
-              mm &= mm - 1;
-              Box e = shfl_box(g, s);
-              event_full<NO>(P, R, O, e, y, active, V);
-            }
-          }
+      unsigned ev = 0;
+      {
+        Box root;
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+          root.lo[k] = C.olo[k];
+          root.hi[k] = C.ohi[k];
+        }
+        const int act = classify(P, root, 1, C.ilo, C.ihi);
+        if (act == ACT_UPPER || act == ACT_PLAT) {
+          ev++;
+          (act == ACT_UPPER ? c_up : c_pl)++;
+          event_plateau<NO>(P, s_rt, s_rw, C, 32, lane, V);
+        } else if (act == ACT_FULL || act == ACT_UPPER_FULL) {
+          ev++;
+          (act == ACT_FULL ? c_full : c_up)++;
+          run_full<NO>(P, s_rt, s_rw, C, 32, y, lane, active, V);
+        } else if (act == ACT_DEAD) {
+          ev++;
+          c_dead++;
+        } else if (act == ACT_SPLIT) {
+          uint32_t *cur = s_split[wib][0], *nxt = s_split[wib][1];
+          int nsplit = 1;
+          if (lane == 0) cur[0] = 0;
           __syncwarp();
-          if (nnext > kSplitCap) {
-            if (lane == 0) atomicExch(P.overflow, 1);
-            nnext = 0;
+          for (int L = 2; L <= P.L_max && nsplit > 0; L++) {
+            const int nchild = nsplit * 8;
+            int nnext = 0;
+            for (int rb = 0; rb < nchild; rb += 32) {
+              const int k = rb + lane;
+              int a = ACT_NONE;
+              uint32_t code = 0;
+              if (k < nchild) {
+                code = cur[k >> 3] | ((uint32_t)(k & 7) << (3 * (L - 2)));
+                Box rt;
+#pragma unroll
+                for (int d = 0; d < 3; d++) {
+                  rt.lo[d] = C.olo[d];
+                  rt.hi[d] = C.ohi[d];
+                }
+                const Box g = path_box(rt, code, L);
+                a = classify(P, g, L, C.ilo, C.ihi);
+                if (a >= ACT_UPPER && a != ACT_DEAD) {
+#pragma unroll
+                  for (int d = 0; d < 3; d++) {
+                    C.blo[lane][d] = g.lo[d];
+                    C.bhi[lane][d] = g.hi[d];
+                  }
+                }
+              }
+              const unsigned msplit =
+                  __ballot_sync(0xffffffffu, a == ACT_SPLIT);
+              if (msplit) {
+                const int pos = nnext + __popc(msplit & ((1u << lane) - 1));
+                if (a == ACT_SPLIT && pos < kSplitCap) nxt[pos] = code;
+                nnext += __popc(msplit);
+              }
+              const unsigned mplat =
+                  __ballot_sync(0xffffffffu, a == ACT_UPPER || a == ACT_PLAT);
+              const unsigned mfull = __ballot_sync(
+                  0xffffffffu, a == ACT_FULL || a == ACT_UPPER_FULL);
+              const unsigned mdead = __ballot_sync(0xffffffffu, a == ACT_DEAD);
+              const unsigned mup = __ballot_sync(
+                  0xffffffffu, a == ACT_UPPER || a == ACT_UPPER_FULL);
+              ev += __popc(mplat) + __popc(mfull) + __popc(mdead);
+              c_dead += __popc(mdead);
+              c_up += __popc(mup);
+              c_pl += __popc(mplat & ~mup);
+              c_full += __popc(mfull & ~mup);
+              __syncwarp();
+              for (unsigned mm = mplat; mm; mm &= mm - 1)
+                event_plateau<NO>(P, s_rt, s_rw, C, __ffs(mm) - 1, lane, V);
+              for (unsigned mm = mfull; mm; mm &= mm - 1)
+                run_full<NO>(P, s_rt, s_rw, C, __ffs(mm) - 1, y, lane,
+                             active, V);
+            }
+            __syncwarp();
+            if (nnext > kSplitCap) {
+              if (lane == 0) atomicExch(P.overflow, 1);
+              nnext = 0;
+            }
+            uint32_t *tmp = cur;
+            cur = nxt;
+            nxt = tmp;
+            nsplit = nnext;
           }
-          uint32_t *tmp = cur;
-          cur = nxt;
-          nxt = tmp;
-          nsplit = nnext;
         }
       }
       if (ev) {
@@ -396,6 +457,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
         for (int j = 0; j < 8; j++) gs += V[j];
         G += gs;
         __syncwarp();
+        const int oj = lane & 7, oi = lane >> 3;
         double b0 = 0.0, b1 = 0.0;
 #pragma unroll
         for (int q = 0; q < NQ1; q++) {
@@ -404,16 +466,18 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
           b1 = fma(s_phiw[q][oi + 4], v, b1);
         }
         __syncwarp();
+        const int64_t *mdofs = M.elem_dofs + m * M.nloc_max;
         const int64_t col = M.elem_dofs[l * M.nloc_max + oj];
         const double sc = -P.scale * jac_in;
-        P.vals[pat_index(P.pat, row0, col)] += sc * b0;
-        P.vals[pat_index(P.pat, row1, col)] += sc * b1;
+        P.vals[pat_index(P.pat, mdofs[oi], col)] += sc * b0;
+        P.vals[pat_index(P.pat, mdofs[oi + 4], col)] += sc * b1;
       }
     }
   }
   // A22 for the whole element: jac_in * sum_q1 G[q1] phiw[q1][i] phi[q1][j]
   if (active) buf[lane][8] = G;
   __syncwarp();
+  const int oj = lane & 7, oi = lane >> 3;
   double b0 = 0.0, b1 = 0.0;
 #pragma unroll
   for (int q = 0; q < NQ1; q++) {
@@ -421,24 +485,25 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
     b0 = fma(s_phiw[q][oi], gq, b0);
     b1 = fma(s_phiw[q][oi + 4], gq, b1);
   }
+  const int64_t *mdofs = M.elem_dofs + m * M.nloc_max;
   const int64_t col = mdofs[oj];
   const double sc = P.scale * jac_in;
-  P.vals[pat_index(P.pat, row0, col)] += sc * b0;
-  P.vals[pat_index(P.pat, row1, col)] += sc * b1;
+  P.vals[pat_index(P.pat, mdofs[oi], col)] += sc * b0;
+  P.vals[pat_index(P.pat, mdofs[oi + 4], col)] += sc * b1;
   if (lane == 0) {
-    unsigned long long *C = P.counters;
-    counter_add(C + MF_CNT_EVENTS, c_ev);
-    counter_add(C + MF_CNT_PAIRS, c_pairs);
-    counter_add(C + MF_CNT_EV_UPPER, c_up);
-    counter_add(C + MF_CNT_EV_PLATEAU, c_pl);
-    counter_add(C + MF_CNT_EV_DEAD, c_dead);
-    counter_add(C + MF_CNT_EV_FULL, c_full);
+    unsigned long long *Cn = P.counters;
+    counter_add(Cn + MF_CNT_EVENTS, c_ev);
+    counter_add(Cn + MF_CNT_PAIRS, c_pairs);
+    counter_add(Cn + MF_CNT_EV_UPPER, c_up);
+    counter_add(Cn + MF_CNT_EV_PLATEAU, c_pl);
+    counter_add(Cn + MF_CNT_EV_DEAD, c_dead);
+    counter_add(Cn + MF_CNT_EV_FULL, c_full);
   }
 }
 
 template <int NO, int NI>
 cudaError_t launch(const AsmParams &P, cudaStream_t s) {
-  int64_t grid = (P.n_inner + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const int64_t grid = (P.n_inner + kWarpsPerBlock - 1) / kWarpsPerBlock;
   k_hex<NO, NI><<<(unsigned)grid, kWarpsPerBlock * 32, 0, s>>>(P);
   return cudaGetLastError();
 }

@@ -1,0 +1,96 @@
+"""Multi-rank host logic of the z-slab path (gloo, world_size 2, CPU).
+
+Per-rank slab partial matrices come from the CPU oracle (the checker);
+the product code under test is the slab plan (row/value ranges), the
+interface-plane exchange and the row-block gather of parallel.py.  The
+merged result must equal the full single-process assembly bit for bit
+(each shared plane is summed as own + previous, which is how the oracle's
+serial scatter adds them only up to rounding order, hence the 1e-14 bound).
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import Golden, rel_frob
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, name, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        from paper_2101_08825_b200.assembly import HostPattern
+        from paper_2101_08825_b200.parallel import (SlabPlan, exchange_interfaces,
+                                                    gather_rows, slab_layers)
+        g = Golden(name)
+        mesh, space, kp, cfg = g.build()
+        layers = slab_layers(mesh, world)
+        A = HostPattern.for_space(mesh, space, kp, cfg)
+        plans = [SlabPlan(mesh, space, A.rowptr, layers, r)
+                 for r in range(world)]
+        plan = plans[rank]
+        inner = plan.inner_ids(mesh)
+        mask = np.zeros(mesh.n_elements, np.uint8)
+        mask[inner] = 1
+        ev = oracle.run_general(mesh, space, kp, cfg, A, inner_mask=mask)
+        a, b = plan.vals_touch
+        outside = np.concatenate([A.vals[:a], A.vals[b:]])
+        assert np.all(outside == 0.0), "slab wrote outside its row range"
+        local = torch.from_numpy(A.vals[a:b].copy())
+        exchange_interfaces(local, plan)
+        full = gather_rows(local, plan, plans, A.nnz)
+        evs = torch.tensor([ev], dtype=torch.int64)
+        dist.all_reduce(evs)
+        if rank == 0:
+            out_q.put((full.numpy() * 2.0, int(evs.item()), layers))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["hex_q1_gl3", "tri_p1_lmax3",
+                                  "quad_q2_lmax2"])
+def test_slab_exchange_and_gather_gloo(name, oracle_lib):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, name, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    vals, events, layers = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    g = Golden(name)
+    assert events == int(g["events"])
+    assert rel_frob(vals, g["vals"]) <= 1e-14
+    assert layers[0][0] == 0 and layers[-1][1] > layers[0][1]
+
+
+def test_slab_layers_balanced():
+    from paper_2101_08825_b200 import build_mesh
+    from paper_2101_08825_b200.parallel import slab_layers
+    mesh = build_mesh(3, ((0, 0.5),) * 3, 1 / 32, 0.1, "hex")
+    for world in (1, 2, 4, 8):
+        L = slab_layers(mesh, world)
+        assert L[0][0] == 0 and L[-1][1] == mesh.grid_ncells[2]
+        assert all(a < b for a, b in L)
+        assert all(L[i][1] == L[i + 1][0] for i in range(world - 1))
+        sizes = [b - a for a, b in L]
+        assert max(sizes) - min(sizes) <= 1
