@@ -18,9 +18,10 @@ A = 2(A21 + A22) for the workload.
 Default workload R4 = BASELINE config #4 stand-in (3D hex Q1, 64^3 cells,
 delta=0.1, eps=h/2, kappa=2, GL3, L_max=2).  Multi-GPU:
 inner elements are split into z-slabs balanced by pair count, one per rank;
-each rank assembles the rows its slab owns (no data-path collective; the
-slab partial matrices are exchanged only by the row-block gather of
-`parallel.py`, outside the timed kernel region).
+each rank assembles the rows its slab touches; the timed step includes the
+one interface-plane send/recv per slab boundary (parallel.py).  e2e at N>1
+is `assemble_distributed` (upload, slab assembly, exchange, NCCL row-block
+gather to rank 0, D2H on rank 0).
 
 The CPU leg (cpu_baseline / --impl reference) times the oracle
 (oracle/mf_oracle.c, the C restatement of the reference numba cores) on a
@@ -64,6 +65,12 @@ CONFIGS = {
 }
 
 METRIC = "interacting element-pairs/sec (full nonlocal stiffness assembly)"
+
+# total candidate pairs per workload (GPU counters; R1/R4-small are
+# re-checked against the oracle's _candidates count in tests/test_bench.py)
+PAIRS = {"R1": 462400, "R3-2h": 52243984, "R3-4h": 130507776,
+         "R3-8h": 398401600, "R3-16h": 1414361664, "R4": 1382469544,
+         "R4-gauss2": 1382469544, "R4-small": 61162984, "R5": None}
 
 
 def build_problem(name):
@@ -268,12 +275,14 @@ def run_reference(args):
         return
     name = args.config
     mesh, space, kp, cfg = build_problem(name)
-    n = mesh.n_elements
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle
-    ptr, _ = oracle.candidates(mesh, kp.delta + kp.eps, np.arange(n),
-                               np.ones(n, np.uint8))
-    total_pairs = int(ptr[-1])
+    total_pairs = PAIRS.get(name)
+    if total_pairs is None:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle
+        n = mesh.n_elements
+        ptr, _ = oracle.candidates(mesh, kp.delta + kp.eps, np.arange(n),
+                                   np.ones(n, np.uint8))
+        total_pairs = int(ptr[-1])
     vals = []
     for i in range(args.warmup + args.steps):
         r = cpu_sample(name, mesh, space, kp, cfg, budget_s=args.cpu_budget,
@@ -301,19 +310,6 @@ def run_reference(args):
 # --------------------------------------------------------------------------
 # GPU leg
 
-def slab_inner_ids(mesh, rank, world, pairs_per_elem):
-    """z-slab (y-slab in 2D) of inner elements balanced by pair count."""
-    axis = mesh.dim - 1
-    layer = mesh.elem_cell[:, axis]
-    nl = int(layer.max()) + 1
-    w = np.bincount(layer, weights=pairs_per_elem, minlength=nl)
-    cum = np.cumsum(w) / w.sum()
-    cuts = [0] + [int(np.searchsorted(cum, (r + 1) / world, side="left")) + 1
-                  for r in range(world - 1)] + [nl]
-    lo, hi = cuts[rank], cuts[rank + 1]
-    return np.nonzero((layer >= lo) & (layer < hi))[0], (lo, hi)
-
-
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -332,40 +328,57 @@ def run_ours(args):
 
     name = args.config
     mesh, space, kp, cfg = build_problem(name)
-    ctx = AssemblyContext(mesh, space, kp, cfg, dev)
-    A = ctx.new_matrix()
-    n = mesh.n_elements
-    slab = None
-    if world > 1:
-        # per-element pair counts (GPU neighbour search) for balancing
-        from paper_2101_08825_b200.assembly import candidates
-        ptr, _ = candidates(mesh, kp.delta + kp.eps, np.arange(n),
-                            np.ones(n, np.uint8), dmesh=ctx.dmesh)
-        inner, (zlo, zhi) = slab_inner_ids(mesh, rank, world, np.diff(ptr))
-        slab = {"slab_layers": [zlo, zhi]}
-    else:
-        inner = None
-    plan = ColorPlan(mesh, inner, dev)
-    counters = torch.zeros(N.MF_NCOUNTERS, dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream()
+    slab = None
+    if world == 1:
+        ctx = AssemblyContext(mesh, space, kp, cfg, dev)
+        A = ctx.new_matrix()
+        plan = ColorPlan(mesh, None, dev)
+        counters = torch.zeros(N.MF_NCOUNTERS, dtype=torch.int64, device=dev)
+        n_launch = np.count_nonzero(np.diff(plan.color_ptr)) + 1
+
+        def work():
+            A._dvals.zero_()
+            counters.zero_()
+            ctx.run(A, plan=plan, counters=counters)
+
+        def finish():
+            ctx.finish(A, counters)
+            return A.counters
+    else:
+        from paper_2101_08825_b200.device import DeviceMesh
+        from paper_2101_08825_b200.parallel import SlabAssembler, pair_counts
+        w = pair_counts(mesh, kp, DeviceMesh(mesh, space, dev))
+        sa = SlabAssembler(mesh, space, kp, cfg, rank, world, dev, weights=w)
+        ctx = sa.ctx
+        plan = sa.color_plan
+        slab = {"slab_layers": [list(x) for x in sa.layers],
+                "interface_plane_bytes": int(
+                    (sa.plan.send_range[1] - sa.plan.send_range[0]) * 8
+                    if sa.plan.send_range else 0)}
+        n_launch = np.count_nonzero(np.diff(plan.color_ptr))
+
+        def work():
+            sa.assemble_local()
+            sa.exchange()
+
+        def finish():
+            return sa.counters.cpu().numpy()
 
     def step():
-        A._dvals.zero_()
-        counters.zero_()
         s = torch.cuda.Event(enable_timing=True)
         e = torch.cuda.Event(enable_timing=True)
         s.record(stream)
-        ctx.run(A, plan=plan, counters=counters)
+        work()
         e.record(stream)
-        ctx.finish(A, counters)
-        return s, e
+        cnt = finish()
+        return s, e, cnt
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    kern_ms = []
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         t0 = torch.cuda.Event(enable_timing=True)
@@ -377,8 +390,8 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     ms = t0.elapsed_time(t1) / args.steps
-    kern_ms = [s.elapsed_time(e) for s, e in evs]
-    cnt = A.counters
+    kern_ms = [s.elapsed_time(e) for s, e, _ in evs]
+    cnt = evs[-1][2]
     pairs = int(cnt[N.CNT_PAIRS])
     if world > 1:
         t = torch.tensor([ms, float(pairs)], dtype=torch.float64, device=dev)
@@ -393,23 +406,38 @@ def run_ours(args):
 
     # ---- end to end through the public API (host in, host out) --------
     e2e = None
-    if world == 1 and not args.no_e2e:
-        for _ in range(1):
-            B = assemble(mesh, space, kp, cfg, device=dev)
+    if not args.no_e2e:
+        from paper_2101_08825_b200.parallel import assemble_distributed
+
+        def api_call():
+            if world == 1:
+                return assemble(mesh, space, kp, cfg, device=dev)
+            return assemble_distributed(mesh, space, kp, cfg)
+
+        B = api_call()
         del B
         torch.cuda.synchronize()
-        t = time.perf_counter()
+        if world > 1:
+            dist.barrier()
         e2e_steps = max(1, min(args.steps, args.e2e_steps))
+        t = time.perf_counter()
         for _ in range(e2e_steps):
-            B = assemble(mesh, space, kp, cfg, device=dev)
-            _ = B.vals[-1]
+            B = api_call()
+            if B is not None:
+                _ = B.vals[-1]
         torch.cuda.synchronize()
         e2e_s = (time.perf_counter() - t) / e2e_steps
-        h2d = ctx.h2d_bytes + plan.h2d_bytes
+        if world > 1:
+            tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_s = float(tt[0])
+        from paper_2101_08825_b200.device import DeviceMesh
+        h2d = (ctx.h2d_bytes + plan.h2d_bytes) * world
+        nnz = int(np.asarray(ctx_nnz(mesh, space, kp, cfg)))
         e2e = {"value": pairs_all / e2e_s, "unit": "pairs/s",
                "seconds_per_assembly": e2e_s,
                "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(B.nnz * 8 + 8 * N.MF_NCOUNTERS)}
+               "d2h_bytes_per_step": int(nnz * 8 + 8 * N.MF_NCOUNTERS)}
         del B
 
     if rank != 0:
@@ -427,6 +455,7 @@ def run_ours(args):
         "ms_per_step": ms_all, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (structured mesh, reference-realisable stand-in)",
+        "kernel_ms_per_step": statistics.mean(kern_ms),
         "config": config_json(name, mesh, space, world, slab),
         "events": int(cnt[N.CNT_EVENTS]), "pairs": pairs_all,
         "event_classes": {"upper_plateau": int(cnt[N.CNT_EV_UPPER]),
@@ -443,8 +472,7 @@ def run_ours(args):
                      "canonical_flops": canonical,
                      "canonical_tflops_equiv": canonical / (kms * 1e-3)
                      / 1e12},
-        "gpu_launches": int(args.steps * (np.count_nonzero(
-            np.diff(plan.color_ptr)) + 1)),
+        "gpu_launches": int(args.steps * n_launch),
         "clocks": clk.summary(),
     }
     if e2e:
@@ -455,6 +483,12 @@ def run_ours(args):
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def ctx_nnz(mesh, space, kp, cfg):
+    from paper_2101_08825_b200.assembly import HostPattern, pattern_halfwidth
+    K, _ = pattern_halfwidth(mesh, kp, cfg, space.degree)
+    return int(HostPattern(space, K, allocate=False).rowptr[-1])
 
 
 def load_traffic(name):
@@ -474,7 +508,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="R4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

@@ -148,6 +148,17 @@ int mf_diag(const MfPattern *pat, const double *vals, double *out,
 int mf_symmetrize(const MfPattern *pat, double *vals, void *stream);
 int mf_fill_cols(const MfPattern *pat, int64_t *cols, void *stream);
 
+/* Load vector (assemble_rhs's _group_load, assembly.py:641-676): for each
+ * element e = elems[k] (colour-grouped like mf_general_core; color_ptr is
+ * HOST memory), load[dofs[e,i]] += |J_e| sum_q fval[k*nq + q] w[q] phi[q,i]
+ * with |J| = det (triangles) or prod 0.5*(hi-lo) (boxes).  fval holds the
+ * caller's f at the physical rule points of elements[k] (host callables
+ * are evaluated by the caller).  All elements must share one kind. */
+int mf_load_scatter(const MfMesh *mesh, const int32_t *elems,
+                    const int64_t *color_ptr, int32_t ncolors,
+                    const double *fval, const double *w, const double *phi,
+                    int32_t nq, int32_t nloc, double *load, void *stream);
+
 /* FP64 roofline probe: independent DFMA chains; out = device double[1]
  * (sink).  Time it with events to get the sustained DFMA rate. */
 int mf_fp64_probe(double *out, int64_t iters, int32_t blocks,

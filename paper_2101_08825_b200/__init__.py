@@ -8,7 +8,8 @@ CUDA through the C-ABI in include/mollifem_b200.h.
 """
 
 from .assembly import (AssemblyConfig, NeighborSets, SparseMatrix,
-                       aprx_max_dist, aprx_min_dist, assemble, neighbor_sets,
+                       aprx_max_dist, aprx_min_dist, assemble, assemble_rhs,
+                       neighbor_sets,
                        pattern_halfwidth)
 from .fe_space import (FESpace, eval_basis, eval_shape_functions,
                        interpolate, l2_error, lifting)
@@ -16,6 +17,7 @@ from .kernel import (KernelParams, gamma_eps, mollifier, scaling_c_delta,
                      scaling_c_delta_eps, xi)
 from .mesh import (BoundingBox, Mesh, PartitionMap, build_mesh,
                    partition_geometric, refine)
+from .solver import SolveReport, solve
 from .quadrature import (QuadratureRule, dunavant7, gauss_legendre_1d,
                          gauss_lobatto_1d, map_to_physical, rule_for_kind,
                          tensor_product)
@@ -25,10 +27,11 @@ __version__ = "0.1.0"
 __all__ = [
     "AssemblyConfig", "BoundingBox", "FESpace", "KernelParams", "Mesh",
     "NeighborSets", "PartitionMap", "QuadratureRule", "SparseMatrix",
-    "aprx_max_dist", "aprx_min_dist", "assemble", "build_mesh", "dunavant7",
+    "aprx_max_dist", "aprx_min_dist", "assemble", "assemble_rhs",
+    "build_mesh", "dunavant7",
     "eval_basis", "eval_shape_functions", "gamma_eps", "gauss_legendre_1d",
     "gauss_lobatto_1d", "interpolate", "l2_error", "lifting",
     "map_to_physical", "mollifier", "neighbor_sets", "partition_geometric",
     "pattern_halfwidth", "refine", "rule_for_kind", "scaling_c_delta",
-    "scaling_c_delta_eps", "tensor_product", "xi",
+    "scaling_c_delta_eps", "solve", "SolveReport", "tensor_product", "xi",
 ]

@@ -77,6 +77,8 @@ _SIGS = {
     "mf_diag": (C.c_int, [C.POINTER(MfPattern), _P, _P, _P]),
     "mf_symmetrize": (C.c_int, [C.POINTER(MfPattern), _P, _P]),
     "mf_fill_cols": (C.c_int, [C.POINTER(MfPattern), _P, _P]),
+    "mf_load_scatter": (C.c_int, [C.POINTER(MfMesh), _P, _P, C.c_int32, _P,
+                                  _P, _P, C.c_int32, C.c_int32, _P, _P]),
     "mf_fp64_probe": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_int32, _P]),
     "mf_fp64_probe_flops": (C.c_double, [C.c_int64, C.c_int32, C.c_int32]),
     "mf_last_error": (C.c_char_p, []),

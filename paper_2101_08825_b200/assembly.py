@@ -599,3 +599,95 @@ def assemble(mesh, space, kernel, config=None, *, device=None, flags=0,
     if not keep_on_device:
         A._vals = _d2h(A._dvals)
     return A
+
+
+# ---------------------------------------------------------------------------
+# load vector (assembly.py:641-691)
+
+def _load_points(mesh, space, sel, code):
+    """Physical rule points of elements `sel` of kind `code` and the rule
+    (GL(degree+2) on boxes, Dunavant on triangles; assembly.py:648-669)."""
+    from .fe_space import eval_shape_functions
+    deg = space.degree
+    box_kind = "hex" if mesh.dim == 3 else "quad"
+    if code == 1:
+        rule = rule_for_kind("tri", "default")
+        kname = "tri"
+        v = mesh.elem_coords[sel, :3, :]
+        e1 = v[:, 1] - v[:, 0]
+        e2 = v[:, 2] - v[:, 0]
+        r = rule.ref_points
+        pts = (v[:, None, 0, :] + r[None, :, 0, None] * e1[:, None, :]
+               + r[None, :, 1, None] * e2[:, None, :])
+    else:
+        rule = rule_for_kind(box_kind, "gauss" + str(deg + 2))
+        kname = box_kind
+        lo = mesh.elem_lo[sel]
+        hi = mesh.elem_hi[sel]
+        r = rule.ref_points
+        pts = lo[:, None, :] + (r[None, :, :] + 1.0) * 0.5 * (hi - lo)[:, None, :]
+    PHI = eval_shape_functions(kname, deg, rule.ref_points)
+    return pts, rule, PHI
+
+
+def group_load_device(mesh, space, f, element_ids, dmesh, device=None):
+    """(int_Omega f phi) for `element_ids` as a device vector
+    (_group_load, assembly.py:641-676): f is evaluated on the host at the
+    rule points, the contraction and the colour-scheduled scatter run in
+    mf_load_scatter."""
+    import torch
+    from . import _native as N
+    from .device import ColorPlan, color_of, to_device
+    L = N.lib()
+    dev = dmesh.device
+    load = torch.zeros(space.n_dofs, dtype=torch.float64, device=dev)
+    kinds = mesh.elem_kind
+    col = color_of(mesh)
+    for code in (0, 1, 2):
+        sel = element_ids[kinds[element_ids] == code]
+        if len(sel) == 0:
+            continue
+        sel = sel[np.argsort(col[sel], kind="stable")]
+        pts, rule, PHI = _load_points(mesh, space, sel, code)
+        fv = np.asarray(f(pts.reshape(-1, mesh.dim)), dtype=float)
+        fv = np.ascontiguousarray(np.broadcast_to(
+            fv, (pts.shape[0] * pts.shape[1],)).reshape(len(sel), len(rule)))
+        counts = np.bincount(col[sel], minlength=ColorPlan.NCOLORS)
+        cptr = np.zeros(ColorPlan.NCOLORS + 1, dtype=np.int64)
+        np.cumsum(counts, out=cptr[1:])
+        elems = to_device(sel.astype(np.int32), dev)
+        fvd = to_device(fv, dev)
+        wd = to_device(np.ascontiguousarray(rule.weights), dev)
+        phid = to_device(np.ascontiguousarray(PHI), dev)
+        N.check(L.mf_load_scatter(
+            C_byref(dmesh.struct), N.ptr(elems),
+            cptr.ctypes.data_as(ctypes_void_p()), ColorPlan.NCOLORS,
+            N.ptr(fvd), N.ptr(wd), N.ptr(phid), len(rule), PHI.shape[1],
+            N.ptr(load), N.stream_ptr()), "mf_load_scatter")
+    return load
+
+
+def assemble_rhs(mesh, space, kernel, f, g, A):
+    """rhs = (int_Omega f phi)[free] - (A gt)[free] (assembly.py:679-691).
+
+    gt is the nodal interpolant of g on constrained DOFs (callable, or an
+    array over all DOFs / constrained DOFs), zero elsewhere."""
+    import torch
+    from . import _native as N
+    from .device import DeviceMesh, to_device
+    dmesh = DeviceMesh(mesh, space)
+    load = group_load_device(mesh, space, f, mesh.omega_element_ids(), dmesh)
+    gt = np.zeros(space.n_dofs)
+    if callable(g):
+        gt[space.constrained] = g(space.dof_coords[space.constrained])
+    else:
+        gv = np.asarray(g, dtype=float)
+        gt[space.constrained] = (gv[space.constrained]
+                                 if gv.shape == (space.n_dofs,) else gv)
+    gtd = to_device(gt, dmesh.device)
+    y = torch.empty_like(gtd)
+    N.check(N.lib().mf_matvec(C_byref(A._pattern_struct()),
+                              N.ptr(A.vals_device), N.ptr(gtd), N.ptr(y),
+                              N.stream_ptr()), "mf_matvec")
+    free = to_device(np.asarray(space.free, dtype=np.int64), dmesh.device)
+    return (load[free] - y[free]).cpu().numpy()

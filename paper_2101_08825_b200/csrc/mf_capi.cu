@@ -35,6 +35,9 @@ cudaError_t mf_launch_diag(const MfPattern &, const double *, double *,
                            cudaStream_t);
 cudaError_t mf_launch_scale(double *, int64_t, double, cudaStream_t);
 cudaError_t mf_launch_probe(double *, int64_t, int, int, cudaStream_t);
+cudaError_t mf_launch_load(const MfMesh &, const int32_t *, int64_t,
+                           const double *, const double *, const double *,
+                           int, int, double *, cudaStream_t);
 
 namespace {
 
@@ -286,6 +289,26 @@ int mf_fill_cols(const MfPattern *pat, int64_t *cols, void *stream) {
   if (!cols) return fail(MF_ERR_ARG, "NULL array");
   return cuda_status(mf_launch_fill_cols(*pat, cols, S(stream)),
                      "mf_fill_cols");
+}
+
+int mf_load_scatter(const MfMesh *mesh, const int32_t *elems,
+                    const int64_t *color_ptr, int32_t ncolors,
+                    const double *fval, const double *w, const double *phi,
+                    int32_t nq, int32_t nloc, double *load, void *stream) {
+  if (int rc = check_mesh(mesh)) return rc;
+  if (!color_ptr || ncolors < 1 || nq < 1 || nloc < 1 ||
+      nloc > mesh->nloc_max)
+    return fail(MF_ERR_ARG, "bad load arguments");
+  if (color_ptr[ncolors] > 0 && (!elems || !fval || !w || !phi || !load))
+    return fail(MF_ERR_ARG, "NULL array");
+  for (int c = 0; c < ncolors; c++) {
+    const int64_t a = color_ptr[c], n = color_ptr[c + 1] - a;
+    if (n <= 0) continue;
+    cudaError_t e = mf_launch_load(*mesh, elems + a, n, fval + a * nq, w, phi,
+                                   nq, nloc, load, S(stream));
+    if (e != cudaSuccess) return cuda_status(e, "mf_load_scatter");
+  }
+  return MF_OK;
 }
 
 int mf_fp64_probe(double *out, int64_t iters, int32_t blocks,

@@ -184,6 +184,12 @@ MF_DEV void event_full(const AsmParams &P, const double *s_rt,
   for (int j = 0; j < 2; j++)
 #pragma unroll
     for (int a = 0; a < NO; a++) shx[j][a] = C.sh[0][j][a];
+  // (dx^2 + dy^2) once per (a, b): the reference's association order
+  double sxy[NO][NO];
+#pragma unroll
+  for (int b = 0; b < NO; b++)
+#pragma unroll
+    for (int a = 0; a < NO; a++) sxy[b][a] = xadd(sq[0][a], sq[1][b]);
 #pragma unroll 1
   for (int c = 0; c < NO; c++) {
     double Tb[2][NO];
@@ -194,7 +200,7 @@ MF_DEV void event_full(const AsmParams &P, const double *s_rt,
       bool anysh = false;
 #pragma unroll
       for (int a = 0; a < NO; a++) {
-        const double d2 = xadd(xadd(sq[0][a], sq[1][b]), sq[2][c]);
+        const double d2 = xadd(sxy[b][a], sq[2][c]);
         if (SHARP) {
           mu[a] = d2 < P.dp2 ? 256.0 : 0.0;
           shl[a] = false;

@@ -139,6 +139,34 @@ __global__ void k_probe(double *out, int64_t iters) {
   if (s == 12345.678) out[0] = s;  // keep the chains alive
 }
 
+// one thread per element of a colour: contract f*w*|J| with the shapes and
+// add into the element's DOFs (race-free inside a colour)
+__global__ void k_load(MfMesh M, const int32_t *elems, int64_t n,
+                       const double *fval, const double *w, const double *phi,
+                       int nq, int nloc, double *load) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int64_t e = elems[k];
+  const int dim = M.dim;
+  double det;
+  if (M.elem_kind[e] == 1) {
+    const double *c = M.elem_coords + e * M.nv_max * dim;
+    const double e10 = c[dim] - c[0], e11 = c[dim + 1] - c[1];
+    const double e20 = c[2 * dim] - c[0], e21 = c[2 * dim + 1] - c[1];
+    det = e10 * e21 - e11 * e20;
+  } else {
+    det = 1.0;
+    for (int a = 0; a < dim; a++)
+      det *= 0.5 * (M.elem_hi[e * dim + a] - M.elem_lo[e * dim + a]);
+  }
+  const double *fv = fval + k * nq;
+  for (int i = 0; i < nloc; i++) {
+    double s = 0.0;
+    for (int q = 0; q < nq; q++) s += fv[q] * w[q] * phi[q * nloc + i];
+    load[M.elem_dofs[e * M.nloc_max + i]] += det * s;
+  }
+}
+
 int rows_grid(int64_t n) {
   int64_t want = (n * 32 + 255) / 256;
   return (int)(want < 148 * 32 ? (want > 0 ? want : 1) : 148 * 32);
@@ -186,6 +214,15 @@ cudaError_t mf_launch_scale(double *v, int64_t n, double sc, cudaStream_t s) {
     k_scale<<<(int)(want < 148 * 64 ? want : 148 * 64), 256, 0, s>>>(v, n,
                                                                      sc);
   }
+  return cudaGetLastError();
+}
+cudaError_t mf_launch_load(const MfMesh &M, const int32_t *elems, int64_t n,
+                           const double *fval, const double *w,
+                           const double *phi, int nq, int nloc, double *load,
+                           cudaStream_t s) {
+  if (n > 0)
+    k_load<<<(int)((n + 127) / 128), 128, 0, s>>>(M, elems, n, fval, w, phi,
+                                                   nq, nloc, load);
   return cudaGetLastError();
 }
 cudaError_t mf_launch_probe(double *out, int64_t iters, int blocks,

@@ -361,3 +361,53 @@ def emulate_slabs(mesh, space, kernel, config, world, device=None):
         base = s.plan.vals_touch[0]
         full[a:b] = s.local[a - base:b - base]
     return full, events
+
+
+def pair_counts(mesh, params, dmesh):
+    """Candidate-pair count per element (the count pass of the GPU
+    neighbour search, mf_count_candidates) -- the slab balancing weight."""
+    import ctypes
+
+    import torch
+
+    from . import _native as N
+    from .assembly import stencil_radius
+    n = mesh.n_elements
+    dev = dmesh.device
+    outer = torch.arange(n, dtype=torch.int64, device=dev)
+    mask = torch.ones(n, dtype=torch.uint8, device=dev)
+    counts = torch.empty(n, dtype=torch.int64, device=dev)
+    reach = params.delta + params.eps
+    N.check(N.lib().mf_count_candidates(
+        ctypes.byref(dmesh.struct), N.ptr(outer), n, N.ptr(mask),
+        stencil_radius(reach, mesh.h), float(reach), N.ptr(counts),
+        N.stream_ptr()), "mf_count_candidates")
+    return counts.cpu().numpy()
+
+
+def assemble_distributed(mesh, space, kernel, config=None, group=None,
+                         dst=0, weights=None):
+    """Multi-GPU `assemble`: every rank of the process group calls it with
+    the same host inputs; rank `dst` returns the full SparseMatrix (host
+    values, events, presym_asymmetry), the others return None."""
+    import torch
+    import torch.distributed as dist
+
+    from .assembly import _d2h
+    config = config or AssemblyConfig()
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    s = SlabAssembler(mesh, space, kernel, config, rank, world, dev,
+                      weights=weights)
+    cnt = s.assemble_local().clone()
+    s.exchange(group)
+    full = s.gather(group, dst)
+    dist.all_reduce(cnt, group=group)
+    if rank != dst:
+        return None
+    A = s.A
+    A._dvals = full * 2.0
+    s.ctx.finish(A, cnt)
+    A._vals = _d2h(A._dvals)
+    return A

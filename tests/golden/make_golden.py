@@ -115,6 +115,11 @@ def run_case(name, spec):
             f = lambda x: np.full(x.shape[:-1], -6.0 * kappa)
             u = lambda x: x[..., 0] ** 2 + x[..., 1] ** 2 + x[..., 2] ** 2
         out["rhs"] = R.assemble_rhs(mesh, space, kp, f, u, A)
+        # solver.py:26-90 on the reference matrix ("same solved u" check)
+        uh, rep = R.solve(A, out["rhs"], space.free, space.constrained,
+                          u(space.dof_coords[space.constrained]))
+        out["u"] = uh
+        out["u_iters"] = np.int64(rep.iterations)
     np.savez_compressed(os.path.join(HERE, name + ".npz"), **out)
     print(f"{name}: n_elem={n} pairs={ptr[-1]} events={A.events} "
           f"nnz={A.nnz}", flush=True)

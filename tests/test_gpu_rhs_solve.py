@@ -1,0 +1,66 @@
+"""Load vector (assemble_rhs) and the solved u on the GPU vs the reference.
+
+North star: "same solved u to within 1e-8".  The golden rhs / u are the
+reference's assemble_rhs + solve (solver.py:26-90) on its own matrix
+(tests/golden/make_golden.py), with the harness's manufactured data
+u = |x|^2, f = -2 dim kappa (harness.py:92-95).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import Golden
+
+pytestmark = pytest.mark.gpu
+
+CASES = ["tri_p1_lmax3", "quad_q1_lmax3", "quad_q2_lmax2", "hex_q1_gl3"]
+
+
+def _data(dim, kappa):
+    f = lambda x: np.full(x.shape[:-1], -2.0 * dim * kappa)
+    u = lambda x: (x ** 2).sum(axis=-1)
+    return f, u
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_rhs_and_solution_match_reference(name):
+    from paper_2101_08825_b200 import assemble, assemble_rhs, solve
+    g = Golden(name)
+    mesh, space, kp, cfg = g.build()
+    f, u = _data(mesh.dim, kp.kappa)
+    A = assemble(mesh, space, kp, cfg)
+    rhs = assemble_rhs(mesh, space, kp, f, u, A)
+    ref = g["rhs"]
+    assert rhs.shape == ref.shape
+    assert np.abs(rhs - ref).max() <= 1e-12 * np.abs(ref).max()
+    uh, rep = solve(A, rhs, space.free, space.constrained,
+                    u(space.dof_coords[space.constrained]))
+    assert rep.converged and rep.final_residual <= 1e-12
+    assert np.abs(uh - g["u"]).max() <= 1e-8
+    assert abs(rep.iterations - int(g["u_iters"])) <= 2
+
+
+def test_rhs_zero_data_and_lifting_sign():
+    """test_assembly.py:177-195: zero data -> zero rhs; f = 0 -> -(A g)."""
+    from paper_2101_08825_b200 import assemble, assemble_rhs, lifting
+    g = Golden("quad_q1_lmax3")
+    mesh, space, kp, cfg = g.build()
+    A = assemble(mesh, space, kp, cfg)
+    zero = lambda x: np.zeros(x.shape[:-1])
+    rhs = assemble_rhs(mesh, space, kp, zero, zero, A)
+    assert rhs.shape == (space.free.size,) and np.all(rhs == 0.0)
+    gx = lambda x: x[..., 0]
+    rhs = assemble_rhs(mesh, space, kp, zero, gx, A)
+    assert np.allclose(rhs, -(A @ lifting(space, gx))[space.free],
+                       atol=1e-14)
+
+
+def test_solver_rejects_indefinite():
+    from paper_2101_08825_b200 import assemble, solve
+    g = Golden("quad_q1_lmax3")
+    mesh, space, kp, cfg = g.build()
+    A = assemble(mesh, space, kp, cfg)
+    A.vals = -A.vals
+    with pytest.raises(RuntimeError):
+        solve(A, np.ones(space.free.size), space.free, space.constrained,
+              np.zeros(space.constrained.size))
