@@ -134,6 +134,36 @@ int mf_general_core(const MfMesh *mesh, const MfRules *rules,
                     int32_t flags, void *workspace, size_t ws_bytes,
                     void *stream);
 
+/* Offset-blocked strategy, the reference default on pure meshes
+ * (strategy "auto"/"blocked", assembly.py:391-437).  mf_offset_blocks runs
+ * Algorithm 1 once per (cell offset d in [-R,R]^dim, outer proto t2, inner
+ * proto t1) on the reference's synthetic geometry (_build_offset_blocks,
+ * _kernels.py:490-594); block bi = (((dz*S + dy)*S + dx)*np + t2)*np + t1
+ * with S = 2R+1 (offsets shifted by R), B21/B22 are (nblk, nloc, nloc),
+ * bev the per-block event count (0 = absent block).  protos: device
+ * (nproto, 3, 2) triangle protos in cell units (NULL for boxes).
+ * mf_scatter_offset_blocks adds every realised (inner element, block)
+ * (_scatter_offset_blocks, _kernels.py:597-647): blk lists the present
+ * blocks grouped by inner proto, blk_ptr (HOST int64[nproto+1]) delimits
+ * the groups; A22 blocks are summed per inner element; counters get the
+ * realised events and pairs. */
+int64_t mf_offset_block_count(int32_t dim, int32_t nproto, int32_t R);
+size_t mf_offset_blocks_workspace_bytes(const MfRules *rules, int64_t nblk);
+int mf_offset_blocks(const MfMesh *mesh, const MfRules *rules,
+                     const MfKernel *kern, int32_t kind, int32_t nproto,
+                     const double *protos, int32_t R, double h, double *B21,
+                     double *B22, uint64_t *bev, int32_t flags,
+                     void *workspace, size_t ws_bytes, void *stream);
+int mf_scatter_offset_blocks(const MfMesh *mesh, const MfPattern *pat,
+                             int32_t nproto, int32_t R, const int32_t *blk,
+                             const int64_t *blk_ptr, const double *B21,
+                             const double *B22, const uint64_t *bev,
+                             const uint8_t *outer_mask,
+                             const int32_t *inner_sorted,
+                             const int64_t *color_ptr, int32_t ncolors,
+                             double scale, double *vals, uint64_t *counters,
+                             void *stream);
+
 /* Matrix utilities on the implicit pattern (_kernels.py:846-1202). */
 int mf_scale(double *vals, int64_t nnz, double s, void *stream);
 /* out: device double[1]; max over rows of sum_c |A_rc - A_cr| */

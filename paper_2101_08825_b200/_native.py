@@ -70,6 +70,18 @@ _SIGS = {
                                   _P, _P, _P, C.c_int32, C.c_int32,
                                   C.c_double, _P, _P, C.c_int32, _P,
                                   C.c_size_t, _P]),
+    "mf_offset_block_count": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32]),
+    "mf_offset_blocks_workspace_bytes": (C.c_size_t, [C.POINTER(MfRules),
+                                                      C.c_int64]),
+    "mf_offset_blocks": (C.c_int, [C.POINTER(MfMesh), C.POINTER(MfRules),
+                                   C.POINTER(MfKernel), C.c_int32, C.c_int32,
+                                   _P, C.c_int32, C.c_double, _P, _P, _P,
+                                   C.c_int32, _P, C.c_size_t, _P]),
+    "mf_scatter_offset_blocks": (C.c_int, [C.POINTER(MfMesh),
+                                           C.POINTER(MfPattern), C.c_int32,
+                                           C.c_int32, _P, _P, _P, _P, _P, _P,
+                                           _P, _P, C.c_int32, C.c_double, _P,
+                                           _P, _P]),
     "mf_scale": (C.c_int, [_P, C.c_int64, C.c_double, _P]),
     "mf_asymmetry_inf": (C.c_int, [C.POINTER(MfPattern), _P, _P, _P]),
     "mf_norm_inf": (C.c_int, [C.POINTER(MfPattern), _P, _P, _P]),

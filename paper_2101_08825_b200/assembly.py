@@ -33,10 +33,8 @@ __all__ = ["AssemblyConfig", "SparseMatrix", "NeighborSets", "assemble",
 class AssemblyConfig:
     """Method, recursion window [L_min, L_max], rule presets, strategy.
 
-    Validation follows assembly.py:58-78.  strategy "auto"/"general"/
-    "blocked" are all accepted; on the device every strategy runs the
-    per-pair general kernel (the blocked CPU shortcut is a host
-    optimisation of the same matrix, assembly.py:391-437).
+    Validation follows assembly.py:58-78; strategies as in the reference
+    ("auto" = blocked on pure meshes, general otherwise).
     """
 
     def __init__(self, method="mollified_adaptive", L_min=1, L_max=3,
@@ -535,6 +533,59 @@ class AssemblyContext:
             N.ptr(ws), wsb, N.stream_ptr()), "mf_general_core")
         return counters
 
+    def run_blocked(self, A, scale=2.0, counters=None):
+        """Offset-blocked strategy (assembly.py:391-437) on the device:
+        mf_offset_blocks + mf_scatter_offset_blocks."""
+        import torch
+        from . import _native as N
+        from .device import ColorPlan, to_device
+        L = N.lib()
+        mesh, space = self.mesh, self.space
+        kind = mesh.kind
+        kcode = {"quad": 0, "tri": 1, "hex": 2}[kind]
+        nproto = 2 if kind == "tri" else 1
+        nloc = 3 * space.degree if kind == "tri" else \
+            (space.degree + 1) ** mesh.dim
+        R = A._offset_reach
+        dev = self.device
+        nblk = int(L.mf_offset_block_count(mesh.dim, nproto, R))
+        B21 = torch.empty(nblk * nloc * nloc, dtype=torch.float64, device=dev)
+        B22 = torch.empty_like(B21)
+        bev = torch.zeros(nblk, dtype=torch.int64, device=dev)
+        protos = (to_device(_TRI_PROTOS, dev) if kind == "tri" else None)
+        wsb = int(L.mf_offset_blocks_workspace_bytes(
+            C_byref(self.drules.struct), nblk))
+        ws = torch.zeros(wsb, dtype=torch.uint8, device=dev)
+        st = N.stream_ptr()
+        N.check(L.mf_offset_blocks(
+            C_byref(self.dmesh.struct), C_byref(self.drules.struct),
+            C_byref(self.kernel_struct()), kcode, nproto, N.ptr(protos), R,
+            float(mesh.h), N.ptr(B21), N.ptr(B22), N.ptr(bev), 0, N.ptr(ws),
+            wsb, st), "mf_offset_blocks")
+        ev = bev.cpu().numpy()
+        ids = np.nonzero(ev > 0)[0]
+        t1 = ids % nproto
+        order = np.argsort(t1, kind="stable")
+        blk = ids[order].astype(np.int32)
+        blk_ptr = np.searchsorted(t1[order], np.arange(nproto + 1)).astype(
+            np.int64)
+        blk_d = to_device(blk if blk.size else np.zeros(1, np.int32), dev)
+        plan = ColorPlan(mesh, None, dev)
+        om = torch.ones(mesh.n_elements, dtype=torch.uint8, device=dev)
+        if counters is None:
+            counters = torch.zeros(N.MF_NCOUNTERS, dtype=torch.int64,
+                                   device=dev)
+        N.check(L.mf_scatter_offset_blocks(
+            C_byref(self.dmesh.struct), C_byref(A._pattern_struct()), nproto,
+            R, N.ptr(blk_d), blk_ptr.ctypes.data_as(ctypes_void_p()),
+            N.ptr(B21), N.ptr(B22), N.ptr(bev), N.ptr(om),
+            N.ptr(plan.inner_sorted),
+            plan.color_ptr.ctypes.data_as(ctypes_void_p()), plan.NCOLORS,
+            float(scale), N.ptr(A._dvals), N.ptr(counters), st),
+            "mf_scatter_offset_blocks")
+        self.n_blocks = int(blk.size)
+        return counters
+
     def finish(self, A, counters):
         """events/asymmetry/symmetrize (assembly.py:440-445, x2 folded)."""
         import torch
@@ -575,13 +626,31 @@ def ctypes_void_p():
     return ctypes.c_void_p
 
 
+# lower (sw, se, ne) and upper (sw, ne, nw) triangle protos in cell units
+# (assembly.py:44-48)
+_TRI_PROTOS = np.array([[[0.0, 0.0], [1.0, 0.0], [1.0, 1.0]],
+                        [[0.0, 0.0], [1.0, 1.0], [0.0, 1.0]]])
+
+
+def resolve_strategy(mesh, config):
+    """assembly.py:448-453: "auto" -> blocked on pure quad/tri/hex meshes."""
+    if config.strategy == "blocked" and mesh.kind not in ("quad", "tri",
+                                                          "hex"):
+        raise ValueError("blocked strategy needs a pure-kind mesh")
+    if config.strategy != "auto":
+        return config.strategy
+    return "blocked" if mesh.kind in ("quad", "tri", "hex") else "general"
+
+
 def assemble(mesh, space, kernel, config=None, *, device=None, flags=0,
              keep_on_device=False):
     """Assemble the stiffness matrix A = 2(A21 + A22) on the GPU.
 
     Same arguments and return contract as the reference (assembly.py:456):
     a `SparseMatrix` with host `vals` (already x2), `events` and
-    `presym_asymmetry`.  keep_on_device=True skips the host copy (the
+    `presym_asymmetry`.  Strategy resolution follows the reference: "auto"
+    runs the offset-blocked path on pure quad/tri/hex meshes, "general" the
+    per-pair path (mf_general_core).  keep_on_device=True skips the host copy (the
     values stay in `A.vals_device`; `A.vals` copies them on first use).
     """
     config = config or AssemblyConfig()
@@ -589,12 +658,12 @@ def assemble(mesh, space, kernel, config=None, *, device=None, flags=0,
         raise NotImplementedError(
             "the barycenter baseline (assembly.py:565-635) is outside the "
             "B200 hot path; use the reference package for it")
-    if config.strategy == "blocked" and mesh.kind not in ("quad", "tri",
-                                                          "hex"):
-        raise ValueError("blocked strategy needs a pure-kind mesh")
     ctx = AssemblyContext(mesh, space, kernel, config, device)
     A = ctx.new_matrix()
-    counters = ctx.run(A, flags=flags)
+    if resolve_strategy(mesh, config) == "blocked":
+        counters = ctx.run_blocked(A)
+    else:
+        counters = ctx.run(A, flags=flags)
     ctx.finish(A, counters)
     if not keep_on_device:
         A._vals = _d2h(A._dvals)

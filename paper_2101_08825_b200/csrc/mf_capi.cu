@@ -17,6 +17,14 @@ size_t mf_scan_bytes(int64_t n);
 cudaError_t mf_scan(const int64_t *, int64_t, int64_t *, void *, size_t,
                     cudaStream_t);
 cudaError_t mf_launch_generic(const AsmParams &, int, int, cudaStream_t);
+cudaError_t mf_launch_blocks(const AsmParams &, int, int, int, double,
+                             const double *, double *, double *,
+                             unsigned long long *, int64_t, cudaStream_t);
+cudaError_t mf_launch_blocked_scatter(const AsmParams &, int, int, int,
+                                      const int32_t *, const int64_t *,
+                                      const double *, const double *,
+                                      const unsigned long long *,
+                                      cudaStream_t);
 // specialised kernels: return cudaErrorNotSupported when they do not cover
 // the configuration
 cudaError_t mf_launch_hex(const AsmParams &, cudaStream_t);
@@ -85,6 +93,51 @@ constexpr int kGenericMaxGrid = 148 * 4;
 
 int nq_in_max(const MfRules *r) {
   return r->nq_box_in > r->nq_tri_in ? r->nq_box_in : r->nq_tri_in;
+}
+
+AsmParams make_params(const MfMesh *mesh, const MfRules *rules,
+                      const MfKernel *kern, const MfPattern *pat,
+                      const uint8_t *outer_mask, int32_t R, double scale,
+                      double *vals, uint64_t *counters, int32_t flags) {
+  AsmParams P;
+  memset(&P, 0, sizeof(P));
+  P.mesh = *mesh;
+  P.rules = *rules;
+  if (pat) P.pat = *pat;
+  P.outer_mask = outer_mask;
+  P.R = R;
+  P.scale = scale;
+  P.vals = vals;
+  P.counters = reinterpret_cast<unsigned long long *>(counters);
+  P.flags = flags;
+  P.L_min = kern->L_min;
+  P.L_max = kern->L_max;
+  P.delta = kern->delta;
+  P.eps = kern->eps;
+  P.cde = kern->cde;
+  const double dm = kern->delta - kern->eps;
+  const double dp = kern->delta + kern->eps;
+  P.dme = dm;
+  P.dpe = dp;
+  P.dm2 = dm * dm;
+  P.dp2 = dp * dp;
+  P.dme2_lo = dm * dm * (1.0 - 4e-12);
+  P.dme2_hi = dm * dm * (1.0 + 4e-12);
+  P.inv_eps = kern->eps > 0.0 ? 1.0 / kern->eps : 0.0;
+  P.alpha = kern->delta * P.inv_eps;
+  {
+    int64_t b;
+    memcpy(&b, &P.dm2, 8);
+    P.hi_dm2 = (int32_t)(b >> 32);
+    memcpy(&b, &P.dp2, 8);
+    P.hi_dp2 = (int32_t)(b >> 32);
+  }
+  P.nl_box = mesh->dim == 3 ? (mesh->degree + 1) * (mesh->degree + 1) *
+                                  (mesh->degree + 1)
+                            : (mesh->degree + 1) * (mesh->degree + 1);
+  P.nl_tri = 3 * mesh->degree;
+  P.shortcuts = (flags & MF_FLAG_NO_SHORTCUTS) == 0 && kern->eps > 0.0;
+  return P;
 }
 
 }  // namespace
@@ -173,43 +226,8 @@ int mf_general_core(const MfMesh *mesh, const MfRules *rules,
   if (n_inner == 0) return MF_OK;
   if (!outer_mask || !inner_sorted) return fail(MF_ERR_ARG, "NULL masks");
 
-  AsmParams P;
-  P.mesh = *mesh;
-  P.rules = *rules;
-  P.pat = *pat;
-  P.outer_mask = outer_mask;
-  P.R = R;
-  P.scale = scale;
-  P.vals = vals;
-  P.counters = reinterpret_cast<unsigned long long *>(counters);
-  P.flags = flags;
-  P.L_min = kern->L_min;
-  P.L_max = kern->L_max;
-  P.delta = kern->delta;
-  P.eps = kern->eps;
-  P.cde = kern->cde;
-  const double dm = kern->delta - kern->eps;
-  const double dp = kern->delta + kern->eps;
-  P.dme = dm;
-  P.dpe = dp;
-  P.dm2 = dm * dm;
-  P.dp2 = dp * dp;
-  P.dme2_lo = dm * dm * (1.0 - 4e-12);
-  P.dme2_hi = dm * dm * (1.0 + 4e-12);
-  P.inv_eps = kern->eps > 0.0 ? 1.0 / kern->eps : 0.0;
-  P.alpha = kern->delta * P.inv_eps;
-  {
-    int64_t b;
-    memcpy(&b, &P.dm2, 8);
-    P.hi_dm2 = (int32_t)(b >> 32);
-    memcpy(&b, &P.dp2, 8);
-    P.hi_dp2 = (int32_t)(b >> 32);
-  }
-  P.nl_box = mesh->dim == 3 ? (mesh->degree + 1) * (mesh->degree + 1) *
-                                  (mesh->degree + 1)
-                            : (mesh->degree + 1) * (mesh->degree + 1);
-  P.nl_tri = 3 * mesh->degree;
-  P.shortcuts = (flags & MF_FLAG_NO_SHORTCUTS) == 0 && kern->eps > 0.0;
+  AsmParams P = make_params(mesh, rules, kern, pat, outer_mask, R, scale,
+                            vals, counters, flags);
   const size_t need = mf_general_workspace_bytes(mesh, rules, n_inner);
   if (!workspace || ws_bytes < need)
     return fail(MF_ERR_ARG, "workspace too small");
@@ -237,6 +255,86 @@ int mf_general_core(const MfMesh *mesh, const MfRules *rules,
       e = mf_launch_generic(P, grid, kGenericBlock, s);
     }
     if (e != cudaSuccess) return cuda_status(e, "mf_general_core");
+  }
+  return MF_OK;
+}
+
+int64_t mf_offset_block_count(int32_t dim, int32_t nproto, int32_t R) {
+  const int64_t span = 2 * (int64_t)R + 1;
+  return span * span * (dim == 3 ? span : 1) * nproto * nproto;
+}
+
+size_t mf_offset_blocks_workspace_bytes(const MfRules *rules, int64_t nblk) {
+  const int nq = rules ? nq_in_max(rules) : 1;
+  return 256 + (size_t)((nblk + 127) / 128 * 128) * nq * sizeof(double);
+}
+
+int mf_offset_blocks(const MfMesh *mesh, const MfRules *rules,
+                     const MfKernel *kern, int32_t kind, int32_t nproto,
+                     const double *protos, int32_t R, double h, double *B21,
+                     double *B22, uint64_t *bev, int32_t flags,
+                     void *workspace, size_t ws_bytes, void *stream) {
+  if (int rc = check_mesh(mesh)) return rc;
+  if (!rules || !kern || !B21 || !B22 || !bev)
+    return fail(MF_ERR_ARG, "NULL argument");
+  if (kind < 0 || kind > 2 || nproto < 1 || nproto > 2 || R < 1 || !(h > 0))
+    return fail(MF_ERR_ARG, "bad block arguments");
+  if (kind == 1 && !protos) return fail(MF_ERR_ARG, "protos NULL");
+  if (kern->L_min < 1 || kern->L_min > kern->L_max || kern->L_max > 24)
+    return fail(MF_ERR_ARG, "need 1 <= L_min <= L_max <= 24");
+  const int64_t nblk = mf_offset_block_count(mesh->dim, nproto, R);
+  if (!workspace || ws_bytes < mf_offset_blocks_workspace_bytes(rules, nblk))
+    return fail(MF_ERR_ARG, "workspace too small");
+  AsmParams P = make_params(mesh, rules, kern, nullptr, nullptr, R, 1.0,
+                            nullptr, nullptr, flags);
+  P.overflow = reinterpret_cast<int32_t *>(workspace);
+  P.scratch = reinterpret_cast<double *>(static_cast<char *>(workspace) + 256);
+  P.scratch_stride = nq_in_max(rules);
+  return cuda_status(
+      mf_launch_blocks(P, kind, nproto, R, h, protos, B21, B22,
+                       reinterpret_cast<unsigned long long *>(bev), nblk,
+                       S(stream)),
+      "mf_offset_blocks");
+}
+
+int mf_scatter_offset_blocks(const MfMesh *mesh, const MfPattern *pat,
+                             int32_t nproto, int32_t R, const int32_t *blk,
+                             const int64_t *blk_ptr, const double *B21,
+                             const double *B22, const uint64_t *bev,
+                             const uint8_t *outer_mask,
+                             const int32_t *inner_sorted,
+                             const int64_t *color_ptr, int32_t ncolors,
+                             double scale, double *vals, uint64_t *counters,
+                             void *stream) {
+  if (int rc = check_mesh(mesh)) return rc;
+  if (int rc = check_pattern(pat)) return rc;
+  if (nproto < 1 || nproto > 2 || !blk_ptr || !color_ptr || ncolors < 1)
+    return fail(MF_ERR_ARG, "bad scatter arguments");
+  if (!vals || !counters || !outer_mask) return fail(MF_ERR_ARG, "NULL");
+  const int nloc = mesh->kinds_present == 2
+                       ? 3 * mesh->degree
+                       : (mesh->dim == 3 ? (mesh->degree + 1) *
+                                               (mesh->degree + 1) *
+                                               (mesh->degree + 1)
+                                         : (mesh->degree + 1) *
+                                               (mesh->degree + 1));
+  AsmParams P;
+  memset(&P, 0, sizeof(P));
+  P.mesh = *mesh;
+  P.pat = *pat;
+  P.outer_mask = outer_mask;
+  P.scale = scale;
+  P.vals = vals;
+  P.counters = reinterpret_cast<unsigned long long *>(counters);
+  for (int c = 0; c < ncolors; c++) {
+    const int64_t n = color_ptr[c + 1] - color_ptr[c];
+    if (n <= 0) continue;
+    P.inner = inner_sorted + color_ptr[c];
+    P.n_inner = n;
+    cudaError_t e = mf_launch_blocked_scatter(
+        P, nproto, R, nloc, blk, blk_ptr, B21, B22,
+        reinterpret_cast<const unsigned long long *>(bev), S(stream));
+    if (e != cudaSuccess) return cuda_status(e, "mf_scatter_offset_blocks");
   }
   return MF_OK;
 }

@@ -234,6 +234,81 @@ MF_DEV void event_plateau(const AsmParams &P, const Outer &O, const double *g,
   }
 }
 
+// Algorithm 1 for one (outer O, inner I) pair (_pair_blocks,
+// _kernels.py:184-313): depth-first walk with one geometry per level and
+// the reference's midpoint arithmetic.  Adds the A21 block into b21, the
+// per-q1 gamma sums into G (plus the q1-independent plateau part into
+// Gall) and returns the event count.
+struct EvCounts {
+  unsigned long long up, pl, dead, full;
+};
+
+template <int DIM, int NLM>
+MF_DEV unsigned long long pair_run(const AsmParams &P, const Outer &O,
+                                   const Inner &I, const double *mvec,
+                                   double *b21, double *G, double &Gall,
+                                   EvCounts &cnt) {
+  const int nchild = O.kind == 1 ? 4 : (1 << DIM);
+  double geo[kLevels + 1][6];
+  int child[kLevels + 1];
+  for (int u = 0; u < 6; u++) geo[1][u] = O.geo[u];
+  int L = 1;
+  unsigned long long ev = 0;
+  for (;;) {
+    double slo[3], shi[3];
+    sub_bbox<DIM>(O.kind, geo[L], slo, shi);
+    bool split = false, integ = false;
+    if (L < P.L_min) {
+      split = true;
+    } else if (L == P.L_max) {
+      integ = aprx_min_d<DIM>(slo, shi, I.lo, I.hi) < P.dpe;
+    } else if (aprx_max_lt_dme(P, aprx_max_sq<DIM>(slo, shi, I.lo, I.hi))) {
+      integ = true;
+    } else if (aprx_min_d<DIM>(slo, shi, I.lo, I.hi) < P.dpe) {
+      split = true;
+    }
+    if (integ) {
+      ev++;
+      if (L < P.L_max) {
+        cnt.up++;
+        if (P.shortcuts)
+          event_plateau<DIM, NLM>(P, O, geo[L], I, mvec, b21, Gall);
+        else
+          event_full<DIM, NLM>(P, O, geo[L], I, b21, G);
+      } else if (P.shortcuts && box_dead<DIM>(P, slo, shi, I.lo, I.hi)) {
+        cnt.dead++;
+      } else if (P.shortcuts &&
+                 aprx_max_lt_dme(P, aprx_max_sq<DIM>(slo, shi, I.lo, I.hi))) {
+        cnt.pl++;
+        event_plateau<DIM, NLM>(P, O, geo[L], I, mvec, b21, Gall);
+      } else {
+        cnt.full++;
+        event_full<DIM, NLM>(P, O, geo[L], I, b21, G);
+      }
+    }
+    if (split) {
+      ++L;
+      child[L] = 0;
+      make_child<DIM>(O.kind, geo[L - 1], 0, geo[L]);
+      continue;
+    }
+    bool done = false;
+    for (;;) {
+      if (L == 1) {
+        done = true;
+        break;
+      }
+      if (++child[L] < nchild) {
+        make_child<DIM>(O.kind, geo[L - 1], child[L], geo[L]);
+        break;
+      }
+      --L;
+    }
+    if (done) break;
+  }
+  return ev;
+}
+
 MF_DEV void scatter_add(const AsmParams &P, const int64_t *rows, int nr,
                         const int64_t *cols, int nc, const double *blk,
                         int ld) {
@@ -254,9 +329,8 @@ __global__ void __launch_bounds__(128)
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
   double *G = P.scratch + tid * P.scratch_stride;
-  unsigned long long c_ev = 0, c_pairs = 0, c_up = 0, c_pl = 0, c_dead = 0,
-                     c_full = 0;
-  const int nchild_box = 1 << DIM;
+  unsigned long long c_ev = 0, c_pairs = 0;
+  EvCounts cnt = {0, 0, 0, 0};
   for (int64_t t = tid; t < P.n_inner; t += nthreads) {
     const int64_t m = P.inner[t];
     Inner I;
@@ -340,68 +414,8 @@ __global__ void __launch_bounds__(128)
             }
             double b21[NLM * NLM];
             for (int i = 0; i < I.nloc * NLM; i++) b21[i] = 0.0;
-            const int nchild = O.kind == 1 ? 4 : nchild_box;
-            // depth-first Algorithm 1 with one geometry per level
-            double geo[kLevels + 1][6];
-            int child[kLevels + 1];
-            for (int u = 0; u < 6; u++) geo[1][u] = O.geo[u];
-            int L = 1;
-            unsigned long long ev = 0;
-            for (;;) {
-              double slo[3], shi[3];
-              sub_bbox<DIM>(O.kind, geo[L], slo, shi);
-              bool split = false, integ = false;
-              if (L < P.L_min) {
-                split = true;
-              } else if (L == P.L_max) {
-                integ = aprx_min_d<DIM>(slo, shi, I.lo, I.hi) < P.dpe;
-              } else if (aprx_max_lt_dme(
-                             P, aprx_max_sq<DIM>(slo, shi, I.lo, I.hi))) {
-                integ = true;
-              } else if (aprx_min_d<DIM>(slo, shi, I.lo, I.hi) < P.dpe) {
-                split = true;
-              }
-              if (integ) {
-                ev++;
-                if (L < P.L_max) {
-                  c_up++;
-                  if (P.shortcuts)
-                    event_plateau<DIM, NLM>(P, O, geo[L], I, mvec, b21, Gall);
-                  else
-                    event_full<DIM, NLM>(P, O, geo[L], I, b21, G);
-                } else if (P.shortcuts &&
-                           box_dead<DIM>(P, slo, shi, I.lo, I.hi)) {
-                  c_dead++;
-                } else if (P.shortcuts &&
-                           aprx_max_lt_dme(P, aprx_max_sq<DIM>(slo, shi, I.lo,
-                                                               I.hi))) {
-                  c_pl++;
-                  event_plateau<DIM, NLM>(P, O, geo[L], I, mvec, b21, Gall);
-                } else {
-                  c_full++;
-                  event_full<DIM, NLM>(P, O, geo[L], I, b21, G);
-                }
-              }
-              if (split) {
-                ++L;
-                child[L] = 0;
-                make_child<DIM>(O.kind, geo[L - 1], 0, geo[L]);
-                continue;
-              }
-              bool done = false;
-              for (;;) {
-                if (L == 1) {
-                  done = true;
-                  break;
-                }
-                if (++child[L] < nchild) {
-                  make_child<DIM>(O.kind, geo[L - 1], child[L], geo[L]);
-                  break;
-                }
-                --L;
-              }
-              if (done) break;
-            }
+            const unsigned long long ev =
+                pair_run<DIM, NLM>(P, O, I, mvec, b21, G, Gall, cnt);
             if (ev) {
               c_ev += ev;
               scatter_add(P, mdofs, I.nloc, M.elem_dofs + (size_t)l * M.nloc_max,
@@ -428,10 +442,10 @@ __global__ void __launch_bounds__(128)
   unsigned long long *C = P.counters;
   counter_add(C + MF_CNT_EVENTS, c_ev);
   counter_add(C + MF_CNT_PAIRS, c_pairs);
-  counter_add(C + MF_CNT_EV_UPPER, c_up);
-  counter_add(C + MF_CNT_EV_PLATEAU, c_pl);
-  counter_add(C + MF_CNT_EV_DEAD, c_dead);
-  counter_add(C + MF_CNT_EV_FULL, c_full);
+  counter_add(C + MF_CNT_EV_UPPER, cnt.up);
+  counter_add(C + MF_CNT_EV_PLATEAU, cnt.pl);
+  counter_add(C + MF_CNT_EV_DEAD, cnt.dead);
+  counter_add(C + MF_CNT_EV_FULL, cnt.full);
 }
 
 }  // namespace
@@ -454,5 +468,262 @@ cudaError_t mf_launch_generic(const AsmParams &P, int grid, int block,
     else
       return cudaErrorInvalidValue;
   }
+  return cudaGetLastError();
+}
+
+// ===========================================================================
+// Offset-blocked strategy (reference default on pure meshes, "auto").
+//
+// _build_offset_blocks (_kernels.py:490-594): on a uniform pure-kind grid
+// the pair geometry depends only on the cell offset d and the proto pair,
+// so Algorithm 1 runs once per (d, t2, t1) on the reference's synthetic
+// geometry (outer cell at the origin, inner cell at d*h) -- one thread per
+// block here.  _scatter_offset_blocks (_kernels.py:597-647): every realised
+// (inner cell, offset) adds the block; A22 blocks are summed per inner
+// element and added once.  Scatter = one warp per inner element of a
+// colour, lanes over block entries (race-free, deterministic).
+namespace {
+
+struct BlockArgs {
+  int kind, nproto, R, nloc;
+  double h;
+  const double *protos;  // (nproto, 3, 2) triangle protos in cell units
+  double *B21, *B22;
+  unsigned long long *bev;
+  int64_t nblk;
+};
+
+template <int DIM, int NLM>
+__global__ void __launch_bounds__(128) k_blocks(AsmParams P, BlockArgs B) {
+  const MfRules &Rr = P.rules;
+  const int64_t bi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (bi >= B.nblk) return;
+  const int span = 2 * B.R + 1, np = B.nproto;
+  int64_t t = bi;
+  const int t1 = (int)(t % np);
+  t /= np;
+  const int t2 = (int)(t % np);
+  t /= np;
+  const int ix = (int)(t % span);
+  t /= span;
+  const int iy = (int)(t % span);
+  t /= span;
+  const int iz = (int)t;
+  const int dx = ix - B.R, dy = iy - B.R, dz = DIM == 3 ? iz - B.R : 0;
+  const double h = B.h;
+  const double dd[3] = {(double)dx * h, (double)dy * h, (double)dz * h};
+  Outer O;
+  Inner I;
+  I.kind = B.kind == 1 ? 1 : 0;
+  O.kind = B.kind;
+  O.nloc = I.nloc = B.nloc;
+  I.nq = B.kind == 1 ? Rr.nq_tri_in : Rr.nq_box_in;
+  I.pts = B.kind == 1 ? Rr.tri_in_pts : Rr.box_in_pts;
+  I.w = B.kind == 1 ? Rr.tri_in_w : Rr.box_in_w;
+  I.phi = B.kind == 1 ? Rr.phi_tri_in : Rr.phi_box_in;
+#pragma unroll
+  for (int k = 0; k < DIM; k++) {
+    I.lo[k] = dd[k];
+    I.hi[k] = xadd(dd[k], h);
+  }
+  if (B.kind == 1) {
+    const double *po = B.protos + t2 * 6, *pi = B.protos + t1 * 6;
+    double oc[6], ic[6];
+    for (int v = 0; v < 3; v++) {
+      oc[2 * v] = xmul(po[2 * v], h);
+      oc[2 * v + 1] = xmul(po[2 * v + 1], h);
+      ic[2 * v] = xadd(xmul(pi[2 * v], h), dd[0]);
+      ic[2 * v + 1] = xadd(xmul(pi[2 * v + 1], h), dd[1]);
+    }
+    for (int u = 0; u < 6; u++) O.geo[u] = oc[u];
+    const double e10 = oc[2] - oc[0], e11 = oc[3] - oc[1];
+    const double e20 = oc[4] - oc[0], e21 = oc[5] - oc[1];
+    const double det = e10 * e21 - e11 * e20;
+    O.v0[0] = oc[0];
+    O.v0[1] = oc[1];
+    O.inv[0] = e21 / det;
+    O.inv[1] = -e20 / det;
+    O.inv[2] = -e11 / det;
+    O.inv[3] = e10 / det;
+    I.c0[0] = ic[0];
+    I.c0[1] = ic[1];
+    I.e1[0] = xsub(ic[2], ic[0]);
+    I.e1[1] = xsub(ic[3], ic[1]);
+    I.e2[0] = xsub(ic[4], ic[0]);
+    I.e2[1] = xsub(ic[5], ic[1]);
+    I.scale_w = I.e1[0] * I.e2[1] - I.e1[1] * I.e2[0];
+  } else {
+    double jac = 1.0;
+#pragma unroll
+    for (int k = 0; k < DIM; k++) {
+      O.lo[k] = 0.0;
+      O.hi[k] = h;
+      O.geo[k] = 0.0;
+      O.geo[DIM + k] = h;
+      jac *= 0.5 * (I.hi[k] - I.lo[k]);
+    }
+    I.scale_w = jac;
+  }
+  double mvec[NLM];
+  for (int i = 0; i < I.nloc; i++) {
+    double s = 0.0;
+    for (int q = 0; q < I.nq; q++) s += I.w[q] * I.phi[q * I.nloc + i];
+    mvec[i] = s * I.scale_w;
+  }
+  double *G = P.scratch + bi * P.scratch_stride;
+  for (int q = 0; q < I.nq; q++) G[q] = 0.0;
+  double Gall = 0.0;
+  double b21[NLM * NLM];
+  for (int i = 0; i < I.nloc * NLM; i++) b21[i] = 0.0;
+  EvCounts cnt = {0, 0, 0, 0};
+  const unsigned long long ev =
+      pair_run<DIM, NLM>(P, O, I, mvec, b21, G, Gall, cnt);
+  const int nl = B.nloc;
+  double *o21 = B.B21 + bi * nl * nl, *o22 = B.B22 + bi * nl * nl;
+  for (int i = 0; i < nl; i++)
+    for (int j = 0; j < nl; j++) {
+      o21[i * nl + j] = b21[i * NLM + j];
+      o22[i * nl + j] = 0.0;
+    }
+  if (ev) {
+    for (int q = 0; q < I.nq; q++) {
+      const double s = (G[q] + Gall) * I.w[q] * I.scale_w;
+      if (s == 0.0) continue;
+      for (int i = 0; i < nl; i++) {
+        const double ci = s * I.phi[q * nl + i];
+        for (int j = 0; j < nl; j++) o22[i * nl + j] += ci * I.phi[q * nl + j];
+      }
+    }
+  }
+  B.bev[bi] = ev;
+}
+
+struct ScatterArgs {
+  int nproto, R, nloc, dim;
+  const int32_t *blk;  // nonzero block ids sorted by inner proto
+  int64_t ptr[3];      // ranges of blk per inner proto (nproto <= 2)
+  const double *B21, *B22;
+  const unsigned long long *bev;
+};
+
+template <int MAXE>
+__global__ void __launch_bounds__(128) k_blocked_scatter(AsmParams P,
+                                                         ScatterArgs S) {
+  const MfMesh &M = P.mesh;
+  const int lane = threadIdx.x & 31;
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= P.n_inner) return;
+  const int64_t m = P.inner[w];
+  const int np = S.nproto, nl = S.nloc, ne = nl * nl;
+  const int t1 = (int)(m % np);
+  const int cell = (int)(m / np);
+  int cx, cy, cz;
+  cell_coords(cell, M.ncx, M.ncy, cx, cy, cz);
+  const int span = 2 * S.R + 1;
+  const int64_t *din = M.elem_dofs + m * M.nloc_max;
+  double a22[MAXE];
+#pragma unroll
+  for (int k = 0; k < MAXE; k++) a22[k] = 0.0;
+  unsigned long long ev = 0, pairs = 0;
+  for (int64_t k = S.ptr[t1]; k < S.ptr[t1 + 1]; k++) {
+    const int bi = S.blk[k];
+    int t = bi / np;
+    const int t2 = t % np;
+    t /= np;
+    const int dx = t % span - S.R;
+    t /= span;
+    const int dy = t % span - S.R;
+    t /= span;
+    const int dz = S.dim == 3 ? t - S.R : 0;
+    const int ox = cx - dx, oy = cy - dy, oz = cz - dz;
+    if (ox < 0 || ox >= M.ncx || oy < 0 || oy >= M.ncy || oz < 0 ||
+        oz >= M.ncz)
+      continue;
+    const int64_t eo = ((int64_t)(oz * M.ncy + oy) * M.ncx + ox) * np + t2;
+    if (!P.outer_mask[eo]) continue;
+    ev += S.bev[bi];
+    pairs++;
+    const int64_t *dout = M.elem_dofs + eo * M.nloc_max;
+    const double *b21 = S.B21 + (int64_t)bi * ne;
+    const double *b22 = S.B22 + (int64_t)bi * ne;
+#pragma unroll
+    for (int u = 0; u < MAXE; u++) {
+      const int e = lane + 32 * u;
+      if (e < ne) {
+        const int i = e / nl, j = e - (e / nl) * nl;
+        P.vals[pat_index(P.pat, din[i], dout[j])] += P.scale * b21[e];
+        a22[u] += b22[e];
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < MAXE; u++) {
+    const int e = lane + 32 * u;
+    if (e < ne && pairs) {
+      const int i = e / nl, j = e - (e / nl) * nl;
+      P.vals[pat_index(P.pat, din[i], din[j])] += P.scale * a22[u];
+    }
+  }
+  if (lane == 0) {
+    counter_add(P.counters + MF_CNT_EVENTS, ev);
+    counter_add(P.counters + MF_CNT_PAIRS, pairs);
+  }
+}
+
+}  // namespace
+
+cudaError_t mf_launch_blocks(const AsmParams &P, int kind, int nproto, int R,
+                             double h, const double *protos, double *B21,
+                             double *B22, unsigned long long *bev,
+                             int64_t nblk, cudaStream_t s) {
+  BlockArgs B;
+  B.kind = kind;
+  B.nproto = nproto;
+  B.R = R;
+  B.h = h;
+  B.protos = protos;
+  B.B21 = B21;
+  B.B22 = B22;
+  B.bev = bev;
+  B.nblk = nblk;
+  const int dim = P.mesh.dim;
+  B.nloc = kind == 1 ? 3 * P.mesh.degree : (dim == 3 ? P.nl_box : P.nl_box);
+  const int grid = (int)((nblk + 127) / 128);
+  if (dim == 2)
+    k_blocks<2, 9><<<grid, 128, 0, s>>>(P, B);
+  else if (B.nloc <= 8)
+    k_blocks<3, 8><<<grid, 128, 0, s>>>(P, B);
+  else
+    k_blocks<3, 27><<<grid, 128, 0, s>>>(P, B);
+  return cudaGetLastError();
+}
+
+cudaError_t mf_launch_blocked_scatter(const AsmParams &P, int nproto, int R,
+                                      int nloc, const int32_t *blk,
+                                      const int64_t *ptr, const double *B21,
+                                      const double *B22,
+                                      const unsigned long long *bev,
+                                      cudaStream_t s) {
+  ScatterArgs S;
+  S.nproto = nproto;
+  S.R = R;
+  S.nloc = nloc;
+  S.dim = P.mesh.dim;
+  S.blk = blk;
+  for (int i = 0; i <= nproto; i++) S.ptr[i] = ptr[i];
+  S.B21 = B21;
+  S.B22 = B22;
+  S.bev = bev;
+  const int64_t threads = P.n_inner * 32;
+  const int grid = (int)((threads + 127) / 128);
+  const int ne = nloc * nloc;
+  if (ne <= 32)
+    k_blocked_scatter<1><<<grid, 128, 0, s>>>(P, S);
+  else if (ne <= 64)
+    k_blocked_scatter<2><<<grid, 128, 0, s>>>(P, S);
+  else if (ne <= 96)
+    k_blocked_scatter<3><<<grid, 128, 0, s>>>(P, S);
+  else
+    k_blocked_scatter<23><<<grid, 128, 0, s>>>(P, S);
   return cudaGetLastError();
 }

@@ -90,6 +90,14 @@ def run_case(name, spec):
         cand_ptr=ptr, cand_ids=ids, vals=A.vals, events=np.int64(A.events),
         asym=np.float64(A.presym_asymmetry), rowptr=A.rowptr,
         K=np.int64(A.K), c_delta_eps=np.float64(kp.c_delta_eps))
+    if kind in ("quad", "tri", "hex"):
+        # the reference default strategy ("auto" -> offset-blocked path,
+        # assembly.py:448-453, 391-437) on the same problem
+        cfg_a = R.AssemblyConfig(L_min=lmin, L_max=lmax, outer_rule=orule,
+                                 inner_rule=irule)
+        B = R.assemble(mesh, space, kp, cfg_a)
+        out.update(vals_auto=B.vals, events_auto=np.int64(B.events),
+                   asym_auto=np.float64(B.presym_asymmetry))
     if "part" in extras:
         # one partition of a 2-way RCB split, as parallel_assemble runs it
         from mollifem.parallel import ghost_regions

@@ -88,8 +88,6 @@ def test_deterministic_bitwise():
 def test_matrix_methods_match_oracle():
     import oracle
     g, A = _assemble("quad_q2_lmax2")
-    H = oracle.HostPattern_from(A) if hasattr(oracle, "HostPattern_from") \
-        else None
     x = np.random.default_rng(1).standard_normal(A.n)
     y = A.matvec(x)
     from paper_2101_08825_b200.assembly import HostPattern
@@ -109,7 +107,6 @@ def test_matrix_methods_match_oracle():
     oracle.symmetrize(R)
     assert np.array_equal(A.vals, R.vals)
     assert A.asymmetry_inf() <= 1e-14 * A.norm_inf()
-    del H
 
 
 def test_r1_full_against_oracle():
@@ -126,3 +123,33 @@ def test_r1_full_against_oracle():
     R = oracle.assemble_general(mesh, space, kp, cfg)
     assert A.events == R.events == 5800432
     assert rel_frob(A.vals, R.vals) <= TOL
+
+
+@pytest.mark.parametrize("name", [n for n in golden_names()
+                                  if "mixed" not in n])
+def test_default_strategy_blocked_matches_reference(name):
+    """strategy="auto" -> offset-blocked path (assembly.py:448-453,
+    391-437): same events (realised block events) and matrix as the
+    reference default."""
+    from paper_2101_08825_b200 import AssemblyConfig, assemble
+    g = Golden(name)
+    mesh, space, kp, cfg = g.build()
+    cfg_a = AssemblyConfig(L_min=cfg.L_min, L_max=cfg.L_max,
+                           outer_rule=cfg.outer_rule,
+                           inner_rule=cfg.inner_rule)
+    A = assemble(mesh, space, kp, cfg_a)
+    assert A.events == int(g["events_auto"])
+    err = rel_frob(A.vals, g["vals_auto"])
+    print(f"{name} blocked relF={err:.3e}")
+    assert err <= TOL
+    ref = float(g["asym_auto"])
+    assert abs(A.presym_asymmetry - ref) <= 1e-8 * max(
+        ref, np.abs(g["vals_auto"]).max())
+
+
+def test_blocked_rejects_mixed():
+    from paper_2101_08825_b200 import AssemblyConfig, assemble
+    g = Golden("mixed_p1_lmax3")
+    mesh, space, kp, cfg = g.build()
+    with pytest.raises(ValueError):
+        assemble(mesh, space, kp, AssemblyConfig(strategy="blocked"))
