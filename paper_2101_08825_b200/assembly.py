@@ -481,6 +481,16 @@ class AssemblyContext:
         self.R = stencil_radius(params.delta + params.eps, mesh.h)
         self.h2d_bytes = self.dmesh.h2d_bytes
 
+    def default_plan(self):
+        """All elements, colour groups ordered heaviest first (candidate
+        pair counts from the GPU count pass)."""
+        from .device import ColorPlan
+        from .parallel import pair_counts
+        if getattr(self, "_plan", None) is None:
+            work = pair_counts(self.mesh, self.params, self.dmesh)
+            self._plan = ColorPlan(self.mesh, None, self.device, work=work)
+        return self._plan
+
     def kernel_struct(self):
         from . import _native as N
         p, c = self.params, self.config
@@ -498,7 +508,7 @@ class AssemblyContext:
         return A
 
     def run(self, A, outer_mask=None, inner_ids=None, scale=2.0, flags=0,
-            plan=None, counters=None, vals_window=None):
+            plan=None, counters=None, vals_window=None, groups=None):
         """Accumulate scale*(A21 + A22) of the selected pairs into A.
 
         vals_window: a `WindowedValues` when the caller only holds the
@@ -514,7 +524,9 @@ class AssemblyContext:
             om = to_device(np.ascontiguousarray(outer_mask, np.uint8),
                            self.device)
         if plan is None:
-            plan = ColorPlan(self.mesh, inner_ids, self.device)
+            plan = (self.default_plan() if inner_ids is None and
+                    outer_mask is None else
+                    ColorPlan(self.mesh, inner_ids, self.device))
         if counters is None:
             counters = torch.zeros(N.MF_NCOUNTERS, dtype=torch.int64,
                                    device=self.device)
@@ -522,16 +534,81 @@ class AssemblyContext:
                                                C_byref(self.drules.struct),
                                                plan.n_inner))
         ws = torch.zeros(wsb, dtype=torch.uint8, device=self.device)
-        cp = plan.color_ptr.ctypes.data_as(ctypes_void_p())
+        g0, g1 = groups if groups is not None else (0, plan.ngroups)
+        cptr = np.ascontiguousarray(plan.color_ptr[g0:g1 + 1])
+        cp = cptr.ctypes.data_as(ctypes_void_p())
         N.check(L.mf_general_core(
             C_byref(self.dmesh.struct), C_byref(self.drules.struct),
             C_byref(self.kernel_struct()), C_byref(A._pattern_struct()),
-            N.ptr(om), N.ptr(plan.inner_sorted), cp, plan.NCOLORS, self.R,
+            N.ptr(om), N.ptr(plan.inner_sorted), cp, g1 - g0, self.R,
             float(scale),
             (vals_window.pointer() if vals_window is not None
              else N.ptr(A._dvals)), N.ptr(counters), int(flags),
             N.ptr(ws), wsb, N.stream_ptr()), "mf_general_core")
         return counters
+
+    # -- general path with the host copy overlapped -----------------------
+    def run_streamed(self, A, flags=0, nslabs=None):
+        """General path in top-axis layer ranges: while range s+1 computes,
+        the rows finished by range s (their DOF planes are touched by no
+        later layer) are copied device->host on a side stream by a worker
+        thread into the result array.  Same kernels and launches otherwise;
+        call `finish` then `join_streamed`."""
+        import threading
+
+        import torch
+        from . import _native as N
+        from .device import ColorPlan
+        from .parallel import pair_counts, slab_layers
+        mesh, space = self.mesh, self.space
+        axis = mesh.dim - 1
+        nl = int(mesh.grid_ncells[axis])
+        if nslabs is None:
+            nslabs = max(1, min(4, nl // 4))
+        work = pair_counts(mesh, self.params, self.dmesh)
+        layers = slab_layers(mesh, nslabs, work)
+        plan = ColorPlan(mesh, None, self.device, work=work, layers=layers)
+        counters = torch.zeros(N.MF_NCOUNTERS, dtype=torch.int64,
+                               device=self.device)
+        d = space.degree
+        plane = int(np.prod(space.grid_dims[:-1]))
+        nplanes = int(space.grid_dims[-1])
+        host = np.empty(A.nnz, dtype=np.float64)
+        self._stream_host = host
+        compute = torch.cuda.current_stream()
+        copy = torch.cuda.Stream(device=self.device)
+        ranges = []
+        done_plane = 0
+        for s_, (lo, hi) in enumerate(layers):
+            g0, g1 = plan.group_range(s_)
+            self.run(A, plan=plan, counters=counters, flags=flags,
+                     groups=(g0, g1))
+            ev = torch.cuda.Event()
+            ev.record(compute)
+            final = nplanes if s_ == len(layers) - 1 else d * hi
+            a = int(A.rowptr[done_plane * plane])
+            b = int(A.rowptr[final * plane])
+            ranges.append((ev, a, b))
+            done_plane = final
+        src = A._dvals
+
+        def worker():
+            ht = torch.from_numpy(host)
+            with torch.cuda.stream(copy):
+                for ev, a, b in ranges:
+                    copy.wait_event(ev)
+                    if b > a:
+                        ht[a:b].copy_(src[a:b])
+                copy.synchronize()
+
+        self._stream_thread = threading.Thread(target=worker, daemon=True)
+        self._stream_thread.start()
+        return counters
+
+    def join_streamed(self, A):
+        self._stream_thread.join()
+        A._vals = self._stream_host
+        self._stream_host = None
 
     def run_blocked(self, A, scale=2.0, counters=None):
         """Offset-blocked strategy (assembly.py:391-437) on the device:
@@ -662,11 +739,19 @@ def assemble(mesh, space, kernel, config=None, *, device=None, flags=0,
     A = ctx.new_matrix()
     if resolve_strategy(mesh, config) == "blocked":
         counters = ctx.run_blocked(A)
-    else:
+        ctx.finish(A, counters)
+        if not keep_on_device:
+            A._vals = _d2h(A._dvals)
+        return A
+    if keep_on_device or config.symmetrize:
         counters = ctx.run(A, flags=flags)
+        ctx.finish(A, counters)
+        if not keep_on_device:
+            A._vals = _d2h(A._dvals)
+        return A
+    counters = ctx.run_streamed(A, flags=flags)
     ctx.finish(A, counters)
-    if not keep_on_device:
-        A._vals = _d2h(A._dvals)
+    ctx.join_streamed(A)
     return A
 
 

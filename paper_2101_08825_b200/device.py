@@ -99,19 +99,45 @@ def color_of(mesh):
 
 
 class ColorPlan:
-    """Inner elements grouped by colour, ascending ids inside a colour."""
+    """Inner elements grouped by colour (one launch per group).
+
+    Default: ascending ids inside a colour.  With `work` (per-element work
+    estimate, e.g. candidate-pair counts) each group is ordered heaviest
+    first, so the last wave of a launch holds the light elements (shorter
+    tail).  With `layers` (a list of top-axis cell-layer ranges) the groups
+    are (layer range, colour) in that order, so the rows of a finished
+    range can leave the device while the next range computes.
+    """
 
     NCOLORS = 16
 
-    def __init__(self, mesh, inner_ids=None, device=None):
+    def __init__(self, mesh, inner_ids=None, device=None, work=None,
+                 layers=None):
         col = color_of(mesh)
         ids = (np.arange(mesh.n_elements, dtype=np.int64) if inner_ids is None
                else np.asarray(inner_ids, dtype=np.int64))
-        order = np.argsort(col[ids], kind="stable")
+        if layers is None:
+            slab = np.zeros(len(ids), dtype=np.int64)
+            nslab = 1
+        else:
+            layer = mesh.elem_cell[ids, mesh.dim - 1]
+            cuts = np.asarray([a for a, _ in layers] + [layers[-1][1]])
+            slab = np.searchsorted(cuts, layer, side="right") - 1
+            nslab = len(layers)
+        key2 = (np.zeros(len(ids)) if work is None
+                else -np.asarray(work, dtype=np.float64)[ids])
+        group = slab * self.NCOLORS + col[ids]
+        order = np.lexsort((ids, key2, group))
         ids = ids[order]
-        counts = np.bincount(col[ids], minlength=self.NCOLORS)
-        self.color_ptr = np.zeros(self.NCOLORS + 1, dtype=np.int64)
+        self.ngroups = nslab * self.NCOLORS
+        counts = np.bincount(group[order], minlength=self.ngroups)
+        self.color_ptr = np.zeros(self.ngroups + 1, dtype=np.int64)
         np.cumsum(counts, out=self.color_ptr[1:])
         self.inner_sorted = to_device(ids.astype(np.int32), _dev(device))
         self.n_inner = int(len(ids))
         self.h2d_bytes = ids.size * 4
+        self.layers = layers
+
+    def group_range(self, slab):
+        """(first, last) group index of one layer range."""
+        return slab * self.NCOLORS, (slab + 1) * self.NCOLORS
