@@ -161,99 +161,84 @@ MF_DEV void event_plateau(const AsmParams &P, const double *s_rt,
 }
 
 // Full event: lane q1 evaluates its NO^3 point pairs and contracts them
-// by sum factorisation (x, then y, then z) into V.  Point pairs are
-// classified on the high word of the exact d2 (certainly inside delta-eps
-// -> mu = 1, certainly beyond delta+eps -> 0); the shell polynomial runs
-// for a group of BATCH points only when a lane of the warp needs it.
-template <int NO, bool SHARP, int BATCH>
+// by sum factorisation into V.  Loop order: x node a outermost (rolled, its
+// operands re-read from shared memory), then y node b and z node c
+// unrolled; contraction z first (2 DFMA per point), then y (4 per b), then
+// x (8 per a).  Point pairs are classified on the high word of the exact
+// d2 (certainly inside delta-eps -> mu = 1, certainly beyond delta+eps ->
+// 0); the shell polynomial runs for the NO z-nodes of one (a, b) only when
+// a lane of the warp needs it.  Inactive lanes carry a far-away point, so
+// every one of their pairs classifies as "beyond".
+template <int NO, bool SHARP>
 MF_DEV void event_full(const AsmParams &P, const double *s_rt,
                        const double *s_rw, WarpCtx<NO> &C, int slot,
-                       const double y[3], int lane, bool active,
-                       double V[8]) {
+                       const double y[3], int lane, double V[8]) {
   event_axes<NO>(P, s_rt, s_rw, C, slot, lane);
-  double sq[3][NO];
+  double sq1[NO], sq2[NO], shy[2][NO], shz[2][NO];
 #pragma unroll
-  for (int k = 0; k < 3; k++)
+  for (int b = 0; b < NO; b++) {
+    const double d1 = xsub(C.X[1][b], y[1]);
+    const double d2 = xsub(C.X[2][b], y[2]);
+    sq1[b] = xmul(d1, d1);
+    sq2[b] = xmul(d2, d2);
 #pragma unroll
-    for (int a = 0; a < NO; a++) {
-      const double d = xsub(C.X[k][a], y[k]);
-      sq[k][a] = xmul(d, d);
+    for (int j = 0; j < 2; j++) {
+      shy[j][b] = C.sh[1][j][b];
+      shz[j][b] = C.sh[2][j][b];
     }
-  double shx[2][NO];
-#pragma unroll
-  for (int j = 0; j < 2; j++)
-#pragma unroll
-    for (int a = 0; a < NO; a++) shx[j][a] = C.sh[0][j][a];
-  // (dx^2 + dy^2) once per (a, b): the reference's association order
-  double sxy[NO][NO];
-#pragma unroll
-  for (int b = 0; b < NO; b++)
-#pragma unroll
-    for (int a = 0; a < NO; a++) sxy[b][a] = xadd(sq[0][a], sq[1][b]);
+  }
 #pragma unroll 1
-  for (int c = 0; c < NO; c++) {
-    double Tb[2][NO];
+  for (int a = 0; a < NO; a++) {
+    const double d0 = xsub(C.X[0][a], y[0]);
+    const double sq0 = xmul(d0, d0);
+    double W[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // [jy][jz]
 #pragma unroll
     for (int b = 0; b < NO; b++) {
-      double mu[NO];
+      const double sxy = xadd(sq0, sq1[b]);
+      double d2v[NO], mu[NO];
       bool shl[NO];
       bool anysh = false;
 #pragma unroll
-      for (int a = 0; a < NO; a++) {
-        const double d2 = xadd(sxy[b][a], sq[2][c]);
+      for (int c = 0; c < NO; c++) {
+        d2v[c] = xadd(sxy, sq2[c]);
         if (SHARP) {
-          mu[a] = d2 < P.dp2 ? 256.0 : 0.0;
-          shl[a] = false;
+          mu[c] = d2v[c] < P.dp2 ? 256.0 : 0.0;
+          shl[c] = false;
         } else {
-          const int hi = __double2hiint(d2);
+          const int hi = __double2hiint(d2v[c]);
           const bool pl = hi < P.hi_dm2;
-          const bool sk = hi > P.hi_dp2;
-          mu[a] = pl ? 256.0 : 0.0;
-          shl[a] = active && !(pl || sk);
-          anysh |= shl[a];
-          if (BATCH == 1) {
-            if (__any_sync(0xffffffffu, shl[a])) {
-              const double v = xi256_unclamped(P, d2);
-              if (shl[a]) mu[a] = v;
-            }
-          } else if (shl[a]) {
-            mu[a] = d2;
-          }
+          shl[c] = !pl && hi <= P.hi_dp2;
+          mu[c] = pl ? 256.0 : 0.0;
+          anysh |= shl[c];
         }
       }
-      if (!SHARP && BATCH != 1) {
-        if (__any_sync(0xffffffffu, anysh)) {
+      if (!SHARP && __any_sync(0xffffffffu, anysh)) {
 #pragma unroll
-          for (int a = 0; a < NO; a++) {
-            const double v = xi256_unclamped(P, mu[a]);
-            if (shl[a]) mu[a] = v;
-          }
+        for (int c = 0; c < NO; c++) {
+          const double v = xi256_unclamped(P, d2v[c]);
+          if (shl[c]) mu[c] = v;
         }
       }
-      double t0 = 0.0, t1 = 0.0;
+      double u0 = 0.0, u1 = 0.0;  // z contraction
 #pragma unroll
-      for (int a = 0; a < NO; a++) {
-        t0 = fma(mu[a], shx[0][a], t0);
-        t1 = fma(mu[a], shx[1][a], t1);
+      for (int c = 0; c < NO; c++) {
+        u0 = fma(mu[c], shz[0][c], u0);
+        u1 = fma(mu[c], shz[1][c], u1);
       }
-      Tb[0][b] = t0;
-      Tb[1][b] = t1;
-    }
-    const double z0 = C.sh[2][0][c], z1 = C.sh[2][1][c];
 #pragma unroll
-    for (int jy = 0; jy < 2; jy++) {
-      double t2x0 = 0.0, t2x1 = 0.0;
-#pragma unroll
-      for (int b = 0; b < NO; b++) {
-        const double yb = C.sh[1][jy][b];
-        t2x0 = fma(Tb[0][b], yb, t2x0);
-        t2x1 = fma(Tb[1][b], yb, t2x1);
+      for (int jy = 0; jy < 2; jy++) {
+        W[jy][0] = fma(u0, shy[jy][b], W[jy][0]);
+        W[jy][1] = fma(u1, shy[jy][b], W[jy][1]);
       }
-      V[2 * jy] = fma(t2x0, z0, V[2 * jy]);
-      V[2 * jy + 1] = fma(t2x1, z0, V[2 * jy + 1]);
-      V[2 * jy + 4] = fma(t2x0, z1, V[2 * jy + 4]);
-      V[2 * jy + 5] = fma(t2x1, z1, V[2 * jy + 5]);
     }
+    const double x0 = C.sh[0][0][a], x1 = C.sh[0][1][a];
+#pragma unroll
+    for (int jz = 0; jz < 2; jz++)
+#pragma unroll
+      for (int jy = 0; jy < 2; jy++) {
+        V[2 * jy + 4 * jz] = fma(x0, W[jy][jz], V[2 * jy + 4 * jz]);
+        V[1 + 2 * jy + 4 * jz] = fma(x1, W[jy][jz], V[1 + 2 * jy + 4 * jz]);
+      }
   }
   __syncwarp();
 }
@@ -263,10 +248,9 @@ MF_DEV void run_full(const AsmParams &P, const double *s_rt,
                      const double *s_rw, WarpCtx<NO> &C, int slot,
                      const double y[3], int lane, bool active, double V[8]) {
   if (P.eps == 0.0)
-    event_full<NO, true, 1>(P, s_rt, s_rw, C, slot, y, lane, active, V);
+    event_full<NO, true>(P, s_rt, s_rw, C, slot, y, lane, V);
   else
-    event_full<NO, false, (MF_HEX_BATCH == 1 ? 1 : NO)>(
-        P, s_rt, s_rw, C, slot, y, lane, active, V);
+    event_full<NO, false>(P, s_rt, s_rw, C, slot, y, lane, V);
 }
 
 template <int NO, int NI>
@@ -311,7 +295,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MF_HEX_MINB)
                         (0.5 * (C.ihi[1] - C.ilo[1])) *
                         (0.5 * (C.ihi[2] - C.ilo[2]));
   const bool active = lane < NQ1;
-  double y[3] = {0.0, 0.0, 0.0};
+  // inactive lanes sit far away: all their pairs classify as "beyond"
+  double y[3] = {1e300, 1e300, 1e300};
   if (active) {
 #pragma unroll
     for (int k = 0; k < 3; k++)
