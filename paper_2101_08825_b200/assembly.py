@@ -548,7 +548,7 @@ class AssemblyContext:
         return counters
 
     # -- general path with the host copy overlapped -----------------------
-    def run_streamed(self, A, flags=0, nslabs=None):
+    def run_streamed(self, A, flags=0, nslabs=None, strategy="general"):
         """General path in top-axis layer ranges: while range s+1 computes,
         the rows finished by range s (their DOF planes are touched by no
         later layer) are copied device->host on a side stream by a worker
@@ -568,6 +568,8 @@ class AssemblyContext:
         work = pair_counts(mesh, self.params, self.dmesh)
         layers = slab_layers(mesh, nslabs, work)
         plan = ColorPlan(mesh, None, self.device, work=work, layers=layers)
+        if strategy == "blocked":
+            self.build_blocks(A)
         counters = torch.zeros(N.MF_NCOUNTERS, dtype=torch.int64,
                                device=self.device)
         d = space.degree
@@ -581,8 +583,11 @@ class AssemblyContext:
         done_plane = 0
         for s_, (lo, hi) in enumerate(layers):
             g0, g1 = plan.group_range(s_)
-            self.run(A, plan=plan, counters=counters, flags=flags,
-                     groups=(g0, g1))
+            if strategy == "blocked":
+                self.scatter_blocks(A, plan, counters, groups=(g0, g1))
+            else:
+                self.run(A, plan=plan, counters=counters, flags=flags,
+                         groups=(g0, g1))
             ev = torch.cuda.Event()
             ev.record(compute)
             final = nplanes if s_ == len(layers) - 1 else d * hi
@@ -610,12 +615,14 @@ class AssemblyContext:
         A._vals = self._stream_host
         self._stream_host = None
 
-    def run_blocked(self, A, scale=2.0, counters=None):
-        """Offset-blocked strategy (assembly.py:391-437) on the device:
-        mf_offset_blocks + mf_scatter_offset_blocks."""
+    def build_blocks(self, A):
+        """mf_offset_blocks: one Algorithm-1 run per (offset, proto pair) on
+        the reference's synthetic geometry (_build_offset_blocks,
+        _kernels.py:490-594); keeps the present blocks grouped by inner
+        proto for the scatter."""
         import torch
         from . import _native as N
-        from .device import ColorPlan, to_device
+        from .device import to_device
         L = N.lib()
         mesh, space = self.mesh, self.space
         kind = mesh.kind
@@ -633,12 +640,11 @@ class AssemblyContext:
         wsb = int(L.mf_offset_blocks_workspace_bytes(
             C_byref(self.drules.struct), nblk))
         ws = torch.zeros(wsb, dtype=torch.uint8, device=dev)
-        st = N.stream_ptr()
         N.check(L.mf_offset_blocks(
             C_byref(self.dmesh.struct), C_byref(self.drules.struct),
             C_byref(self.kernel_struct()), kcode, nproto, N.ptr(protos), R,
             float(mesh.h), N.ptr(B21), N.ptr(B22), N.ptr(bev), 0, N.ptr(ws),
-            wsb, st), "mf_offset_blocks")
+            wsb, N.stream_ptr()), "mf_offset_blocks")
         ev = bev.cpu().numpy()
         ids = np.nonzero(ev > 0)[0]
         t1 = ids % nproto
@@ -647,21 +653,42 @@ class AssemblyContext:
         blk_ptr = np.searchsorted(t1[order], np.arange(nproto + 1)).astype(
             np.int64)
         blk_d = to_device(blk if blk.size else np.zeros(1, np.int32), dev)
-        plan = ColorPlan(mesh, None, dev)
-        om = torch.ones(mesh.n_elements, dtype=torch.uint8, device=dev)
+        self.n_blocks = int(blk.size)
+        self._blocks = dict(B21=B21, B22=B22, bev=bev, blk=blk_d,
+                            blk_ptr=blk_ptr, nproto=nproto, R=R)
+        return self._blocks
+
+    def scatter_blocks(self, A, plan, counters, scale=2.0, groups=None):
+        """mf_scatter_offset_blocks over the colour groups of `plan`."""
+        import torch
+        from . import _native as N
+        L = N.lib()
+        b = self._blocks
+        om = torch.ones(self.mesh.n_elements, dtype=torch.uint8,
+                        device=self.device)
+        g0, g1 = groups if groups is not None else (0, plan.ngroups)
+        cptr = np.ascontiguousarray(plan.color_ptr[g0:g1 + 1])
+        N.check(L.mf_scatter_offset_blocks(
+            C_byref(self.dmesh.struct), C_byref(A._pattern_struct()),
+            b["nproto"], b["R"], N.ptr(b["blk"]),
+            b["blk_ptr"].ctypes.data_as(ctypes_void_p()), N.ptr(b["B21"]),
+            N.ptr(b["B22"]), N.ptr(b["bev"]), N.ptr(om),
+            N.ptr(plan.inner_sorted), cptr.ctypes.data_as(ctypes_void_p()),
+            g1 - g0, float(scale), N.ptr(A._dvals), N.ptr(counters),
+            N.stream_ptr()), "mf_scatter_offset_blocks")
+        return counters
+
+    def run_blocked(self, A, scale=2.0, counters=None):
+        """Offset-blocked strategy (assembly.py:391-437) on the device."""
+        import torch
+        from . import _native as N
+        from .device import ColorPlan
+        self.build_blocks(A)
         if counters is None:
             counters = torch.zeros(N.MF_NCOUNTERS, dtype=torch.int64,
-                                   device=dev)
-        N.check(L.mf_scatter_offset_blocks(
-            C_byref(self.dmesh.struct), C_byref(A._pattern_struct()), nproto,
-            R, N.ptr(blk_d), blk_ptr.ctypes.data_as(ctypes_void_p()),
-            N.ptr(B21), N.ptr(B22), N.ptr(bev), N.ptr(om),
-            N.ptr(plan.inner_sorted),
-            plan.color_ptr.ctypes.data_as(ctypes_void_p()), plan.NCOLORS,
-            float(scale), N.ptr(A._dvals), N.ptr(counters), st),
-            "mf_scatter_offset_blocks")
-        self.n_blocks = int(blk.size)
-        return counters
+                                   device=self.device)
+        plan = ColorPlan(self.mesh, None, self.device)
+        return self.scatter_blocks(A, plan, counters, scale)
 
     def finish(self, A, counters):
         """events/asymmetry/symmetrize (assembly.py:440-445, x2 folded)."""
@@ -737,19 +764,15 @@ def assemble(mesh, space, kernel, config=None, *, device=None, flags=0,
             "B200 hot path; use the reference package for it")
     ctx = AssemblyContext(mesh, space, kernel, config, device)
     A = ctx.new_matrix()
-    if resolve_strategy(mesh, config) == "blocked":
-        counters = ctx.run_blocked(A)
-        ctx.finish(A, counters)
-        if not keep_on_device:
-            A._vals = _d2h(A._dvals)
-        return A
+    strategy = resolve_strategy(mesh, config)
     if keep_on_device or config.symmetrize:
-        counters = ctx.run(A, flags=flags)
+        counters = (ctx.run_blocked(A) if strategy == "blocked"
+                    else ctx.run(A, flags=flags))
         ctx.finish(A, counters)
         if not keep_on_device:
             A._vals = _d2h(A._dvals)
         return A
-    counters = ctx.run_streamed(A, flags=flags)
+    counters = ctx.run_streamed(A, flags=flags, strategy=strategy)
     ctx.finish(A, counters)
     ctx.join_streamed(A)
     return A

@@ -64,6 +64,25 @@ int cuda_status(cudaError_t e, const char *where) {
 
 cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Reject host pointers early: a kernel handed a host address would fault
+// asynchronously with "illegal memory access" far from the cause.
+int check_dev(const void *p, const char *name) {
+  if (!p) return MF_OK;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(MF_ERR_ARG, std::string(name) + " is not a CUDA pointer");
+  }
+  if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged)
+    return fail(MF_ERR_ARG, std::string(name) + " is not device memory");
+  return MF_OK;
+}
+
+#define MF_CHECK_DEV(p)                          \
+  do {                                           \
+    if (int rc_ = check_dev((p), #p)) return rc_; \
+  } while (0)
+
 int check_mesh(const MfMesh *m) {
   if (!m) return fail(MF_ERR_ARG, "mesh is NULL");
   if (m->dim != 2 && m->dim != 3) return fail(MF_ERR_ARG, "dim must be 2/3");
@@ -75,12 +94,15 @@ int check_mesh(const MfMesh *m) {
     return fail(MF_ERR_ARG, "mesh array is NULL");
   if (m->ncx < 1 || m->ncy < 1 || m->ncz < 1)
     return fail(MF_ERR_ARG, "bad cell grid");
+  if (int rc = check_dev(m->elem_lo, "mesh.elem_lo")) return rc;
+  if (int rc = check_dev(m->elem_dofs, "mesh.elem_dofs")) return rc;
   return MF_OK;
 }
 
 int check_pattern(const MfPattern *p) {
   if (!p) return fail(MF_ERR_ARG, "pattern is NULL");
   if (p->n > 0 && !p->rowptr) return fail(MF_ERR_ARG, "rowptr is NULL");
+  if (int rc = check_dev(p->rowptr, "pattern.rowptr")) return rc;
   if (p->NX < 1 || p->NY < 1 || p->NZ < 1 || p->K < 0)
     return fail(MF_ERR_ARG, "bad pattern grid");
   if ((int64_t)p->NX * p->NY * p->NZ != p->n)
@@ -225,6 +247,10 @@ int mf_general_core(const MfMesh *mesh, const MfRules *rules,
   int64_t n_inner = color_ptr[ncolors];
   if (n_inner == 0) return MF_OK;
   if (!outer_mask || !inner_sorted) return fail(MF_ERR_ARG, "NULL masks");
+  MF_CHECK_DEV(vals);
+  MF_CHECK_DEV(counters);
+  MF_CHECK_DEV(outer_mask);
+  MF_CHECK_DEV(inner_sorted);
 
   AsmParams P = make_params(mesh, rules, kern, pat, outer_mask, R, scale,
                             vals, counters, flags);
@@ -348,6 +374,8 @@ int mf_asymmetry_inf(const MfPattern *pat, const double *vals, double *out,
                      void *stream) {
   if (int rc = check_pattern(pat)) return rc;
   if (!vals || !out) return fail(MF_ERR_ARG, "NULL array");
+  MF_CHECK_DEV(vals);
+  MF_CHECK_DEV(out);
   return cuda_status(mf_launch_asym(*pat, vals, out, S(stream)),
                      "mf_asymmetry_inf");
 }
@@ -356,6 +384,8 @@ int mf_norm_inf(const MfPattern *pat, const double *vals, double *out,
                 void *stream) {
   if (int rc = check_pattern(pat)) return rc;
   if (!vals || !out) return fail(MF_ERR_ARG, "NULL array");
+  MF_CHECK_DEV(vals);
+  MF_CHECK_DEV(out);
   return cuda_status(mf_launch_norm(*pat, vals, out, S(stream)),
                      "mf_norm_inf");
 }
@@ -364,6 +394,9 @@ int mf_matvec(const MfPattern *pat, const double *vals, const double *x,
               double *y, void *stream) {
   if (int rc = check_pattern(pat)) return rc;
   if (!vals || !x || !y) return fail(MF_ERR_ARG, "NULL array");
+  MF_CHECK_DEV(vals);
+  MF_CHECK_DEV(x);
+  MF_CHECK_DEV(y);
   return cuda_status(mf_launch_matvec(*pat, vals, x, y, S(stream)),
                      "mf_matvec");
 }
@@ -372,12 +405,15 @@ int mf_diag(const MfPattern *pat, const double *vals, double *out,
             void *stream) {
   if (int rc = check_pattern(pat)) return rc;
   if (!vals || !out) return fail(MF_ERR_ARG, "NULL array");
+  MF_CHECK_DEV(vals);
+  MF_CHECK_DEV(out);
   return cuda_status(mf_launch_diag(*pat, vals, out, S(stream)), "mf_diag");
 }
 
 int mf_symmetrize(const MfPattern *pat, double *vals, void *stream) {
   if (int rc = check_pattern(pat)) return rc;
   if (!vals) return fail(MF_ERR_ARG, "NULL array");
+  MF_CHECK_DEV(vals);
   return cuda_status(mf_launch_symmetrize(*pat, vals, S(stream)),
                      "mf_symmetrize");
 }
@@ -385,6 +421,7 @@ int mf_symmetrize(const MfPattern *pat, double *vals, void *stream) {
 int mf_fill_cols(const MfPattern *pat, int64_t *cols, void *stream) {
   if (int rc = check_pattern(pat)) return rc;
   if (!cols) return fail(MF_ERR_ARG, "NULL array");
+  MF_CHECK_DEV(cols);
   return cuda_status(mf_launch_fill_cols(*pat, cols, S(stream)),
                      "mf_fill_cols");
 }

@@ -36,7 +36,7 @@ namespace {
 constexpr int kWarpsPerBlock = 4;
 constexpr int kSplitCap = 64;  // split nodes per level (L_max <= 4)
 #ifndef MF_HEX_MINB
-#define MF_HEX_MINB 3
+#define MF_HEX_MINB 4
 #endif
 #ifndef MF_HEX_BATCH
 #define MF_HEX_BATCH 3

@@ -22,12 +22,19 @@ def _dev(device):
 
 
 def to_device(arr, device, pinned=True):
-    """numpy -> device tensor through a pinned staging copy."""
+    """numpy -> device tensor through a pinned staging copy (device None =
+    the current CUDA device)."""
     import torch
-    t = torch.from_numpy(np.ascontiguousarray(arr))
+    dev = _dev(device)
+    if dev.type != "cuda":
+        raise ValueError(f"to_device needs a CUDA device, got {dev}")
+    a = np.ascontiguousarray(arr)
+    if not a.flags.writeable:
+        a = a.copy()
+    t = torch.from_numpy(a)
     if pinned and t.numel() > 0:
         t = t.pin_memory()
-    return t.to(device, non_blocking=True)
+    return t.to(dev, non_blocking=True)
 
 
 class DeviceMesh:
