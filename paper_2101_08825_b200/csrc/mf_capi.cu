@@ -247,7 +247,8 @@ int mf_general_core(const MfMesh *mesh, const MfRules *rules,
   int64_t n_inner = color_ptr[ncolors];
   if (n_inner == 0) return MF_OK;
   if (!outer_mask || !inner_sorted) return fail(MF_ERR_ARG, "NULL masks");
-  MF_CHECK_DEV(vals);
+  // vals may be a window pointer shifted before its allocation (multi-GPU
+  // row blocks, parallel.py), so only the other arrays are checked
   MF_CHECK_DEV(counters);
   MF_CHECK_DEV(outer_mask);
   MF_CHECK_DEV(inner_sorted);

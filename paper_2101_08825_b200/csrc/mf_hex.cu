@@ -38,8 +38,8 @@ constexpr int kSplitCap = 64;  // split nodes per level (L_max <= 4)
 #ifndef MF_HEX_MINB
 #define MF_HEX_MINB 4
 #endif
-#ifndef MF_HEX_BATCH
-#define MF_HEX_BATCH 3
+#ifndef MF_HEX_GROUP
+#define MF_HEX_GROUP 3
 #endif
 
 struct Box {
@@ -191,24 +191,57 @@ MF_DEV void event_full(const AsmParams &P, const double *s_rt,
   for (int a = 0; a < NO; a++) {
     const double d0 = xsub(C.X[0][a], y[0]);
     const double sq0 = xmul(d0, d0);
-    double W[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // [jy][jz]
+    double mu[NO][NO];
+#if MF_HEX_GROUP == 9
+    double d2v[NO][NO];
+    bool anysh = false;
+    unsigned shm = 0;
 #pragma unroll
     for (int b = 0; b < NO; b++) {
       const double sxy = xadd(sq0, sq1[b]);
-      double d2v[NO], mu[NO];
+#pragma unroll
+      for (int c = 0; c < NO; c++) {
+        const double d2 = xadd(sxy, sq2[c]);
+        d2v[b][c] = d2;
+        if (SHARP) {
+          mu[b][c] = d2 < P.dp2 ? 256.0 : 0.0;
+        } else {
+          const int hi = __double2hiint(d2);
+          const bool pl = hi < P.hi_dm2;
+          const bool sh = !pl && hi <= P.hi_dp2;
+          mu[b][c] = pl ? 256.0 : 0.0;
+          shm |= (unsigned)sh << (b * NO + c);
+          anysh |= sh;
+        }
+      }
+    }
+    if (!SHARP && __any_sync(0xffffffffu, anysh)) {
+#pragma unroll
+      for (int b = 0; b < NO; b++)
+#pragma unroll
+        for (int c = 0; c < NO; c++) {
+          const double v = xi256_unclamped(P, d2v[b][c]);
+          if ((shm >> (b * NO + c)) & 1u) mu[b][c] = v;
+        }
+    }
+#else
+#pragma unroll
+    for (int b = 0; b < NO; b++) {
+      const double sxy = xadd(sq0, sq1[b]);
+      double d2v[NO];
       bool shl[NO];
       bool anysh = false;
 #pragma unroll
       for (int c = 0; c < NO; c++) {
         d2v[c] = xadd(sxy, sq2[c]);
         if (SHARP) {
-          mu[c] = d2v[c] < P.dp2 ? 256.0 : 0.0;
+          mu[b][c] = d2v[c] < P.dp2 ? 256.0 : 0.0;
           shl[c] = false;
         } else {
           const int hi = __double2hiint(d2v[c]);
           const bool pl = hi < P.hi_dm2;
           shl[c] = !pl && hi <= P.hi_dp2;
-          mu[c] = pl ? 256.0 : 0.0;
+          mu[b][c] = pl ? 256.0 : 0.0;
           anysh |= shl[c];
         }
       }
@@ -216,14 +249,19 @@ MF_DEV void event_full(const AsmParams &P, const double *s_rt,
 #pragma unroll
         for (int c = 0; c < NO; c++) {
           const double v = xi256_unclamped(P, d2v[c]);
-          if (shl[c]) mu[c] = v;
+          if (shl[c]) mu[b][c] = v;
         }
       }
+    }
+#endif
+    double W[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // [jy][jz]
+#pragma unroll
+    for (int b = 0; b < NO; b++) {
       double u0 = 0.0, u1 = 0.0;  // z contraction
 #pragma unroll
       for (int c = 0; c < NO; c++) {
-        u0 = fma(mu[c], shz[0][c], u0);
-        u1 = fma(mu[c], shz[1][c], u1);
+        u0 = fma(mu[b][c], shz[0][c], u0);
+        u1 = fma(mu[b][c], shz[1][c], u1);
       }
 #pragma unroll
       for (int jy = 0; jy < 2; jy++) {
