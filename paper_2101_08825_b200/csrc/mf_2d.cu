@@ -23,6 +23,9 @@
 namespace {
 
 constexpr int kMaxLevels = 6;
+#ifndef MF_2D_MINB
+#define MF_2D_MINB 2
+#endif
 
 template <int KIND>
 struct Cfg;
@@ -94,6 +97,23 @@ MF_DEV void make_child(const double *g, int b, double *c) {
     }
     c[4] = 0.0;
     c[5] = 0.0;
+  }
+}
+
+// local DOF offsets on the DOF grid (degree 1, fe_space.py:68-80):
+// tri lower (sw, se, ne), tri upper (sw, ne, nw), quad tensor-lex
+MF_DEV void dof_offset(int kind, int proto, int j, int &ox, int &oy) {
+  if (kind == 1) {
+    if (proto == 0) {
+      ox = j == 0 ? 0 : 1;
+      oy = j == 2 ? 1 : 0;
+    } else {
+      ox = j == 1 ? 1 : 0;
+      oy = j == 0 ? 0 : 1;
+    }
+  } else {
+    ox = j & 1;
+    oy = j >> 1;
   }
 }
 
@@ -290,7 +310,7 @@ enum : int { ACT_NONE = 0, ACT_SPLIT = 1, ACT_UPPER = 2, ACT_PLAT = 3,
 // KIND 1: tri P1 with Dunavant (NO = NI = 7 points, unused template args)
 // KIND 0: quad Q1 with NO / NI points per axis
 template <int KIND, int NO, int NI>
-__global__ void __launch_bounds__(128, 4) k_2d(AsmParams P) {
+__global__ void __launch_bounds__(128, MF_2D_MINB) k_2d(AsmParams P) {
   constexpr int NL = Cfg<KIND>::NL;
   constexpr int NQ1 = KIND == 1 ? 7 : NI * NI;
   constexpr int NQO = KIND == 1 ? 7 : NO;  // per-axis (quad) / total (tri)
@@ -357,6 +377,22 @@ __global__ void __launch_bounds__(128, 4) k_2d(AsmParams P) {
   cell_coords(M.elem_cell[m], M.ncx, M.ncy, cx, cy, cz);
   const int64_t *mdofs = M.elem_dofs + m * M.nloc_max;
   const int Rs = P.R;
+  // implicit-pattern geometry of this element's rows (assembly.py:197-223):
+  // entry (r, c) = rowbase + (gy_c - ylo) * Wx + (gx_c - xlo)
+  const int nproto = KIND == 1 ? 2 : 1;
+  const int tin = (int)(m % nproto);
+  int64_t rowbase[NL];
+  int rxlo[NL], rylo[NL], rwx[NL];
+#pragma unroll
+  for (int i = 0; i < NL; i++) {
+    int ox, oy;
+    dof_offset(KIND, tin, i, ox, oy);
+    const int gx = cx + ox, gy = cy + oy;
+    rxlo[i] = max(gx - P.pat.K, 0);
+    rwx[i] = min(gx + P.pat.K, P.pat.NX - 1) - rxlo[i] + 1;
+    rylo[i] = max(gy - P.pat.K, 0);
+    rowbase[i] = P.pat.rowptr[mdofs[i]];
+  }
 
   for (int dy = -Rs; dy <= Rs; dy++) {
     const int y2 = cy + dy;
@@ -369,6 +405,22 @@ __global__ void __launch_bounds__(128, 4) k_2d(AsmParams P) {
         if (!P.outer_mask[l]) continue;
         if (!(elem_gap<2>(M.elem_lo, M.elem_hi, l, m) < P.dpe)) continue;
         c_pairs++;
+        // value slots of this pair's A21 block, prefetched into L2 now so
+        // the read-modify-write at the end of the pair does not stall
+        const int tout = (int)(l % nproto);
+        int64_t slot[NL][NL];
+#pragma unroll
+        for (int j = 0; j < NL; j++) {
+          int ox, oy;
+          dof_offset(KIND, tout, j, ox, oy);
+          const int gx = x2 + ox, gy = y2 + oy;
+#pragma unroll
+          for (int i = 0; i < NL; i++) {
+            slot[i][j] = rowbase[i] + (int64_t)(gy - rylo[i]) * rwx[i] +
+                         (gx - rxlo[i]);
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(P.vals + slot[i][j]));
+          }
+        }
         OuterTri OT;
         OuterBox OB;
         double root[6];
@@ -488,20 +540,18 @@ __global__ void __launch_bounds__(128, 4) k_2d(AsmParams P) {
           double spsum = 0.0;
 #pragma unroll
           for (int j = 0; j < NL; j++) spsum += SP[j];
-          const int64_t *ldofs = M.elem_dofs + l * M.nloc_max;
           const double sc = -P.scale * scale_in;
 #pragma unroll
           for (int i = 0; i < NL; i++) {
             double mi = 0.0;
 #pragma unroll
             for (int q = 0; q < NQ1; q++) mi += s_phiw[q][i];
-            const int64_t r = mdofs[i];
 #pragma unroll
             for (int j = 0; j < NL; j++) {
               double b = mi * SP[j];
 #pragma unroll
               for (int q = 0; q < NQ1; q++) b = fma(s_phiw[q][i], V[q][j], b);
-              P.vals[pat_index(P.pat, r, ldofs[j])] += sc * b;
+              P.vals[slot[i][j]] += sc * b;
             }
           }
 #pragma unroll
