@@ -110,9 +110,9 @@ struct WarpCtx {
 // pullback shapes (1-s, s) * w_a on axis k; the x axis also carries
 // cde * |sub-cell| / 8 / 256.
 template <int NO>
-MF_DEV void event_axes(const AsmParams &P, const double *s_rt,
-                       const double *s_rw, WarpCtx<NO> &C, int slot,
-                       int lane) {
+MF_DEV void event_axes_to(const AsmParams &P, const double *s_rt,
+                          const double *s_rw, WarpCtx<NO> &C, int slot,
+                          int lane, double (*X)[NO], double (*sh)[2][NO]) {
   if (lane < 3 * NO) {
     const int k = lane / NO, a = lane - (lane / NO) * NO;
     const double lo = C.blo[slot][k], hi = C.bhi[slot][k];
@@ -125,10 +125,17 @@ MF_DEV void event_axes(const AsmParams &P, const double *s_rt,
     }
     const double x = xadd(lo, xmul(s_rt[a], xsub(hi, lo)));
     const double s1 = (x - C.olo[k]) * C.oinv[k];
-    C.X[k][a] = x;
-    C.sh[k][0][a] = (1.0 - s1) * wa;
-    C.sh[k][1][a] = s1 * wa;
+    X[k][a] = x;
+    sh[k][0][a] = (1.0 - s1) * wa;
+    sh[k][1][a] = s1 * wa;
   }
+}
+
+template <int NO>
+MF_DEV void event_axes(const AsmParams &P, const double *s_rt,
+                       const double *s_rw, WarpCtx<NO> &C, int slot,
+                       int lane) {
+  event_axes_to<NO>(P, s_rt, s_rw, C, slot, lane, C.X, C.sh);
   __syncwarp();
 }
 
