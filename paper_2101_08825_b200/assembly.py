@@ -568,10 +568,13 @@ class AssemblyContext:
         work = pair_counts(mesh, self.params, self.dmesh)
         layers = slab_layers(mesh, nslabs, work)
         plan = ColorPlan(mesh, None, self.device, work=work, layers=layers)
-        if strategy == "blocked":
-            self.build_blocks(A)
+        gather = strategy == "blocked" and space.degree == 1
         counters = torch.zeros(N.MF_NCOUNTERS, dtype=torch.int64,
                                device=self.device)
+        if strategy == "blocked":
+            self.build_blocks(A)
+            if gather:
+                self.block_a22(counters)
         d = space.degree
         plane = int(np.prod(space.grid_dims[:-1]))
         nplanes = int(space.grid_dims[-1])
@@ -583,14 +586,16 @@ class AssemblyContext:
         done_plane = 0
         for s_, (lo, hi) in enumerate(layers):
             g0, g1 = plan.group_range(s_)
-            if strategy == "blocked":
+            final = nplanes if s_ == len(layers) - 1 else d * hi
+            if gather:
+                self.gather_blocks(A, done_plane * plane, final * plane)
+            elif strategy == "blocked":
                 self.scatter_blocks(A, plan, counters, groups=(g0, g1))
             else:
                 self.run(A, plan=plan, counters=counters, flags=flags,
                          groups=(g0, g1))
             ev = torch.cuda.Event()
             ev.record(compute)
-            final = nplanes if s_ == len(layers) - 1 else d * hi
             a = int(A.rowptr[done_plane * plane])
             b = int(A.rowptr[final * plane])
             ranges.append((ev, a, b))
@@ -678,8 +683,36 @@ class AssemblyContext:
             N.stream_ptr()), "mf_scatter_offset_blocks")
         return counters
 
+    def block_a22(self, counters):
+        """Per-element sum of realised B22 blocks (mf_offset_block_a22)."""
+        import torch
+        from . import _native as N
+        b = self._blocks
+        kcode = {"quad": 0, "tri": 1, "hex": 2}[self.mesh.kind]
+        nloc = 3 if kcode == 1 else 2 ** self.mesh.dim
+        b["a22"] = torch.empty(self.mesh.n_elements * nloc * nloc,
+                               dtype=torch.float64, device=self.device)
+        b["kcode"] = kcode
+        N.check(N.lib().mf_offset_block_a22(
+            C_byref(self.dmesh.struct), kcode, b["nproto"], b["R"],
+            N.ptr(b["B22"]), N.ptr(b["bev"]), N.ptr(b["a22"]),
+            N.ptr(counters), N.stream_ptr()), "mf_offset_block_a22")
+
+    def gather_blocks(self, A, row0, row1, scale=2.0):
+        """Write vals rows [row0, row1) by the entry-wise gather
+        (mf_gather_offset_blocks)."""
+        from . import _native as N
+        b = self._blocks
+        N.check(N.lib().mf_gather_offset_blocks(
+            C_byref(self.dmesh.struct), C_byref(A._pattern_struct()),
+            b["kcode"], b["nproto"], b["R"], N.ptr(b["B21"]), N.ptr(b["bev"]),
+            N.ptr(b["a22"]), int(row0), int(row1), float(scale),
+            N.ptr(A._dvals), N.stream_ptr()), "mf_gather_offset_blocks")
+
     def run_blocked(self, A, scale=2.0, counters=None):
-        """Offset-blocked strategy (assembly.py:391-437) on the device."""
+        """Offset-blocked strategy (assembly.py:391-437) on the device:
+        the blocks, then the entry-wise gather (degree 1) or the
+        colour-scheduled scatter (degree 2)."""
         import torch
         from . import _native as N
         from .device import ColorPlan
@@ -687,6 +720,10 @@ class AssemblyContext:
         if counters is None:
             counters = torch.zeros(N.MF_NCOUNTERS, dtype=torch.int64,
                                    device=self.device)
+        if self.space.degree == 1:
+            self.block_a22(counters)
+            self.gather_blocks(A, 0, A.n, scale)
+            return counters
         plan = ColorPlan(self.mesh, None, self.device)
         return self.scatter_blocks(A, plan, counters, scale)
 

@@ -727,3 +727,220 @@ cudaError_t mf_launch_blocked_scatter(const AsmParams &P, int nproto, int R,
     k_blocked_scatter<23><<<grid, 128, 0, s>>>(P, S);
   return cudaGetLastError();
 }
+
+// ===========================================================================
+// Blocked strategy, gather form (degree 1, pure quad / tri / hex).
+//
+// vals(r, c) = sum over inner m containing r, outer l containing c with
+// the block of offset cell(l) - cell(m) present and realised, of
+// B21[block][i(r, m)][j(c, l)], plus A22acc[m][i][j(c, m)] when c is a DOF
+// of m -- exactly the sum _scatter_offset_blocks accumulates
+// (_kernels.py:597-647), evaluated entry by entry.  Every value is written
+// once (coalesced, no read-modify-write, no colouring); A22acc (the sum of
+// an element's realised B22 blocks) and the realised events/pairs come
+// from k_blocked_a22, one warp per element.
+namespace {
+
+struct GatherArgs {
+  int nproto, R, nloc, dim, kind;
+  int64_t row0, row1;
+  const double *B21, *B22;
+  const unsigned long long *bev;
+  double *a22;  // (n_elem, nloc, nloc)
+};
+
+// local index of DOF offset (ox, oy, oz) in an element of (kind, proto),
+// -1 if the element does not carry it (degree 1, fe_space.py:68-80)
+MF_DEV int local_of(int kind, int proto, int ox, int oy, int oz) {
+  if (kind == 1) {
+    if (proto == 0) {  // (0,0) (1,0) (1,1)
+      if (ox == 0 && oy == 0) return 0;
+      if (ox == 1 && oy == 0) return 1;
+      if (ox == 1 && oy == 1) return 2;
+    } else {           // (0,0) (1,1) (0,1)
+      if (ox == 0 && oy == 0) return 0;
+      if (ox == 1 && oy == 1) return 1;
+      if (ox == 0 && oy == 1) return 2;
+    }
+    return -1;
+  }
+  return ox + 2 * oy + 4 * oz;
+}
+
+MF_DEV int64_t block_id(int R, int np, int dx, int dy, int dz, int t2,
+                        int t1) {
+  const int span = 2 * R + 1;
+  return ((((int64_t)(dz + R) * span + (dy + R)) * span + (dx + R)) * np +
+          t2) * np + t1;
+}
+
+__global__ void __launch_bounds__(128) k_blocked_a22(AsmParams P,
+                                                     GatherArgs G) {
+  const MfMesh &M = P.mesh;
+  const int lane = threadIdx.x & 31;
+  const int64_t m = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (m >= M.n_elem) return;
+  const int np = G.nproto, nl = G.nloc, ne = nl * nl;
+  const int t1 = (int)(m % np);
+  int cx, cy, cz;
+  cell_coords((int)(m / np), M.ncx, M.ncy, cx, cy, cz);
+  double acc[2] = {0.0, 0.0};
+  unsigned long long ev = 0, pairs = 0;
+  const int zr = G.dim == 3 ? G.R : 0;
+  for (int dz = -zr; dz <= zr; dz++)
+    for (int dy = -G.R; dy <= G.R; dy++)
+      for (int dx = -G.R; dx <= G.R; dx++) {
+        const int ox = cx - dx, oy = cy - dy, oz = cz - dz;
+        if (ox < 0 || ox >= M.ncx || oy < 0 || oy >= M.ncy || oz < 0 ||
+            oz >= M.ncz)
+          continue;
+        for (int t2 = 0; t2 < np; t2++) {
+          const int64_t b = block_id(G.R, np, dx, dy, dz, t2, t1);
+          const unsigned long long e = G.bev[b];
+          if (!e) continue;
+          ev += e;
+          pairs++;
+          const double *b22 = G.B22 + b * ne;
+          for (int u = 0; u < 2; u++) {
+            const int k = lane + 32 * u;
+            if (k < ne) acc[u] += b22[k];
+          }
+        }
+      }
+  double *out = G.a22 + m * ne;
+  for (int u = 0; u < 2; u++) {
+    const int k = lane + 32 * u;
+    if (k < ne) out[k] = acc[u];
+  }
+  if (lane == 0) {
+    counter_add(P.counters + MF_CNT_EVENTS, ev);
+    counter_add(P.counters + MF_CNT_PAIRS, pairs);
+  }
+}
+
+// one warp per DOF row, lanes over the row's entries
+__global__ void __launch_bounds__(256) k_blocked_gather(AsmParams P,
+                                                        GatherArgs G) {
+  const MfMesh &M = P.mesh;
+  const MfPattern &Pt = P.pat;
+  const int lane = threadIdx.x & 31;
+  const int64_t r =
+      G.row0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (r >= G.row1) return;
+  const int np = G.nproto, nl = G.nloc, ne = nl * nl;
+  const int rx = (int)(r % Pt.NX);
+  const int64_t rt = r / Pt.NX;
+  const int ry = (int)(rt % Pt.NY), rz = (int)(rt / Pt.NY);
+  const int xlo = max(rx - Pt.K, 0), xhi = min(rx + Pt.K, Pt.NX - 1);
+  const int ylo = max(ry - Pt.K, 0), yhi = min(ry + Pt.K, Pt.NY - 1);
+  const int zlo = max(rz - Pt.K, 0), zhi = min(rz + Pt.K, Pt.NZ - 1);
+  const int Wx = xhi - xlo + 1, Wy = yhi - ylo + 1;
+  const int nent = Wx * Wy * (zhi - zlo + 1);
+  const int64_t p0 = Pt.rowptr[r];
+  // inner elements holding r (cell r - offset, proto), uniform per warp
+  int mcx[8], mcy[8], mcz[8], mt[8], mi[8];
+  int64_t mid[8];
+  int nm = 0;
+  const int az = G.dim == 3 ? 1 : 0;
+  for (int oz = 0; oz <= az; oz++)
+    for (int oy = 0; oy <= 1; oy++)
+      for (int ox = 0; ox <= 1; ox++)
+        for (int t = 0; t < np; t++) {
+          const int ccx = rx - ox, ccy = ry - oy, ccz = rz - oz;
+          if (ccx < 0 || ccx >= M.ncx || ccy < 0 || ccy >= M.ncy ||
+              ccz < 0 || ccz >= M.ncz)
+            continue;
+          const int i = local_of(G.kind, t, ox, oy, oz);
+          if (i < 0) continue;
+          const int64_t e = ((int64_t)(ccz * M.ncy + ccy) * M.ncx + ccx) *
+                                np + t;
+          mcx[nm] = ccx;
+          mcy[nm] = ccy;
+          mcz[nm] = ccz;
+          mt[nm] = t;
+          mi[nm] = i;
+          mid[nm] = e;
+          nm++;
+        }
+  for (int k = lane; k < nent; k += 32) {
+    const int ix = k % Wx;
+    const int tt = k / Wx;
+    const int cxg = xlo + ix, cyg = ylo + tt % Wy, czg = zlo + tt / Wy;
+    double s = 0.0;
+    for (int a = 0; a < nm; a++) {
+      // A21: outer elements holding c
+      for (int oz = 0; oz <= az; oz++)
+        for (int oy = 0; oy <= 1; oy++)
+          for (int ox = 0; ox <= 1; ox++) {
+            const int lcx = cxg - ox, lcy = cyg - oy, lcz = czg - oz;
+            if (lcx < 0 || lcx >= M.ncx || lcy < 0 || lcy >= M.ncy ||
+                lcz < 0 || lcz >= M.ncz)
+              continue;
+            const int dx = lcx - mcx[a], dy = lcy - mcy[a], dz = lcz - mcz[a];
+            if (dx < -G.R || dx > G.R || dy < -G.R || dy > G.R ||
+                dz < -G.R || dz > G.R)
+              continue;
+            for (int t2 = 0; t2 < np; t2++) {
+              const int j = local_of(G.kind, t2, ox, oy, oz);
+              if (j < 0) continue;
+              const int64_t b = block_id(G.R, np, dx, dy, dz, t2, mt[a]);
+              if (!G.bev[b]) continue;
+              s += G.B21[b * ne + mi[a] * nl + j];
+            }
+          }
+      // A22: c a DOF of m itself
+      const int ox = cxg - mcx[a], oy = cyg - mcy[a], oz = czg - mcz[a];
+      if (ox >= 0 && ox <= 1 && oy >= 0 && oy <= 1 && oz >= 0 && oz <= az) {
+        const int j = local_of(G.kind, mt[a], ox, oy, oz);
+        if (j >= 0) s += G.a22[mid[a] * ne + mi[a] * nl + j];
+      }
+    }
+    P.vals[p0 + k] = P.scale * s;
+  }
+}
+
+}  // namespace
+
+static GatherArgs gather_args(const AsmParams &P, int kind, int nproto,
+                              int R, const double *B21, const double *B22,
+                              const unsigned long long *bev, double *a22) {
+  GatherArgs G;
+  G.nproto = nproto;
+  G.R = R;
+  G.dim = P.mesh.dim;
+  G.kind = kind;
+  G.nloc = kind == 1 ? 3 : (P.mesh.dim == 3 ? 8 : 4);
+  G.B21 = B21;
+  G.B22 = B22;
+  G.bev = bev;
+  G.a22 = a22;
+  G.row0 = 0;
+  G.row1 = P.pat.n;
+  return G;
+}
+
+cudaError_t mf_launch_blocked_a22(const AsmParams &P, int kind, int nproto,
+                                  int R, const double *B22,
+                                  const unsigned long long *bev, double *a22,
+                                  cudaStream_t s) {
+  GatherArgs G = gather_args(P, kind, nproto, R, nullptr, B22, bev, a22);
+  const int64_t t = P.mesh.n_elem * 32;
+  if (t > 0)
+    k_blocked_a22<<<(unsigned)((t + 127) / 128), 128, 0, s>>>(P, G);
+  return cudaGetLastError();
+}
+
+cudaError_t mf_launch_blocked_gather(const AsmParams &P, int kind, int nproto,
+                                     int R, const double *B21,
+                                     const unsigned long long *bev,
+                                     const double *a22, int64_t row0,
+                                     int64_t row1, cudaStream_t s) {
+  GatherArgs G = gather_args(P, kind, nproto, R, B21, nullptr, bev,
+                             const_cast<double *>(a22));
+  G.row0 = row0;
+  G.row1 = row1;
+  const int64_t t = (row1 - row0) * 32;
+  if (t > 0)
+    k_blocked_gather<<<(unsigned)((t + 255) / 256), 256, 0, s>>>(P, G);
+  return cudaGetLastError();
+}
