@@ -359,10 +359,29 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MF_HEX_MINB)
   const int zlo = max(cz - Rs, 0), zhi = min(cz + Rs, M.ncz - 1);
   const int nx = xhi - xlo + 1, ny = yhi - ylo + 1;
   const int ncell = nx * ny * (zhi - zlo + 1);
+  // this lane's two A21 rows: local DOFs oi and oi + 4 of m (same x/y
+  // corner, z and z+1); row box of the implicit pattern per row
+  int rx0, ry0, rz0, rz1, rwx, rwy;
+  int64_t rb0, rb1;
+  {
+    const int oi = lane >> 3;
+    const int gx = cx + (oi & 1), gy = cy + ((oi >> 1) & 1);
+    const int K = P.pat.K;
+    rx0 = max(gx - K, 0);
+    rwx = min(gx + K, P.pat.NX - 1) - rx0 + 1;
+    ry0 = max(gy - K, 0);
+    rwy = min(gy + K, P.pat.NY - 1) - ry0 + 1;
+    rz0 = max(cz - K, 0);
+    rz1 = max(cz + 1 - K, 0);
+    const int64_t *md = M.elem_dofs + m * M.nloc_max;
+    rb0 = P.pat.rowptr[md[oi]];
+    rb1 = P.pat.rowptr[md[oi + 4]];
+  }
 
   for (int base = 0; base < ncell; base += 32) {
     const int ci = base + lane;
     int64_t cand = -1;
+    int cpos = 0;  // candidate cell, packed x | y << 10 | z << 20
     if (ci < ncell) {
       const int x2 = xlo + ci % nx;
       const int tt = ci / nx;
@@ -371,14 +390,17 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MF_HEX_MINB)
       const int64_t c2 = ((int64_t)z2 * M.ncy + y2) * M.ncx + x2;
       const int64_t l = M.cell_ptr[c2];
       if (l < M.cell_ptr[c2 + 1] && P.outer_mask[l] &&
-          elem_gap<3>(M.elem_lo, M.elem_hi, l, m) < P.dpe)
+          elem_gap<3>(M.elem_lo, M.elem_hi, l, m) < P.dpe) {
         cand = l;
+        cpos = x2 | (y2 << 10) | (z2 << 20);
+      }
     }
     unsigned mask = __ballot_sync(0xffffffffu, cand >= 0);
     while (mask) {
       const int src = __ffs(mask) - 1;
       mask &= mask - 1;
       const int64_t l = __shfl_sync(0xffffffffu, cand, src);
+      const int lpos = __shfl_sync(0xffffffffu, cpos, src);
       c_pairs++;
       if (lane < 3) {
         const double lo = M.elem_lo[l * 3 + lane];
@@ -502,11 +524,16 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MF_HEX_MINB)
           b1 = fma(s_phiw[q][oi + 4], v, b1);
         }
         __syncwarp();
-        const int64_t *mdofs = M.elem_dofs + m * M.nloc_max;
-        const int64_t col = M.elem_dofs[l * M.nloc_max + oj];
+        // column DOF oj of l sits at cell(l) + corner offset (hex Q1 DOF
+        // grid = vertex grid, fe_space.py:68-80)
+        const int gx = (lpos & 1023) + (oj & 1);
+        const int gy = ((lpos >> 10) & 1023) + ((oj >> 1) & 1);
+        const int gz = (lpos >> 20) + (oj >> 2);
         const double sc = -P.scale * jac_in;
-        P.vals[pat_index(P.pat, mdofs[oi], col)] += sc * b0;
-        P.vals[pat_index(P.pat, mdofs[oi + 4], col)] += sc * b1;
+        P.vals[rb0 + ((int64_t)(gz - rz0) * rwy + (gy - ry0)) * rwx +
+               (gx - rx0)] += sc * b0;
+        P.vals[rb1 + ((int64_t)(gz - rz1) * rwy + (gy - ry0)) * rwx +
+               (gx - rx0)] += sc * b1;
       }
     }
   }
