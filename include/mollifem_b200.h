@@ -164,22 +164,27 @@ int mf_scatter_offset_blocks(const MfMesh *mesh, const MfPattern *pat,
                              double scale, double *vals, uint64_t *counters,
                              void *stream);
 
-/* Gather form of the blocked scatter (degree 1 only): mf_offset_block_a22
- * sums every element's realised B22 blocks into a22 (n_elem, nloc, nloc)
- * and adds the realised events/pairs to counters; mf_gather_offset_blocks
- * then WRITES (not adds) vals for the rows [row0, row1): each entry (r, c)
- * is the sum over inner m containing r and outer l containing c of the
- * present block of offset cell(l) - cell(m), plus a22 of m when c is a
- * DOF of m -- the same sum _scatter_offset_blocks accumulates, computed
- * entry by entry (coalesced, deterministic, no read-modify-write). */
+/* Gather form of the blocked scatter (degree 1 only).
+ * mf_offset_block_a22 re-lays the present B21 blocks into the gather
+ * table (device scratch of mf_gather_table_doubles() doubles: the block
+ * entries with the cell offset innermost, zero-padded), sums every
+ * element's realised B22 blocks into a22 (n_elem, nloc, nloc) and adds the
+ * realised events/pairs to counters.  mf_gather_offset_blocks then WRITES
+ * (not adds) vals for rows [row0, row1): entry (r, c) is the sum over
+ * inner m containing r and outer l containing c of the present block of
+ * offset cell(m) - cell(l), plus a22 of m when c is a DOF of m -- the sum
+ * _scatter_offset_blocks accumulates, computed entry by entry (coalesced,
+ * deterministic, no read-modify-write). */
+int64_t mf_gather_table_doubles(int32_t dim, int32_t kind, int32_t R);
 int mf_offset_block_a22(const MfMesh *mesh, int32_t kind, int32_t nproto,
-                        int32_t R, const double *B22, const uint64_t *bev,
-                        double *a22, uint64_t *counters, void *stream);
+                        int32_t R, const double *B21, const double *B22,
+                        const uint64_t *bev, double *a22, double *table,
+                        uint64_t *counters, void *stream);
 int mf_gather_offset_blocks(const MfMesh *mesh, const MfPattern *pat,
                             int32_t kind, int32_t nproto, int32_t R,
-                            const double *B21, const uint64_t *bev,
-                            const double *a22, int64_t row0, int64_t row1,
-                            double scale, double *vals, void *stream);
+                            const double *table, const double *a22,
+                            int64_t row0, int64_t row1, double scale,
+                            double *vals, void *stream);
 
 /* Matrix utilities on the implicit pattern (_kernels.py:846-1202). */
 int mf_scale(double *vals, int64_t nnz, double s, void *stream);

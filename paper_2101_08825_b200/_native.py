@@ -82,12 +82,14 @@ _SIGS = {
                                            C.c_int32, _P, _P, _P, _P, _P, _P,
                                            _P, _P, C.c_int32, C.c_double, _P,
                                            _P, _P]),
+    "mf_gather_table_doubles": (C.c_int64, [C.c_int32, C.c_int32,
+                                            C.c_int32]),
     "mf_offset_block_a22": (C.c_int, [C.POINTER(MfMesh), C.c_int32,
                                       C.c_int32, C.c_int32, _P, _P, _P, _P,
-                                      _P]),
+                                      _P, _P, _P]),
     "mf_gather_offset_blocks": (C.c_int, [C.POINTER(MfMesh),
                                           C.POINTER(MfPattern), C.c_int32,
-                                          C.c_int32, C.c_int32, _P, _P, _P,
+                                          C.c_int32, C.c_int32, _P, _P,
                                           C.c_int64, C.c_int64, C.c_double,
                                           _P, _P]),
     "mf_scale": (C.c_int, [_P, C.c_int64, C.c_double, _P]),

@@ -371,14 +371,18 @@ def C_byref(s):
 
 
 def _d2h(t):
-    """Device tensor -> host numpy through a pinned buffer."""
+    """Device float64 vector -> fresh host numpy array (HostStager)."""
     import torch
+    from .device import HostStager
     if t.numel() == 0:
         return np.zeros(0, dtype=np.float64)
-    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
-    h.copy_(t, non_blocking=True)
-    torch.cuda.current_stream().synchronize()
-    return h.numpy()
+    if t.dtype != torch.float64 or t.dim() != 1:
+        return t.cpu().numpy()
+    host = np.empty(t.numel(), dtype=np.float64)
+    ev = torch.cuda.Event()
+    ev.record(torch.cuda.current_stream(t.device))
+    HostStager(t.device).run(t, host, [(ev, 0, t.numel())])
+    return host
 
 
 def _new_matrix(mesh, space, params, config, allocate):
@@ -558,13 +562,14 @@ class AssemblyContext:
 
         import torch
         from . import _native as N
-        from .device import ColorPlan
+        from .device import ColorPlan, HostStager
         from .parallel import pair_counts, slab_layers
         mesh, space = self.mesh, self.space
         axis = mesh.dim - 1
         nl = int(mesh.grid_ncells[axis])
         if nslabs is None:
-            nslabs = max(1, min(4, nl // 4))
+            # ~2 GB of values per range keeps the exposed tail copy short
+            nslabs = int(max(1, min(8, nl // 4, -(-A.nnz * 8 // 2**31))))
         work = pair_counts(mesh, self.params, self.dmesh)
         layers = slab_layers(mesh, nslabs, work)
         plan = ColorPlan(mesh, None, self.device, work=work, layers=layers)
@@ -581,7 +586,6 @@ class AssemblyContext:
         host = np.empty(A.nnz, dtype=np.float64)
         self._stream_host = host
         compute = torch.cuda.current_stream()
-        copy = torch.cuda.Stream(device=self.device)
         ranges = []
         done_plane = 0
         for s_, (lo, hi) in enumerate(layers):
@@ -601,15 +605,10 @@ class AssemblyContext:
             ranges.append((ev, a, b))
             done_plane = final
         src = A._dvals
+        stager = HostStager(self.device)
 
         def worker():
-            ht = torch.from_numpy(host)
-            with torch.cuda.stream(copy):
-                for ev, a, b in ranges:
-                    copy.wait_event(ev)
-                    if b > a:
-                        ht[a:b].copy_(src[a:b])
-                copy.synchronize()
+            stager.run(src, host, ranges)
 
         self._stream_thread = threading.Thread(target=worker, daemon=True)
         self._stream_thread.start()
@@ -684,19 +683,25 @@ class AssemblyContext:
         return counters
 
     def block_a22(self, counters):
-        """Per-element sum of realised B22 blocks (mf_offset_block_a22)."""
+        """Gather table + per-element sums of realised B22 blocks
+        (mf_offset_block_a22)."""
         import torch
         from . import _native as N
+        L = N.lib()
         b = self._blocks
         kcode = {"quad": 0, "tri": 1, "hex": 2}[self.mesh.kind]
         nloc = 3 if kcode == 1 else 2 ** self.mesh.dim
         b["a22"] = torch.empty(self.mesh.n_elements * nloc * nloc,
                                dtype=torch.float64, device=self.device)
+        b["T"] = torch.empty(int(L.mf_gather_table_doubles(
+            self.mesh.dim, kcode, b["R"])), dtype=torch.float64,
+            device=self.device)
         b["kcode"] = kcode
-        N.check(N.lib().mf_offset_block_a22(
+        N.check(L.mf_offset_block_a22(
             C_byref(self.dmesh.struct), kcode, b["nproto"], b["R"],
-            N.ptr(b["B22"]), N.ptr(b["bev"]), N.ptr(b["a22"]),
-            N.ptr(counters), N.stream_ptr()), "mf_offset_block_a22")
+            N.ptr(b["B21"]), N.ptr(b["B22"]), N.ptr(b["bev"]),
+            N.ptr(b["a22"]), N.ptr(b["T"]), N.ptr(counters),
+            N.stream_ptr()), "mf_offset_block_a22")
 
     def gather_blocks(self, A, row0, row1, scale=2.0):
         """Write vals rows [row0, row1) by the entry-wise gather
@@ -705,9 +710,9 @@ class AssemblyContext:
         b = self._blocks
         N.check(N.lib().mf_gather_offset_blocks(
             C_byref(self.dmesh.struct), C_byref(A._pattern_struct()),
-            b["kcode"], b["nproto"], b["R"], N.ptr(b["B21"]), N.ptr(b["bev"]),
-            N.ptr(b["a22"]), int(row0), int(row1), float(scale),
-            N.ptr(A._dvals), N.stream_ptr()), "mf_gather_offset_blocks")
+            b["kcode"], b["nproto"], b["R"], N.ptr(b["T"]), N.ptr(b["a22"]),
+            int(row0), int(row1), float(scale), N.ptr(A._dvals),
+            N.stream_ptr()), "mf_gather_offset_blocks")
 
     def run_blocked(self, A, scale=2.0, counters=None):
         """Offset-blocked strategy (assembly.py:391-437) on the device:

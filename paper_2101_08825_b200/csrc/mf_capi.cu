@@ -21,13 +21,13 @@ cudaError_t mf_launch_blocks(const AsmParams &, int, int, int, double,
                              const double *, double *, double *,
                              unsigned long long *, int64_t, cudaStream_t);
 cudaError_t mf_launch_blocked_a22(const AsmParams &, int, int, int,
-                                  const double *, const unsigned long long *,
+                                  const double *, const double *,
+                                  const unsigned long long *, double *,
                                   double *, cudaStream_t);
 cudaError_t mf_launch_blocked_gather(const AsmParams &, int, int, int,
-                                     const double *,
-                                     const unsigned long long *,
-                                     const double *, int64_t, int64_t,
-                                     cudaStream_t);
+                                     const double *, const double *, int64_t,
+                                     int64_t, cudaStream_t);
+int64_t mf_gather_table_doubles(int, int, int);
 cudaError_t mf_launch_blocked_scatter(const AsmParams &, int, int, int,
                                       const int32_t *, const int64_t *,
                                       const double *, const double *,
@@ -374,37 +374,44 @@ int mf_scatter_offset_blocks(const MfMesh *mesh, const MfPattern *pat,
   return MF_OK;
 }
 
+int64_t mf_gather_table_doubles(int32_t dim, int32_t kind, int32_t R);
+
 int mf_offset_block_a22(const MfMesh *mesh, int32_t kind, int32_t nproto,
-                        int32_t R, const double *B22, const uint64_t *bev,
-                        double *a22, uint64_t *counters, void *stream) {
+                        int32_t R, const double *B21, const double *B22,
+                        const uint64_t *bev, double *a22, double *table,
+                        uint64_t *counters, void *stream) {
   if (int rc = check_mesh(mesh)) return rc;
   if (mesh->degree != 1) return fail(MF_ERR_UNSUPPORTED, "degree 1 only");
   if (kind < 0 || kind > 2 || nproto < 1 || nproto > 2 || R < 1)
     return fail(MF_ERR_ARG, "bad block arguments");
-  if (!B22 || !bev || !a22 || !counters) return fail(MF_ERR_ARG, "NULL");
+  if (!B21 || !B22 || !bev || !a22 || !table || !counters)
+    return fail(MF_ERR_ARG, "NULL");
   MF_CHECK_DEV(a22);
+  MF_CHECK_DEV(table);
   AsmParams P;
   memset(&P, 0, sizeof(P));
   P.mesh = *mesh;
   P.counters = reinterpret_cast<unsigned long long *>(counters);
   return cuda_status(
       mf_launch_blocked_a22(
-          P, kind, nproto, R, B22,
-          reinterpret_cast<const unsigned long long *>(bev), a22, S(stream)),
+          P, kind, nproto, R, B21, B22,
+          reinterpret_cast<const unsigned long long *>(bev), a22, table,
+          S(stream)),
       "mf_offset_block_a22");
 }
 
 int mf_gather_offset_blocks(const MfMesh *mesh, const MfPattern *pat,
                             int32_t kind, int32_t nproto, int32_t R,
-                            const double *B21, const uint64_t *bev,
-                            const double *a22, int64_t row0, int64_t row1,
-                            double scale, double *vals, void *stream) {
+                            const double *table, const double *a22,
+                            int64_t row0, int64_t row1, double scale,
+                            double *vals, void *stream) {
   if (int rc = check_mesh(mesh)) return rc;
   if (int rc = check_pattern(pat)) return rc;
   if (mesh->degree != 1) return fail(MF_ERR_UNSUPPORTED, "degree 1 only");
   if (row0 < 0 || row1 > pat->n || row0 > row1)
     return fail(MF_ERR_ARG, "bad row range");
-  if (!B21 || !bev || !a22 || !vals) return fail(MF_ERR_ARG, "NULL");
+  if (!table || !a22 || !vals) return fail(MF_ERR_ARG, "NULL");
+  if (pat->K != R + 1) return fail(MF_ERR_ARG, "pattern K != R + 1");
   MF_CHECK_DEV(vals);
   AsmParams P;
   memset(&P, 0, sizeof(P));
@@ -412,12 +419,9 @@ int mf_gather_offset_blocks(const MfMesh *mesh, const MfPattern *pat,
   P.pat = *pat;
   P.scale = scale;
   P.vals = vals;
-  return cuda_status(
-      mf_launch_blocked_gather(
-          P, kind, nproto, R, B21,
-          reinterpret_cast<const unsigned long long *>(bev), a22, row0, row1,
-          S(stream)),
-      "mf_gather_offset_blocks");
+  return cuda_status(mf_launch_blocked_gather(P, kind, nproto, R, table,
+                                              a22, row0, row1, S(stream)),
+                     "mf_gather_offset_blocks");
 }
 
 int mf_scale(double *vals, int64_t nnz, double sc, void *stream) {

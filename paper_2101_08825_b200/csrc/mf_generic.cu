@@ -731,86 +731,151 @@ cudaError_t mf_launch_blocked_scatter(const AsmParams &P, int nproto, int R,
 // ===========================================================================
 // Blocked strategy, gather form (degree 1, pure quad / tri / hex).
 //
-// vals(r, c) = sum over inner m containing r, outer l containing c with
-// the block of offset cell(l) - cell(m) present and realised, of
-// B21[block][i(r, m)][j(c, l)], plus A22acc[m][i][j(c, m)] when c is a DOF
-// of m -- exactly the sum _scatter_offset_blocks accumulates
-// (_kernels.py:597-647), evaluated entry by entry.  Every value is written
-// once (coalesced, no read-modify-write, no colouring); A22acc (the sum of
-// an element's realised B22 blocks) and the realised events/pairs come
-// from k_blocked_a22, one warp per element.
+// vals(r, c) = sum over inner m containing r, outer l containing c of the
+// block of offset d = cell(m) - cell(l) (the reference's convention: outer
+// cell at the origin, inner at d*h, _kernels.py:531-548, 622-634), entry
+// (i(r in m), j(c in l)), plus A22acc[m][i][j(c in m)] when c is a DOF of
+// m -- exactly the sum _scatter_offset_blocks accumulates
+// (_kernels.py:597-647), evaluated entry by entry.  Each value is written
+// once (coalesced, deterministic, no read-modify-write, no colouring).
+//
+// Elements holding a DOF are enumerated as "combos" u = (cell offset a_u,
+// proto t_u, local index i_u): 8 for hexes, 4 for quads, 6 for triangles.
+// With r's combo u and c's combo v, d = b_v - a_u - (c - r), so for a fixed
+// (u, v) the lanes of a warp (consecutive columns of one row) read
+// consecutive words of T[u][v][d] -- the block entries re-laid out with
+// the offset innermost and zero-padded to |d| <= R+2 (absent blocks are
+// exactly zero).  A22acc of elements whose whole offset box is realised is
+// one constant per proto, computed once.
 namespace {
 
+struct Combo {
+  int ax, ay, az, t, i;
+};
+
+// combos of a DOF (degree 1): element (cell = dof - a, proto t) carries it
+// as local index i (fe_space.py:68-80)
+MF_DEV int dof_combos(int kind, int dim, Combo *cb) {
+  int n = 0;
+  if (kind == 1) {  // lower (0,0)(1,0)(1,1), upper (0,0)(1,1)(0,1)
+    const int tab[6][4] = {{0, 0, 0, 0}, {1, 0, 0, 1}, {1, 1, 0, 2},
+                           {0, 0, 1, 0}, {1, 1, 1, 1}, {0, 1, 1, 2}};
+    for (int k = 0; k < 6; k++)
+      cb[n++] = {tab[k][0], tab[k][1], 0, tab[k][2], tab[k][3]};
+    return n;
+  }
+  const int az = dim == 3 ? 1 : 0;
+  for (int z = 0; z <= az; z++)
+    for (int y = 0; y <= 1; y++)
+      for (int x = 0; x <= 1; x++) cb[n++] = {x, y, z, 0, x + 2 * y + 4 * z};
+  return n;
+}
+
+MF_DEV int64_t block_id(int R, int np, int dim, int dx, int dy, int dz,
+                        int t2, int t1) {
+  const int span = 2 * R + 1;
+  const int iz = dim == 3 ? dz + R : 0;
+  return ((((int64_t)iz * span + (dy + R)) * span + (dx + R)) * np + t2) *
+             np + t1;
+}
+
 struct GatherArgs {
-  int nproto, R, nloc, dim, kind;
+  int nproto, R, nloc, dim, kind, ncombo, P2;  // P2 = 2R+5 (padded span)
   int64_t row0, row1;
   const double *B21, *B22;
   const unsigned long long *bev;
-  double *a22;  // (n_elem, nloc, nloc)
+  double *T;          // (ncombo, ncombo, P2^dim)
+  double *a22;        // (n_elem, nloc, nloc)
+  double *a22full;    // (nproto, nloc, nloc)
 };
 
-// local index of DOF offset (ox, oy, oz) in an element of (kind, proto),
-// -1 if the element does not carry it (degree 1, fe_space.py:68-80)
-MF_DEV int local_of(int kind, int proto, int ox, int oy, int oz) {
-  if (kind == 1) {
-    if (proto == 0) {  // (0,0) (1,0) (1,1)
-      if (ox == 0 && oy == 0) return 0;
-      if (ox == 1 && oy == 0) return 1;
-      if (ox == 1 && oy == 1) return 2;
-    } else {           // (0,0) (1,1) (0,1)
-      if (ox == 0 && oy == 0) return 0;
-      if (ox == 1 && oy == 1) return 1;
-      if (ox == 0 && oy == 1) return 2;
-    }
-    return -1;
+// T[u][v][d] = B21[block(d, t_v, t_u)][i_u][j_v], zero outside |d| <= R
+__global__ void k_build_T(GatherArgs G) {
+  const int64_t vol = G.dim == 3 ? (int64_t)G.P2 * G.P2 * G.P2
+                                 : (int64_t)G.P2 * G.P2;
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= (int64_t)G.ncombo * G.ncombo * vol) return;
+  Combo cb[8];
+  dof_combos(G.kind, G.dim, cb);
+  const int u = (int)(k / (G.ncombo * vol));
+  const int v = (int)((k / vol) % G.ncombo);
+  int64_t rem = k % vol;
+  const int h = G.R + 2;
+  const int dx = (int)(rem % G.P2) - h;
+  rem /= G.P2;
+  const int dy = (int)(rem % G.P2) - h;
+  const int dz = G.dim == 3 ? (int)(rem / G.P2) - h : 0;
+  double val = 0.0;
+  if (abs(dx) <= G.R && abs(dy) <= G.R && abs(dz) <= G.R) {
+    const int64_t b = block_id(G.R, G.nproto, G.dim, dx, dy, dz, cb[v].t,
+                               cb[u].t);
+    if (G.bev[b])
+      val = G.B21[b * G.nloc * G.nloc + cb[u].i * G.nloc + cb[v].i];
   }
-  return ox + 2 * oy + 4 * oz;
+  G.T[k] = val;
 }
 
-MF_DEV int64_t block_id(int R, int np, int dx, int dy, int dz, int t2,
-                        int t1) {
-  const int span = 2 * R + 1;
-  return ((((int64_t)(dz + R) * span + (dy + R)) * span + (dx + R)) * np +
-          t2) * np + t1;
+// A22acc of a fully realised element, per proto (one warp)
+__global__ void k_a22_full(GatherArgs G) {
+  const int lane = threadIdx.x;
+  const int np = G.nproto, ne = G.nloc * G.nloc;
+  const int zr = G.dim == 3 ? G.R : 0;
+  for (int t1 = 0; t1 < np; t1++)
+    for (int e = lane; e < ne; e += 32) {
+      double acc = 0.0;
+      for (int dz = -zr; dz <= zr; dz++)
+        for (int dy = -G.R; dy <= G.R; dy++)
+          for (int dx = -G.R; dx <= G.R; dx++)
+            for (int t2 = 0; t2 < np; t2++) {
+              const int64_t b = block_id(G.R, np, G.dim, dx, dy, dz, t2, t1);
+              if (G.bev[b]) acc += G.B22[b * ne + e];
+            }
+      G.a22full[t1 * ne + e] = acc;
+    }
 }
 
+// per element: A22acc (boundary elements loop over their realised offset
+// box, interior ones copy the constant) and the realised events / pairs
 __global__ void __launch_bounds__(128) k_blocked_a22(AsmParams P,
                                                      GatherArgs G) {
   const MfMesh &M = P.mesh;
   const int lane = threadIdx.x & 31;
   const int64_t m = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (m >= M.n_elem) return;
-  const int np = G.nproto, nl = G.nloc, ne = nl * nl;
+  const int np = G.nproto, ne = G.nloc * G.nloc;
   const int t1 = (int)(m % np);
   int cx, cy, cz;
   cell_coords((int)(m / np), M.ncx, M.ncy, cx, cy, cz);
+  const int zr = G.dim == 3 ? G.R : 0;
+  // realised offsets: outer cell (c - d) inside the grid
+  const int dxlo = max(-G.R, cx - (M.ncx - 1)), dxhi = min(G.R, cx);
+  const int dylo = max(-G.R, cy - (M.ncy - 1)), dyhi = min(G.R, cy);
+  const int dzlo = max(-zr, cz - (M.ncz - 1)), dzhi = min(zr, cz);
+  const bool full = dxlo == -G.R && dxhi == G.R && dylo == -G.R &&
+                    dyhi == G.R && dzlo == -zr && dzhi == zr;
   double acc[2] = {0.0, 0.0};
   unsigned long long ev = 0, pairs = 0;
-  const int zr = G.dim == 3 ? G.R : 0;
-  for (int dz = -zr; dz <= zr; dz++)
-    for (int dy = -G.R; dy <= G.R; dy++)
-      for (int dx = -G.R; dx <= G.R; dx++) {
-        const int ox = cx - dx, oy = cy - dy, oz = cz - dz;
-        if (ox < 0 || ox >= M.ncx || oy < 0 || oy >= M.ncy || oz < 0 ||
-            oz >= M.ncz)
-          continue;
+  for (int dz = dzlo; dz <= dzhi; dz++)
+    for (int dy = dylo; dy <= dyhi; dy++)
+      for (int dx = dxlo; dx <= dxhi; dx++)
         for (int t2 = 0; t2 < np; t2++) {
-          const int64_t b = block_id(G.R, np, dx, dy, dz, t2, t1);
+          const int64_t b = block_id(G.R, np, G.dim, dx, dy, dz, t2, t1);
           const unsigned long long e = G.bev[b];
           if (!e) continue;
           ev += e;
           pairs++;
-          const double *b22 = G.B22 + b * ne;
-          for (int u = 0; u < 2; u++) {
-            const int k = lane + 32 * u;
-            if (k < ne) acc[u] += b22[k];
+          if (!full) {
+            const double *b22 = G.B22 + b * ne;
+            for (int u = 0; u < 2; u++) {
+              const int k = lane + 32 * u;
+              if (k < ne) acc[u] += b22[k];
+            }
           }
         }
-      }
   double *out = G.a22 + m * ne;
   for (int u = 0; u < 2; u++) {
     const int k = lane + 32 * u;
-    if (k < ne) out[k] = acc[u];
+    if (k < ne) out[k] = full ? G.a22full[t1 * ne + k] : acc[u];
   }
   if (lane == 0) {
     counter_add(P.counters + MF_CNT_EVENTS, ev);
@@ -827,7 +892,7 @@ __global__ void __launch_bounds__(256) k_blocked_gather(AsmParams P,
   const int64_t r =
       G.row0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   if (r >= G.row1) return;
-  const int np = G.nproto, nl = G.nloc, ne = nl * nl;
+  const int np = G.nproto, nl = G.nloc, ne = nl * nl, nc = G.ncombo;
   const int rx = (int)(r % Pt.NX);
   const int64_t rt = r / Pt.NX;
   const int ry = (int)(rt % Pt.NY), rz = (int)(rt / Pt.NY);
@@ -837,93 +902,117 @@ __global__ void __launch_bounds__(256) k_blocked_gather(AsmParams P,
   const int Wx = xhi - xlo + 1, Wy = yhi - ylo + 1;
   const int nent = Wx * Wy * (zhi - zlo + 1);
   const int64_t p0 = Pt.rowptr[r];
-  // inner elements holding r (cell r - offset, proto), uniform per warp
-  int mcx[8], mcy[8], mcz[8], mt[8], mi[8];
-  int64_t mid[8];
-  int nm = 0;
-  const int az = G.dim == 3 ? 1 : 0;
-  for (int oz = 0; oz <= az; oz++)
-    for (int oy = 0; oy <= 1; oy++)
-      for (int ox = 0; ox <= 1; ox++)
-        for (int t = 0; t < np; t++) {
-          const int ccx = rx - ox, ccy = ry - oy, ccz = rz - oz;
-          if (ccx < 0 || ccx >= M.ncx || ccy < 0 || ccy >= M.ncy ||
-              ccz < 0 || ccz >= M.ncz)
-            continue;
-          const int i = local_of(G.kind, t, ox, oy, oz);
-          if (i < 0) continue;
-          const int64_t e = ((int64_t)(ccz * M.ncy + ccy) * M.ncx + ccx) *
-                                np + t;
-          mcx[nm] = ccx;
-          mcy[nm] = ccy;
-          mcz[nm] = ccz;
-          mt[nm] = t;
-          mi[nm] = i;
-          mid[nm] = e;
-          nm++;
-        }
+  Combo cb[8];
+  dof_combos(G.kind, G.dim, cb);
+  // inner elements holding r (uniform per warp)
+  unsigned mexist = 0;
+  int64_t melem[8];
+#pragma unroll
+  for (int u = 0; u < 8; u++) {
+    melem[u] = 0;
+    if (u < nc) {
+      const int ccx = rx - cb[u].ax, ccy = ry - cb[u].ay, ccz = rz - cb[u].az;
+      if (ccx >= 0 && ccx < M.ncx && ccy >= 0 && ccy < M.ncy && ccz >= 0 &&
+          ccz < M.ncz) {
+        mexist |= 1u << u;
+        melem[u] = ((int64_t)(ccz * M.ncy + ccy) * M.ncx + ccx) * np +
+                   cb[u].t;
+      }
+    }
+  }
+  const int h = G.R + 2, P2 = G.P2;
+  const int64_t vol = G.dim == 3 ? (int64_t)P2 * P2 * P2 : (int64_t)P2 * P2;
   for (int k = lane; k < nent; k += 32) {
     const int ix = k % Wx;
     const int tt = k / Wx;
     const int cxg = xlo + ix, cyg = ylo + tt % Wy, czg = zlo + tt / Wy;
+    const int Dx = cxg - rx, Dy = cyg - ry, Dz = czg - rz;
+    // outer elements holding c
+    unsigned lexist = 0;
+#pragma unroll
+    for (int v = 0; v < 8; v++) {
+      if (v < nc) {
+        const int lx = cxg - cb[v].ax, ly = cyg - cb[v].ay,
+                  lz = czg - cb[v].az;
+        if (lx >= 0 && lx < M.ncx && ly >= 0 && ly < M.ncy && lz >= 0 &&
+            lz < M.ncz)
+          lexist |= 1u << v;
+      }
+    }
     double s = 0.0;
-    for (int a = 0; a < nm; a++) {
-      // A21: outer elements holding c
-      for (int oz = 0; oz <= az; oz++)
-        for (int oy = 0; oy <= 1; oy++)
-          for (int ox = 0; ox <= 1; ox++) {
-            const int lcx = cxg - ox, lcy = cyg - oy, lcz = czg - oz;
-            if (lcx < 0 || lcx >= M.ncx || lcy < 0 || lcy >= M.ncy ||
-                lcz < 0 || lcz >= M.ncz)
-              continue;
-            const int dx = lcx - mcx[a], dy = lcy - mcy[a], dz = lcz - mcz[a];
-            if (dx < -G.R || dx > G.R || dy < -G.R || dy > G.R ||
-                dz < -G.R || dz > G.R)
-              continue;
-            for (int t2 = 0; t2 < np; t2++) {
-              const int j = local_of(G.kind, t2, ox, oy, oz);
-              if (j < 0) continue;
-              const int64_t b = block_id(G.R, np, dx, dy, dz, t2, mt[a]);
-              if (!G.bev[b]) continue;
-              s += G.B21[b * ne + mi[a] * nl + j];
-            }
-          }
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      if (u >= nc || !((mexist >> u) & 1u)) continue;
+      const double *Tu = G.T + (int64_t)u * nc * vol;
+#pragma unroll
+      for (int v = 0; v < 8; v++) {
+        if (v >= nc || !((lexist >> v) & 1u)) continue;
+        const int dx = cb[v].ax - cb[u].ax - Dx + h;
+        const int dy = cb[v].ay - cb[u].ay - Dy + h;
+        const int dz = G.dim == 3 ? cb[v].az - cb[u].az - Dz + h : 0;
+        s += Tu[v * vol + ((int64_t)dz * P2 + dy) * P2 + dx];
+      }
       // A22: c a DOF of m itself
-      const int ox = cxg - mcx[a], oy = cyg - mcy[a], oz = czg - mcz[a];
-      if (ox >= 0 && ox <= 1 && oy >= 0 && oy <= 1 && oz >= 0 && oz <= az) {
-        const int j = local_of(G.kind, mt[a], ox, oy, oz);
-        if (j >= 0) s += G.a22[mid[a] * ne + mi[a] * nl + j];
+      const int ox = Dx + cb[u].ax, oy = Dy + cb[u].ay, oz = Dz + cb[u].az;
+      if (ox >= 0 && ox <= 1 && oy >= 0 && oy <= 1 && oz >= 0 &&
+          oz <= (G.dim == 3 ? 1 : 0)) {
+        int j = -1;
+        for (int w = 0; w < nc; w++)
+          if (cb[w].t == cb[u].t && cb[w].ax == ox && cb[w].ay == oy &&
+              cb[w].az == oz)
+            j = cb[w].i;
+        if (j >= 0) s += G.a22[melem[u] * ne + cb[u].i * nl + j];
       }
     }
     P.vals[p0 + k] = P.scale * s;
   }
 }
 
-}  // namespace
-
-static GatherArgs gather_args(const AsmParams &P, int kind, int nproto,
-                              int R, const double *B21, const double *B22,
-                              const unsigned long long *bev, double *a22) {
+GatherArgs gather_args(const AsmParams &P, int kind, int nproto, int R,
+                       const double *B21, const double *B22,
+                       const unsigned long long *bev, double *T, double *a22,
+                       double *a22full) {
   GatherArgs G;
   G.nproto = nproto;
   G.R = R;
   G.dim = P.mesh.dim;
   G.kind = kind;
   G.nloc = kind == 1 ? 3 : (P.mesh.dim == 3 ? 8 : 4);
+  G.ncombo = kind == 1 ? 6 : (P.mesh.dim == 3 ? 8 : 4);
+  G.P2 = 2 * R + 5;
   G.B21 = B21;
   G.B22 = B22;
   G.bev = bev;
+  G.T = T;
   G.a22 = a22;
+  G.a22full = a22full;
   G.row0 = 0;
   G.row1 = P.pat.n;
   return G;
 }
 
+}  // namespace
+
+// workspace doubles: T + a22full (a22 is separate)
+int64_t mf_gather_table_doubles(int dim, int kind, int R) {
+  const int64_t P2 = 2 * R + 5;
+  const int nc = kind == 1 ? 6 : (dim == 3 ? 8 : 4);
+  const int nl = kind == 1 ? 3 : (dim == 3 ? 8 : 4);
+  return (int64_t)nc * nc * (dim == 3 ? P2 * P2 * P2 : P2 * P2) +
+         2 * nl * nl;
+}
+
 cudaError_t mf_launch_blocked_a22(const AsmParams &P, int kind, int nproto,
-                                  int R, const double *B22,
+                                  int R, const double *B21, const double *B22,
                                   const unsigned long long *bev, double *a22,
-                                  cudaStream_t s) {
-  GatherArgs G = gather_args(P, kind, nproto, R, nullptr, B22, bev, a22);
+                                  double *table, cudaStream_t s) {
+  const int64_t tsz = mf_gather_table_doubles(P.mesh.dim, kind, R);
+  const int nl = kind == 1 ? 3 : (P.mesh.dim == 3 ? 8 : 4);
+  GatherArgs G = gather_args(P, kind, nproto, R, B21, B22, bev, table, a22,
+                             table + tsz - 2 * nl * nl);
+  const int64_t nT = tsz - 2 * nl * nl;
+  k_build_T<<<(unsigned)((nT + 255) / 256), 256, 0, s>>>(G);
+  k_a22_full<<<1, 32, 0, s>>>(G);
   const int64_t t = P.mesh.n_elem * 32;
   if (t > 0)
     k_blocked_a22<<<(unsigned)((t + 127) / 128), 128, 0, s>>>(P, G);
@@ -931,12 +1020,12 @@ cudaError_t mf_launch_blocked_a22(const AsmParams &P, int kind, int nproto,
 }
 
 cudaError_t mf_launch_blocked_gather(const AsmParams &P, int kind, int nproto,
-                                     int R, const double *B21,
-                                     const unsigned long long *bev,
+                                     int R, const double *table,
                                      const double *a22, int64_t row0,
                                      int64_t row1, cudaStream_t s) {
-  GatherArgs G = gather_args(P, kind, nproto, R, B21, nullptr, bev,
-                             const_cast<double *>(a22));
+  GatherArgs G = gather_args(P, kind, nproto, R, nullptr, nullptr, nullptr,
+                             const_cast<double *>(table),
+                             const_cast<double *>(a22), nullptr);
   G.row0 = row0;
   G.row1 = row1;
   const int64_t t = (row1 - row0) * 32;
