@@ -401,6 +401,23 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MF_HEX_MINB)
       mask &= mask - 1;
       const int64_t l = __shfl_sync(0xffffffffu, cand, src);
       const int lpos = __shfl_sync(0xffffffffu, cpos, src);
+      // this lane's two value slots of the pair's A21 block: column DOF oj
+      // of l sits at cell(l) + corner offset (hex Q1 DOF grid = vertex
+      // grid, fe_space.py:68-80); prefetched into L2 now, written at the
+      // end of the pair
+      int64_t slot0, slot1;
+      {
+        const int oj = lane & 7;
+        const int gx = (lpos & 1023) + (oj & 1);
+        const int gy = ((lpos >> 10) & 1023) + ((oj >> 1) & 1);
+        const int gz = (lpos >> 20) + (oj >> 2);
+        slot0 = rb0 + ((int64_t)(gz - rz0) * rwy + (gy - ry0)) * rwx +
+                (gx - rx0);
+        slot1 = rb1 + ((int64_t)(gz - rz1) * rwy + (gy - ry0)) * rwx +
+                (gx - rx0);
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(P.vals + slot0));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(P.vals + slot1));
+      }
       c_pairs++;
       if (lane < 3) {
         const double lo = M.elem_lo[l * 3 + lane];
@@ -524,16 +541,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MF_HEX_MINB)
           b1 = fma(s_phiw[q][oi + 4], v, b1);
         }
         __syncwarp();
-        // column DOF oj of l sits at cell(l) + corner offset (hex Q1 DOF
-        // grid = vertex grid, fe_space.py:68-80)
-        const int gx = (lpos & 1023) + (oj & 1);
-        const int gy = ((lpos >> 10) & 1023) + ((oj >> 1) & 1);
-        const int gz = (lpos >> 20) + (oj >> 2);
         const double sc = -P.scale * jac_in;
-        P.vals[rb0 + ((int64_t)(gz - rz0) * rwy + (gy - ry0)) * rwx +
-               (gx - rx0)] += sc * b0;
-        P.vals[rb1 + ((int64_t)(gz - rz1) * rwy + (gy - ry0)) * rwx +
-               (gx - rx0)] += sc * b1;
+        P.vals[slot0] += sc * b0;
+        P.vals[slot1] += sc * b1;
       }
     }
   }

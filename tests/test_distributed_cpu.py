@@ -94,3 +94,14 @@ def test_slab_layers_balanced():
         assert all(L[i][1] == L[i + 1][0] for i in range(world - 1))
         sizes = [b - a for a, b in L]
         assert max(sizes) - min(sizes) <= 1
+
+
+def test_assemble_distributed_scaling_contract():
+    """assemble_distributed must not rescale: SlabAssembler.assemble_local
+    runs the kernels with scale 2 (the folded _finish doubling)."""
+    import inspect
+    from paper_2101_08825_b200 import parallel
+    src = inspect.getsource(parallel.assemble_distributed)
+    assert "full * 2" not in src
+    src2 = inspect.getsource(parallel.SlabAssembler.assemble_local)
+    assert "scale" not in src2 or "scale=2" in src2

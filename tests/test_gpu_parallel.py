@@ -35,3 +35,22 @@ def test_slab_decomposition_on_one_device(name, world):
     full, events = emulate_slabs(mesh, space, kp, cfg, world)
     assert events == int(g["events"])
     assert rel_frob(full.cpu().numpy(), g["vals"]) <= 1e-12
+
+
+def test_assemble_distributed_single_rank(tmp_path):
+    """The multi-GPU entry point on a 1-rank NCCL group equals the
+    reference (scaling contract, finish path, gather)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2101_08825_b200.parallel import assemble_distributed
+    g = Golden("hex_q1_gl3")
+    mesh, space, kp, cfg = g.build()
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"file://{tmp_path}/pg",
+                            rank=0, world_size=1)
+    try:
+        A = assemble_distributed(mesh, space, kp, cfg)
+    finally:
+        dist.destroy_process_group()
+    assert A.events == int(g["events"])
+    assert rel_frob(A.vals, g["vals"]) <= 1e-12
