@@ -394,50 +394,33 @@ __global__ void __launch_bounds__(128, MF_2D_MINB) k_2d(AsmParams P) {
     rowbase[i] = P.pat.rowptr[mdofs[i]];
   }
 
-  // A21 column accumulation: the partners of one stencil row are visited
-  // left to right; a cell's DOFs sit at corner positions 0 (x, y),
-  // 1 (x+1, y), 2 (x+1, y+1), 3 (x, y+1) and the right column (1, 2) of a
-  // cell is the left column (0, 3) of the next, so each DOF column of the
-  // element's rows is read-modified-written once per stencil row instead of
-  // once per pair.
-  const double sc21 = -P.scale * scale_in;
   for (int dy = -Rs; dy <= Rs; dy++) {
     const int y2 = cy + dy;
     if (y2 < 0 || y2 >= M.ncy) continue;
-    double acc[4][NL];
-#pragma unroll
-    for (int u = 0; u < 4; u++)
-#pragma unroll
-      for (int i = 0; i < NL; i++) acc[u][i] = 0.0;
-    int xlast = -1;
     for (int dx = -Rs; dx <= Rs; dx++) {
       const int x2 = cx + dx;
-      if (x2 < 0) continue;
-      if (x2 >= M.ncx) break;
-      xlast = x2;
-      // carry the previous cell's right column in as this cell's left
-#pragma unroll
-      for (int i = 0; i < NL; i++) {
-        acc[0][i] = acc[1][i];
-        acc[3][i] = acc[2][i];
-        acc[1][i] = 0.0;
-        acc[2][i] = 0.0;
-      }
-      // left-column slots of this cell, prefetched into L2: they are
-      // written after the cell's pairs
-#pragma unroll
-      for (int i = 0; i < NL; i++) {
-        const int64_t s0 = rowbase[i] + (int64_t)(y2 - rylo[i]) * rwx[i] +
-                           (x2 - rxlo[i]);
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(P.vals + s0));
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(P.vals + s0 + rwx[i]));
-      }
+      if (x2 < 0 || x2 >= M.ncx) continue;
       const int64_t c2 = (int64_t)y2 * M.ncx + x2;
       for (int64_t l = M.cell_ptr[c2]; l < M.cell_ptr[c2 + 1]; l++) {
         if (!P.outer_mask[l]) continue;
         if (!(elem_gap<2>(M.elem_lo, M.elem_hi, l, m) < P.dpe)) continue;
         c_pairs++;
+        // value slots of this pair's A21 block, prefetched into L2 now so
+        // the read-modify-write at the end of the pair does not stall
         const int tout = (int)(l % nproto);
+        int64_t slot[NL][NL];
+#pragma unroll
+        for (int j = 0; j < NL; j++) {
+          int ox, oy;
+          dof_offset(KIND, tout, j, ox, oy);
+          const int gx = x2 + ox, gy = y2 + oy;
+#pragma unroll
+          for (int i = 0; i < NL; i++) {
+            slot[i][j] = rowbase[i] + (int64_t)(gy - rylo[i]) * rwx[i] +
+                         (gx - rxlo[i]);
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(P.vals + slot[i][j]));
+          }
+        }
         OuterTri OT;
         OuterBox OB;
         double root[6];
@@ -557,34 +540,18 @@ __global__ void __launch_bounds__(128, MF_2D_MINB) k_2d(AsmParams P) {
           double spsum = 0.0;
 #pragma unroll
           for (int j = 0; j < NL; j++) spsum += SP[j];
+          const double sc = -P.scale * scale_in;
 #pragma unroll
           for (int i = 0; i < NL; i++) {
             double mi = 0.0;
 #pragma unroll
             for (int q = 0; q < NQ1; q++) mi += s_phiw[q][i];
-            double bj[NL];
 #pragma unroll
             for (int j = 0; j < NL; j++) {
               double b = mi * SP[j];
 #pragma unroll
               for (int q = 0; q < NQ1; q++) b = fma(s_phiw[q][i], V[q][j], b);
-              bj[j] = sc21 * b;
-            }
-            // local DOF j of l -> corner position (dof_offset)
-            if (KIND == 1) {
-              acc[0][i] += bj[0];
-              if (tout == 0) {
-                acc[1][i] += bj[1];
-                acc[2][i] += bj[2];
-              } else {
-                acc[2][i] += bj[1];
-                acc[3][i] += bj[2];
-              }
-            } else {
-              acc[0][i] += bj[0];
-              acc[1][i] += bj[1];
-              acc[3][i] += bj[2 % NL];
-              acc[2][i] += bj[3 % NL];
+              P.vals[slot[i][j]] += sc * b;
             }
           }
 #pragma unroll
@@ -595,24 +562,6 @@ __global__ void __launch_bounds__(128, MF_2D_MINB) k_2d(AsmParams P) {
             G[q] += s;
           }
         }
-      }
-      // the left column (positions 0, 3) of this cell is complete
-#pragma unroll
-      for (int i = 0; i < NL; i++) {
-        const int64_t s0 = rowbase[i] + (int64_t)(y2 - rylo[i]) * rwx[i] +
-                           (x2 - rxlo[i]);
-        if (acc[0][i] != 0.0) P.vals[s0] += acc[0][i];
-        if (acc[3][i] != 0.0) P.vals[s0 + rwx[i]] += acc[3][i];
-      }
-    }
-    // right column of the last cell of the row
-    if (xlast >= 0) {
-#pragma unroll
-      for (int i = 0; i < NL; i++) {
-        const int64_t s0 = rowbase[i] + (int64_t)(y2 - rylo[i]) * rwx[i] +
-                           (xlast + 1 - rxlo[i]);
-        if (acc[1][i] != 0.0) P.vals[s0] += acc[1][i];
-        if (acc[2][i] != 0.0) P.vals[s0 + rwx[i]] += acc[2][i];
       }
     }
   }
