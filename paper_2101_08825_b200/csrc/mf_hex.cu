@@ -77,14 +77,30 @@ enum : int { ACT_NONE = 0, ACT_SPLIT = 1, ACT_UPPER = 2, ACT_PLAT = 3,
 
 // Algorithm-1 decision for one sub-cell (_kernels.py:224-251) plus the
 // dead/plateau proofs for L_max events
+// Algorithm-1 decision for one sub-cell (_kernels.py:224-251) plus the
+// dead/plateau proofs for L_max events.  The proofs use the bounding boxes
+// of the quadrature POINT SETS (outer sub-cell points: lo + t_min/max*(hi -
+// lo); inner element points: pilo/pihi), which lie strictly inside the
+// cells, with a 1e-9 relative margin: every point pair is then certainly
+// beyond delta+eps (the reference skips them all, _kernels.py:134-135) or
+// certainly inside delta-eps (mu == 1 for all of them).  The event is still
+// counted; only its arithmetic changes form.
 MF_DEV int classify(const AsmParams &P, const Box &g, int L,
-                    const double *ilo, const double *ihi) {
+                    const double *ilo, const double *ihi, const double *pilo,
+                    const double *pihi, double tmin, double tmax) {
   if (L < P.L_min) return ACT_SPLIT;
   if (L == P.L_max) {
     if (!(aprx_min_d<3>(g.lo, g.hi, ilo, ihi) < P.dpe)) return ACT_NONE;
     if (!P.shortcuts) return ACT_FULL;
-    if (box_dead<3>(P, g.lo, g.hi, ilo, ihi)) return ACT_DEAD;
-    if (aprx_max_lt_dme(P, aprx_max_sq<3>(g.lo, g.hi, ilo, ihi)))
+    double qlo[3], qhi[3];
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+      const double w = g.hi[k] - g.lo[k];
+      qlo[k] = g.lo[k] + tmin * w;
+      qhi[k] = g.lo[k] + tmax * w;
+    }
+    if (box_dead<3>(P, qlo, qhi, pilo, pihi)) return ACT_DEAD;
+    if (aprx_max_sq<3>(qlo, qhi, pilo, pihi) < P.dm2 * (1.0 - 4e-9))
       return ACT_PLAT;
     return ACT_FULL;
   }
@@ -99,6 +115,7 @@ MF_DEV int classify(const AsmParams &P, const Box &g, int L,
 template <int NO>
 struct WarpCtx {
   double ilo[3], ihi[3];           // inner element box
+  double pilo[3], pihi[3];         // bounding box of its quadrature points
   double olo[3], ohi[3], oinv[3];  // current outer element box
   double blo[33][3], bhi[33][3];   // event boxes of the round (32 = root)
   double X[3][NO];                 // event: outer 1D coordinates
@@ -349,6 +366,22 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MF_HEX_MINB)
                   xmul(xmul(xadd(Rr.box_in_pts[lane * 3 + k], 1.0), 0.5),
                        xsub(C.ihi[k], C.ilo[k])));
   }
+  // point-set bounding boxes (outer rule nodes are sorted ascending)
+  const double tmin = s_rt[0], tmax = s_rt[NO - 1];
+  if (lane < 3) {
+    const double w = C.ihi[lane] - C.ilo[lane];
+    double pmn = 1e300, pmx = -1e300;
+    for (int q = 0; q < NI; q++) {
+      const double tq = xmul(xadd(Rr.box_in_x1d[q], 1.0), 0.5);
+      pmn = fmin(pmn, C.ilo[lane] + tq * w);
+      pmx = fmax(pmx, C.ilo[lane] + tq * w);
+    }
+    // widen by a relative 1e-12 of the cell so rounding of the points'
+    // exact coordinates can never leave the box
+    C.pilo[lane] = pmn - 1e-12 * w;
+    C.pihi[lane] = pmx + 1e-12 * w;
+  }
+  __syncwarp();
   double G = 0.0;
   unsigned c_ev = 0, c_pairs = 0, c_up = 0, c_pl = 0, c_dead = 0, c_full = 0;
   int cx, cy, cz;
@@ -440,7 +473,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MF_HEX_MINB)
           root.lo[k] = C.olo[k];
           root.hi[k] = C.ohi[k];
         }
-        const int act = classify(P, root, 1, C.ilo, C.ihi);
+        const int act = classify(P, root, 1, C.ilo, C.ihi, C.pilo, C.pihi,
+                                 tmin, tmax);
         if (act == ACT_UPPER || act == ACT_PLAT) {
           ev++;
           (act == ACT_UPPER ? c_up : c_pl)++;
@@ -473,7 +507,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MF_HEX_MINB)
                   rt.hi[d] = C.ohi[d];
                 }
                 const Box g = path_box(rt, code, L);
-                a = classify(P, g, L, C.ilo, C.ihi);
+                a = classify(P, g, L, C.ilo, C.ihi, C.pilo, C.pihi, tmin, tmax);
                 if (a >= ACT_UPPER && a != ACT_DEAD) {
 #pragma unroll
                   for (int d = 0; d < 3; d++) {
