@@ -500,6 +500,7 @@ def run_ours(args):
                           "lmax_plateau": int(cnt[N.CNT_EV_PLATEAU]),
                           "lmax_dead": int(cnt[N.CNT_EV_DEAD]),
                           "lmax_full": int(cnt[N.CNT_EV_FULL])},
+        "counters": [int(c) for c in cnt],
         "roofline": roof,
         "gpu_launches": int(args.steps * n_launch),
         "clocks": clk.summary(),

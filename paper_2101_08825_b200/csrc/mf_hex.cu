@@ -270,11 +270,21 @@ MF_DEV void event_full(const AsmParams &P, const double *s_rt,
         }
       }
       if (!SHARP && __any_sync(0xffffffffu, anysh)) {
+#ifdef MF_HEX_STATS
+        unsigned nsh = 0;
 #pragma unroll
-        for (int c = 0; c < NO; c++) {
-          const double v = xi256_unclamped(P, d2v[c]);
-          if (shl[c]) mu[b][c] = v;
+        for (int c = 0; c < NO; c++) nsh += shl[c];
+        nsh = __reduce_add_sync(0xffffffffu, nsh);
+        if (lane == 0) {
+          atomicAdd(P.counters + 6, 1ull);
+          atomicAdd(P.counters + 7, (unsigned long long)nsh);
         }
+#endif
+        double v[NO];
+        xi256_unclamped_n<NO>(P, d2v, v);
+#pragma unroll
+        for (int c = 0; c < NO; c++)
+          if (shl[c]) mu[b][c] = v[c];
       }
     }
 #endif
