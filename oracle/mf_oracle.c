@@ -27,6 +27,15 @@
  * Pinned against the live reference by tests/golden (bit-exact vals,
  * events and candidate lists; see tests/golden/make_golden.py).
  *
+ * Tetrahedra (element kind 3, P1) are NEW: the
+ * reference has no tet element, so event_tet / tet_inv / the 8-child split
+ * below extend Algorithm 1 in the reference's style (box distances on the
+ * sub-cell's vertex bounding box, rank-1 event form, midpoint children by
+ * Bey's red refinement).  Parity for tets is unpinned against the
+ * reference; tests/test_tet.py pins it by identities instead (A 1 = 0,
+ * symmetry, quadrature convergence) and checks the GPU against this code.
+ * In 3D the "tri" rule slots carry the tet rule (points nq x 3).
+ *
  * Extra over the reference (instrumentation only, does not change any
  * arithmetic): an optional event census and a pthread driver that runs
  * disjoint outer-element subsets concurrently (the reference's
@@ -65,9 +74,14 @@ static inline void shape1d(int degree, double t, double *out) {
   }
 }
 
-/* kind: 0 quad, 1 tri, 2 hex */
+/* kind: 0 quad, 1 tri, 2 hex, 3 tet (P1 only) */
 static int shape_at(int kind, int degree, int dim, double r0, double r1,
                     double r2, double *out) {
+  if (kind == 3) {
+    out[0] = ((1.0 - r0) - r1) - r2;
+    out[1] = r0; out[2] = r1; out[3] = r2;
+    return 4;
+  }
   if (kind == 1) {
     double la = 1.0 - r0 - r1;
     if (degree == 1) {
@@ -237,6 +251,83 @@ static void event_tri(const Ctx *c, const double *g, const double *o_v0,
   }
 }
 
+/* tet edge vectors from vertex 0 of g (12 doubles) and the determinant
+ * e1 . (e2 x e3) in a fixed order (shared by event_tet, tet_inv and
+ * inner_data) */
+static inline double tet_edges(const double *g, double *e1, double *e2,
+                               double *e3) {
+  for (int k = 0; k < 3; k++) {
+    e1[k] = g[3 + k] - g[k];
+    e2[k] = g[6 + k] - g[k];
+    e3[k] = g[9 + k] - g[k];
+  }
+  double c0 = e2[1] * e3[2] - e2[2] * e3[1];
+  double c1 = e2[2] * e3[0] - e2[0] * e3[2];
+  double c2 = e2[0] * e3[1] - e2[1] * e3[0];
+  return (e1[0] * c0 + e1[1] * c1) + e1[2] * c2;
+}
+
+/* event on sub-tet g: outer points mapped affinely, weights times |det|,
+ * pulled back through the outer element's inverse map (o_v0, o_inv 3x3) */
+static void event_tet(const Ctx *c, const double *g, const double *o_v0,
+                      const double *o_inv, const double *y1,
+                      const double *w1, int nq1, const double *PHI1,
+                      int nloc1, double *b21, int ldb, double *gsum) {
+  double phi2[4], e1[3], e2[3], e3[3];
+  double det = fabs(tet_edges(g, e1, e2, e3));
+  for (int q2 = 0; q2 < c->nq_tri; q2++) {
+    const double *pt = c->tri_pts + (size_t)q2 * 3;
+    double x[3];
+    for (int k = 0; k < 3; k++)
+      x[k] = ((g[k] + pt[0] * e1[k]) + pt[1] * e2[k]) + pt[2] * e3[k];
+    double w2q = c->tri_w[q2] * det;
+    double d0 = x[0] - o_v0[0], d1 = x[1] - o_v0[1], d2v = x[2] - o_v0[2];
+    double rx = (o_inv[0] * d0 + o_inv[1] * d1) + o_inv[2] * d2v;
+    double ry = (o_inv[3] * d0 + o_inv[4] * d1) + o_inv[5] * d2v;
+    double rz = (o_inv[6] * d0 + o_inv[7] * d1) + o_inv[8] * d2v;
+    shape_at(3, 1, 3, rx, ry, rz, phi2);
+    for (int q1 = 0; q1 < nq1; q1++) {
+      double dx = x[0] - y1[q1 * 3 + 0];
+      double dy = x[1] - y1[q1 * 3 + 1];
+      double dz = x[2] - y1[q1 * 3 + 2];
+      double d2 = (dx * dx + dy * dy) + dz * dz;
+      if (d2 >= c->dp2) {
+        if (c->census) c->census[6]++;
+        continue;
+      }
+      if (c->census) c->census[d2 <= c->dm2 ? 4 : 5]++;
+      double gam = c->cde * mu2(d2, c->dm2, c->dp2, c->delta, c->eps);
+      double tq = gam * w2q;
+      gsum[q1] += tq;
+      double tw = tq * w1[q1];
+      for (int i = 0; i < nloc1; i++) {
+        double ci = tw * PHI1[q1 * nloc1 + i];
+        for (int j = 0; j < 4; j++) b21[i * ldb + j] -= ci * phi2[j];
+      }
+    }
+  }
+}
+
+/* the 8 children of a tet by red refinement (Bey): 4 corner tets and the
+ * interior octahedron cut along the m02-m13 diagonal; vertex lists index
+ * P = {x0, x1, x2, x3, m01, m02, m03, m12, m13, m23} */
+static const int TET_CHILD[8][4] = {{0, 4, 5, 6}, {4, 1, 7, 8}, {5, 7, 2, 9},
+                                    {6, 8, 9, 3}, {4, 5, 6, 8}, {4, 5, 7, 8},
+                                    {5, 6, 8, 9}, {5, 7, 8, 9}};
+
+static void tet_children(const double *g, double (*out)[12]) {
+  double P[10][3];
+  static const int E[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
+  for (int v = 0; v < 4; v++)
+    for (int k = 0; k < 3; k++) P[v][k] = g[3 * v + k];
+  for (int e = 0; e < 6; e++)
+    for (int k = 0; k < 3; k++)
+      P[4 + e][k] = 0.5 * (g[3 * E[e][0] + k] + g[3 * E[e][1] + k]);
+  for (int b = 0; b < 8; b++)
+    for (int v = 0; v < 4; v++)
+      for (int k = 0; k < 3; k++) out[b][3 * v + k] = P[TET_CHILD[b][v]][k];
+}
+
 /* Algorithm 1 for one (outer, inner) pair; returns the event count. */
 static int64_t pair_blocks(const Ctx *c, int okind, const double *ogeo,
                            const double *o_lo, const double *o_hi,
@@ -245,19 +336,24 @@ static int64_t pair_blocks(const Ctx *c, int okind, const double *ogeo,
                            const double *PHI1, int nloc1, const double *i_lo,
                            const double *i_hi, double *b21, double *b22,
                            int ldb, int nloc2, double *gsum,
-                           double (*stack_geo)[6], int *stack_lvl) {
+                           double (*stack_geo)[12], int *stack_lvl) {
   int dim = c->dim;
   int64_t events = 0;
-  double slo[3], shi[3], g[6];
-  for (int t = 0; t < 6; t++) stack_geo[0][t] = ogeo[t];
+  double slo[3], shi[3], g[12];
+  for (int t = 0; t < 12; t++) stack_geo[0][t] = ogeo[t];
   stack_lvl[0] = 1;
   int top = 1;
   for (int q1 = 0; q1 < nq1; q1++) gsum[q1] = 0.0;
   while (top > 0) {
     top -= 1;
-    for (int t = 0; t < 6; t++) g[t] = stack_geo[top][t];
+    for (int t = 0; t < 12; t++) g[t] = stack_geo[top][t];
     int L = stack_lvl[top];
-    if (okind == 1) {
+    if (okind == 3) {
+      for (int k = 0; k < 3; k++) {
+        slo[k] = pymin(g[k], pymin(g[3 + k], pymin(g[6 + k], g[9 + k])));
+        shi[k] = pymax(g[k], pymax(g[3 + k], pymax(g[6 + k], g[9 + k])));
+      }
+    } else if (okind == 1) {
       slo[0] = pymin(g[0], pymin(g[2], g[4]));
       shi[0] = pymax(g[0], pymax(g[2], g[4]));
       slo[1] = pymin(g[1], pymin(g[3], g[5]));
@@ -291,7 +387,10 @@ static int64_t pair_blocks(const Ctx *c, int okind, const double *ogeo,
         else
           c->census[3]++;
       }
-      if (okind == 1)
+      if (okind == 3)
+        event_tet(c, g, o_v0, o_inv, y1, w1, nq1, PHI1, nloc1, b21, ldb,
+                  gsum);
+      else if (okind == 1)
         event_tri(c, g, o_v0, o_inv, y1, w1, nq1, PHI1, nloc1, b21, ldb,
                   gsum, nloc2);
       else
@@ -299,7 +398,11 @@ static int64_t pair_blocks(const Ctx *c, int okind, const double *ogeo,
                   ldb, gsum, nloc2);
     }
     if (do_split) {
-      if (okind == 1) {
+      if (okind == 3) {
+        tet_children(g, stack_geo + top);
+        for (int b = 0; b < 8; b++) stack_lvl[top + b] = L + 1;
+        top += 8;
+      } else if (okind == 1) {
         double m010 = 0.5 * (g[0] + g[2]);
         double m011 = 0.5 * (g[1] + g[3]);
         double m120 = 0.5 * (g[2] + g[4]);
@@ -354,6 +457,18 @@ static int inner_data(int dim, int kind, const double *coords, int nv_max,
                       const double *box_pts, const double *box_w, int nq_box,
                       const double *tri_pts, const double *tri_w, int nq_tri,
                       double *y1, double *w1) {
+  if (kind == 3) {
+    double e1[3], e2[3], e3[3];
+    double det = fabs(tet_edges(coords, e1, e2, e3));
+    for (int q = 0; q < nq_tri; q++) {
+      const double *pt = tri_pts + (size_t)q * 3;
+      for (int k = 0; k < 3; k++)
+        y1[q * 3 + k] =
+            ((coords[k] + pt[0] * e1[k]) + pt[1] * e2[k]) + pt[2] * e3[k];
+      w1[q] = tri_w[q] * det;
+    }
+    return nq_tri;
+  }
   if (kind == 1) {
     const double *c0 = coords, *c1 = coords + dim, *c2 = coords + 2 * dim;
     double e10 = c1[0] - c0[0];
@@ -394,6 +509,21 @@ static void tri_inv(const double *coords, int dim, double *o_v0,
   o_inv[1] = -e20 / det;
   o_inv[2] = -e11 / det;
   o_inv[3] = e10 / det;
+}
+
+/* inverse of the outer tet's edge matrix [e1 e2 e3]: rows (e2 x e3),
+ * (e3 x e1), (e1 x e2) over det */
+static void tet_inv(const double *coords, double *o_v0, double *o_inv) {
+  double e1[3], e2[3], e3[3];
+  double det = tet_edges(coords, e1, e2, e3);
+  const double *a[3][2] = {{e2, e3}, {e3, e1}, {e1, e2}};
+  for (int r = 0; r < 3; r++) {
+    const double *u = a[r][0], *v = a[r][1];
+    o_inv[3 * r + 0] = (u[1] * v[2] - u[2] * v[1]) / det;
+    o_inv[3 * r + 1] = (u[2] * v[0] - u[0] * v[2]) / det;
+    o_inv[3 * r + 2] = (u[0] * v[1] - u[1] * v[0]) / det;
+  }
+  for (int k = 0; k < 3; k++) o_v0[k] = coords[k];
 }
 
 static inline void dof_grid(int64_t r, int NX, int NY, int *gx, int *gy,
@@ -462,7 +592,7 @@ static int64_t general_core_range(const GeneralArgs *a, double *vals,
   int dim = a->dim, degree = a->degree;
   int nl_box = 1;
   for (int k = 0; k < dim; k++) nl_box *= degree + 1;
-  int nl_tri = 3 * degree;
+  int nl_tri = dim == 3 ? 4 : 3 * degree;  /* simplex: tri or tet (P1) */
   int nloc_max = nl_box > nl_tri ? nl_box : nl_tri;
   int nq_max = a->nq_box_in > a->nq_tri_in ? a->nq_box_in : a->nq_tri_in;
   Ctx c;
@@ -491,10 +621,10 @@ static int64_t general_core_range(const GeneralArgs *a, double *vals,
   double *gsum = malloc(sizeof(double) * nq_max);
   double *y1 = malloc(sizeof(double) * nq_max * 3);
   double *w1 = malloc(sizeof(double) * nq_max);
-  double (*stack_geo)[6] = malloc(sizeof(double) * 6 * STACK_CAP);
+  double (*stack_geo)[12] = malloc(sizeof(double) * 12 * STACK_CAP);
   int *stack_lvl = malloc(sizeof(int) * STACK_CAP);
-  double ogeo[6] = {0}, o_lo[3] = {0}, o_hi[3] = {0}, o_v0[2] = {0},
-         o_inv[4] = {0}, i_lo[3], i_hi[3];
+  double ogeo[12] = {0}, o_lo[3] = {0}, o_hi[3] = {0}, o_v0[3] = {0},
+         o_inv[9] = {0}, i_lo[3], i_hi[3];
   int64_t events = 0;
   for (int64_t b0 = o_first; b0 < a->n_outer; b0 += o_step_blk) {
     int64_t b1 = b0 + blk < a->n_outer ? b0 + blk : a->n_outer;
@@ -503,7 +633,11 @@ static int64_t general_core_range(const GeneralArgs *a, double *vals,
       int okind = a->elem_kind[l];
       const double *lc = a->elem_coords + (size_t)l * a->nv_max * dim;
       int nloc2;
-      if (okind == 1) {
+      if (okind == 3) {
+        for (int t = 0; t < 12; t++) ogeo[t] = lc[t];
+        tet_inv(lc, o_v0, o_inv);
+        nloc2 = 4;
+      } else if (okind == 1) {
         for (int t = 0; t < 3; t++) {
           ogeo[2 * t] = lc[t * dim + 0];
           ogeo[2 * t + 1] = lc[t * dim + 1];
@@ -528,12 +662,12 @@ static int64_t general_core_range(const GeneralArgs *a, double *vals,
         }
         const double *PHI1;
         int nloc1, nq1;
-        nq1 = inner_data(dim, ikind == 1 ? 1 : 0,
+        nq1 = inner_data(dim, ikind == 3 ? 3 : (ikind == 1 ? 1 : 0),
                          a->elem_coords + (size_t)m * a->nv_max * dim,
                          a->nv_max, i_lo, i_hi, a->box_in_pts, a->box_in_w,
                          a->nq_box_in, a->tri_in_pts, a->tri_in_w,
                          a->nq_tri_in, y1, w1);
-        if (ikind == 1) {
+        if (ikind == 1 || ikind == 3) {
           PHI1 = a->PHI1_tri;
           nloc1 = nl_tri;
         } else {

@@ -85,11 +85,11 @@ def _grid(mesh):
 
 def candidates(mesh, reach, outer_ids, inner_mask):
     """(ptr, ids) exactly as the reference `_candidates`."""
-    from paper_2101_08825_b200.assembly import stencil_radius
+    from paper_2101_08825_b200.assembly import stencil_pad, stencil_radius
     L = lib()
     flat, cptr = mesh.cell_ptr()
     ncx, ncy, ncz = _grid(mesh)
-    R = stencil_radius(reach, mesh.h)
+    R = stencil_radius(reach + stencil_pad(mesh), mesh.h)
     outer = np.ascontiguousarray(outer_ids, dtype=np.int64)
     mask = np.ascontiguousarray(inner_mask, dtype=np.uint8)
     counts = np.empty(len(outer), dtype=np.int64)

@@ -92,13 +92,20 @@ def stencil_radius(reach, h):
     return int(math.floor(reach / h + 1e-12)) + 1
 
 
+def stencil_pad(mesh):
+    """Extra stencil reach for meshes whose element boxes leave their cells
+    (jittered tets; 0 for the reference's structured meshes)."""
+    return float(getattr(mesh, "stencil_pad", 0.0))
+
+
 def pattern_halfwidth(mesh, params, config, degree):
     """(K, oe): grid half-width of a row's coupling box (assembly.py:313)."""
     if config.method == "barycenter":
         f = 2.0 / 3.0 if mesh.kind in ("tri", "mixed") else 0.5
         oe = int(math.floor(params.delta / mesh.h + f + 1e-12))
     else:
-        oe = int(math.floor((params.delta + params.eps) / mesh.h + 1e-12)) + 1
+        oe = int(math.floor((params.delta + params.eps + stencil_pad(mesh))
+                            / mesh.h + 1e-12)) + 1
     return degree * (oe + 1), oe
 
 
@@ -112,17 +119,25 @@ class PrepTables:
         dim = mesh.dim
         box_kind = "hex" if dim == 3 else "quad"
         outer = config.outer_rule
+        inner = config.inner_rule
         if outer == "default" and config.method == "barycenter":
             outer = "lobatto3"
-        self.box_out = rule_for_kind(box_kind, outer)
-        self.box_in = rule_for_kind(box_kind, config.inner_rule)
-        self.tri_out = rule_for_kind("tri", outer)
-        self.tri_in = rule_for_kind("tri", config.inner_rule)
+        # simplex slots ("tri_*"): triangles in 2D, tetrahedra in 3D (the
+        # tet element is new; its rules are "default" = tet4, tet1/4/11)
+        simplex = "tet" if mesh.kind == "tet" else "tri"
+        if simplex == "tet":
+            box_outer = box_inner = "gauss2"   # unused placeholders
+        else:
+            box_outer, box_inner = outer, inner
+        self.box_out = rule_for_kind(box_kind, box_outer)
+        self.box_in = rule_for_kind(box_kind, box_inner)
+        self.tri_out = rule_for_kind(simplex, outer)
+        self.tri_in = rule_for_kind(simplex, inner)
         deg = space.degree
         self.PHI_box_in = np.ascontiguousarray(
             eval_shape_functions(box_kind, deg, self.box_in.ref_points))
         self.PHI_tri_in = np.ascontiguousarray(
-            eval_shape_functions("tri", deg, self.tri_in.ref_points))
+            eval_shape_functions(simplex, deg, self.tri_in.ref_points))
         self.box_out_pts = np.ascontiguousarray(self.box_out.ref_points)
         self.box_out_w = np.ascontiguousarray(self.box_out.weights)
         self.box_in_pts = np.ascontiguousarray(self.box_in.ref_points)
@@ -132,8 +147,8 @@ class PrepTables:
         self.tri_in_pts = np.ascontiguousarray(self.tri_in.ref_points)
         self.tri_in_w = np.ascontiguousarray(self.tri_in.weights)
         # 1D factors of the tensor box rules (for sum factorisation)
-        self.box_out_1d = _rule_1d(outer)
-        self.box_in_1d = _rule_1d(config.inner_rule)
+        self.box_out_1d = _rule_1d(box_outer)
+        self.box_in_1d = _rule_1d(box_inner)
 
 
 def _rule_1d(preset):
@@ -425,7 +440,7 @@ def candidates(mesh, reach, outer_ids, inner_mask, device=None,
     outer = to_device(np.ascontiguousarray(outer_ids, np.int64), dev)
     mask = to_device(np.ascontiguousarray(inner_mask, np.uint8), dev)
     n = int(outer.numel())
-    R = stencil_radius(reach, mesh.h)
+    R = stencil_radius(reach + stencil_pad(mesh), mesh.h)
     st = N.stream_ptr()
     counts = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
     N.check(L.mf_count_candidates(C_byref(dmesh.struct), N.ptr(outer), n,
@@ -482,7 +497,8 @@ class AssemblyContext:
         self.dmesh = DeviceMesh(mesh, space, device)
         self.drules = DeviceRules(self.prep, device)
         self.device = self.dmesh.device
-        self.R = stencil_radius(params.delta + params.eps, mesh.h)
+        self.R = stencil_radius(params.delta + params.eps + stencil_pad(mesh),
+                                mesh.h)
         self.h2d_bytes = self.dmesh.h2d_bytes
 
     def default_plan(self):
@@ -779,10 +795,13 @@ _TRI_PROTOS = np.array([[[0.0, 0.0], [1.0, 0.0], [1.0, 1.0]],
 
 
 def resolve_strategy(mesh, config):
-    """assembly.py:448-453: "auto" -> blocked on pure quad/tri/hex meshes."""
+    """assembly.py:448-453: "auto" -> blocked on pure quad/tri/hex meshes.
+
+    Tet meshes (new element) always run the general path: jittered meshes
+    have no translation-invariant offset blocks."""
     if config.strategy == "blocked" and mesh.kind not in ("quad", "tri",
                                                           "hex"):
-        raise ValueError("blocked strategy needs a pure-kind mesh")
+        raise ValueError("blocked strategy needs a pure quad/tri/hex mesh")
     if config.strategy != "auto":
         return config.strategy
     return "blocked" if mesh.kind in ("quad", "tri", "hex") else "general"
@@ -829,7 +848,15 @@ def _load_points(mesh, space, sel, code):
     from .fe_space import eval_shape_functions
     deg = space.degree
     box_kind = "hex" if mesh.dim == 3 else "quad"
-    if code == 1:
+    if code == 3:
+        # tetrahedra (new element): degree-4 Keast rule, affine map
+        rule = rule_for_kind("tet", "tet11")
+        kname = "tet"
+        v = mesh.elem_coords[sel, :4, :]
+        E = np.stack([v[:, 1] - v[:, 0], v[:, 2] - v[:, 0],
+                      v[:, 3] - v[:, 0]], axis=2)
+        pts = v[:, None, 0, :] + np.einsum("ekj,qj->eqk", E, rule.ref_points)
+    elif code == 1:
         rule = rule_for_kind("tri", "default")
         kname = "tri"
         v = mesh.elem_coords[sel, :3, :]
@@ -856,13 +883,13 @@ def group_load_device(mesh, space, f, element_ids, dmesh, device=None):
     mf_load_scatter."""
     import torch
     from . import _native as N
-    from .device import ColorPlan, color_of, to_device
+    from .device import color_of, ncolors_of, to_device
     L = N.lib()
     dev = dmesh.device
     load = torch.zeros(space.n_dofs, dtype=torch.float64, device=dev)
     kinds = mesh.elem_kind
     col = color_of(mesh)
-    for code in (0, 1, 2):
+    for code in (0, 1, 2, 3):
         sel = element_ids[kinds[element_ids] == code]
         if len(sel) == 0:
             continue
@@ -871,8 +898,9 @@ def group_load_device(mesh, space, f, element_ids, dmesh, device=None):
         fv = np.asarray(f(pts.reshape(-1, mesh.dim)), dtype=float)
         fv = np.ascontiguousarray(np.broadcast_to(
             fv, (pts.shape[0] * pts.shape[1],)).reshape(len(sel), len(rule)))
-        counts = np.bincount(col[sel], minlength=ColorPlan.NCOLORS)
-        cptr = np.zeros(ColorPlan.NCOLORS + 1, dtype=np.int64)
+        ncol = ncolors_of(mesh)
+        counts = np.bincount(col[sel], minlength=ncol)
+        cptr = np.zeros(ncol + 1, dtype=np.int64)
         np.cumsum(counts, out=cptr[1:])
         elems = to_device(sel.astype(np.int32), dev)
         fvd = to_device(fv, dev)
@@ -880,7 +908,7 @@ def group_load_device(mesh, space, f, element_ids, dmesh, device=None):
         phid = to_device(np.ascontiguousarray(PHI), dev)
         N.check(L.mf_load_scatter(
             C_byref(dmesh.struct), N.ptr(elems),
-            cptr.ctypes.data_as(ctypes_void_p()), ColorPlan.NCOLORS,
+            cptr.ctypes.data_as(ctypes_void_p()), ncol,
             N.ptr(fvd), N.ptr(wd), N.ptr(phid), len(rule), PHI.shape[1],
             N.ptr(load), N.stream_ptr()), "mf_load_scatter")
     return load

@@ -39,6 +39,8 @@ cudaError_t mf_launch_hex(const AsmParams &, cudaStream_t);
 cudaError_t mf_launch_2d(const AsmParams &, cudaStream_t);
 bool mf_hex_supported(const AsmParams &);
 bool mf_2d_supported(const AsmParams &);
+cudaError_t mf_launch_tet(const AsmParams &, cudaStream_t);
+bool mf_tet_supported(const AsmParams &);
 cudaError_t mf_launch_asym(const MfPattern &, const double *, double *,
                            cudaStream_t);
 cudaError_t mf_launch_norm(const MfPattern &, const double *, double *,
@@ -165,7 +167,8 @@ AsmParams make_params(const MfMesh *mesh, const MfRules *rules,
   P.nl_box = mesh->dim == 3 ? (mesh->degree + 1) * (mesh->degree + 1) *
                                   (mesh->degree + 1)
                             : (mesh->degree + 1) * (mesh->degree + 1);
-  P.nl_tri = 3 * mesh->degree;
+  // simplex slots: triangles (3 * degree) in 2D, P1 tetrahedra in 3D
+  P.nl_tri = mesh->dim == 3 ? 4 : 3 * mesh->degree;
   P.shortcuts = (flags & MF_FLAG_NO_SHORTCUTS) == 0 && kern->eps > 0.0;
   return P;
 }
@@ -272,6 +275,22 @@ int mf_general_core(const MfMesh *mesh, const MfRules *rules,
   cudaStream_t s = S(stream);
 
   const bool force_generic = (flags & MF_FLAG_FORCE_GENERIC) != 0;
+  if (mesh->kinds_present & 8) {
+    // tetrahedra (new element) have one kernel, mf_tet.cu
+    if (!mf_tet_supported(P))
+      return fail(MF_ERR_UNSUPPORTED,
+                  "tetrahedra need a pure P1 tet mesh, L_max <= 6 and "
+                  "1/4/11-point tet rules");
+    for (int c = 0; c < ncolors; c++) {
+      int64_t n = color_ptr[c + 1] - color_ptr[c];
+      if (n <= 0) continue;
+      P.inner = inner_sorted + color_ptr[c];
+      P.n_inner = n;
+      cudaError_t e = mf_launch_tet(P, s);
+      if (e != cudaSuccess) return cuda_status(e, "mf_general_core");
+    }
+    return MF_OK;
+  }
   bool use_hex = !force_generic && mf_hex_supported(P);
   bool use_2d = !force_generic && !use_hex && mf_2d_supported(P);
   for (int c = 0; c < ncolors; c++) {

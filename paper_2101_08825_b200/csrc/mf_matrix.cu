@@ -149,7 +149,18 @@ __global__ void k_load(MfMesh M, const int32_t *elems, int64_t n,
   const int64_t e = elems[k];
   const int dim = M.dim;
   double det;
-  if (M.elem_kind[e] == 1) {
+  if (M.elem_kind[e] == 3) {  // tetrahedron: |det| of the edge matrix
+    const double *c = M.elem_coords + e * M.nv_max * 3;
+    double a[3], b[3], d[3];
+    for (int k = 0; k < 3; k++) {
+      a[k] = c[3 + k] - c[k];
+      b[k] = c[6 + k] - c[k];
+      d[k] = c[9 + k] - c[k];
+    }
+    det = fabs(a[0] * (b[1] * d[2] - b[2] * d[1]) +
+               a[1] * (b[2] * d[0] - b[0] * d[2]) +
+               a[2] * (b[0] * d[1] - b[1] * d[0]));
+  } else if (M.elem_kind[e] == 1) {
     const double *c = M.elem_coords + e * M.nv_max * dim;
     const double e10 = c[dim] - c[0], e11 = c[dim + 1] - c[1];
     const double e20 = c[2 * dim] - c[0], e21 = c[2 * dim + 1] - c[1];

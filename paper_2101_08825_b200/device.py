@@ -96,13 +96,26 @@ class DeviceRules:
             n1d_box_in=len(prep.box_in_1d[0]), **p)
 
 
+def _nproto(mesh):
+    return 6 if getattr(mesh, "kind", None) == "tet" else 2
+
+
+def ncolors_of(mesh):
+    """Colours of `color_of`: 16 (2 protos), 48 for Kuhn tets (6 protos)."""
+    return 8 * _nproto(mesh)
+
+
 def color_of(mesh):
-    """Colour id per element: cell parity bits * 2 + proto (< 16)."""
+    """Colour id per element: cell parity bits * nproto + proto.
+
+    Elements of one colour have one proto and lie in cells of one parity
+    (two apart on some axis), so they share no DOF (race-free scatter)."""
     c = mesh.elem_cell.astype(np.int64)
     col = (c[:, 0] & 1) | ((c[:, 1] & 1) << 1)
     if mesh.dim == 3:
         col |= (c[:, 2] & 1) << 2
-    return (col * 2 + mesh.elem_proto.astype(np.int64)).astype(np.int64)
+    return (col * _nproto(mesh)
+            + mesh.elem_proto.astype(np.int64)).astype(np.int64)
 
 
 class ColorPlan:
@@ -121,6 +134,7 @@ class ColorPlan:
     def __init__(self, mesh, inner_ids=None, device=None, work=None,
                  layers=None):
         col = color_of(mesh)
+        self.NCOLORS = ncolors_of(mesh)
         ids = (np.arange(mesh.n_elements, dtype=np.int64) if inner_ids is None
                else np.asarray(inner_ids, dtype=np.int64))
         if layers is None:

@@ -17,8 +17,24 @@ import numpy as np
 __all__ = ["BoundingBox", "Element", "Mesh", "PartitionMap", "build_mesh",
            "refine", "partition_geometric"]
 
-KIND_CODE = {"quad": 0, "tri": 1, "hex": 2}
-KIND_NAME = {0: "quad", 1: "tri", 2: "hex"}
+KIND_CODE = {"quad": 0, "tri": 1, "hex": 2, "tet": 3}
+KIND_NAME = {0: "quad", 1: "tri", 2: "hex", 3: "tet"}
+
+# 6-tet (Kuhn / Freudenthal) split of a cube: tet p follows the axis
+# permutation KUHN_PERMS[p] from corner 0 to corner 7 (corner bit k = axis
+# k).  The triangulation is conforming across cubes.  Odd permutations swap
+# their middle vertices so that every tet is positively oriented.
+KUHN_PERMS = ((0, 1, 2), (0, 2, 1), (1, 0, 2), (1, 2, 0), (2, 0, 1),
+              (2, 1, 0))
+
+
+def kuhn_corners(p):
+    """Cube corner ids (bit k = axis k) of Kuhn tet p, positive orientation."""
+    a, b, _ = KUHN_PERMS[p]
+    v1 = 1 << a
+    v2 = v1 | (1 << b)
+    odd = p in (1, 2, 5)
+    return (0, v2, v1, 7) if odd else (0, v1, v2, 7)
 
 
 class BoundingBox:
@@ -62,6 +78,9 @@ class Element:
             a = self.coords[1] - self.coords[0]
             b = self.coords[2] - self.coords[0]
             return 0.5 * abs(a[0] * b[1] - a[1] * b[0])
+        if self.kind == "tet":
+            e = self.coords[1:4] - self.coords[0]
+            return abs(float(np.linalg.det(e))) / 6.0
         return float(np.prod(self.bbox.hi - self.bbox.lo))
 
     def __repr__(self):
@@ -102,8 +121,11 @@ class Mesh:
     """Structured mesh; see module docstring for the flat arrays."""
 
     def __init__(self, dim, nodes, elem_nodes, h, omega_bounds, gamma_layers,
-                 kind, layer_width, grid_ncells, grid_origin, arrays):
+                 kind, layer_width, grid_ncells, grid_origin, arrays,
+                 jitter=0.0, seed=0):
         self.dim = dim
+        self.jitter = float(jitter)      # fraction of h (tet meshes only)
+        self.seed = int(seed)
         self.nodes = nodes
         self.elem_nodes = elem_nodes
         self.h = h
@@ -120,6 +142,12 @@ class Mesh:
     @property
     def n_elements(self):
         return int(self.elem_kind.shape[0])
+
+    @property
+    def stencil_pad(self):
+        """Extra reach of the cell stencil: element boxes of a jittered mesh
+        stick out of their cells by up to jitter*h on every side."""
+        return 2.0 * self.jitter * self.h
 
     def omega_element_ids(self):
         return np.nonzero(self.elem_region == 0)[0]
@@ -177,24 +205,36 @@ def _as_bounds(omega_bounds, dim):
     return BoundingBox(lo, hi)
 
 
-def build_mesh(dim, omega_bounds, h, layer_width, kind="quad"):
+def build_mesh(dim, omega_bounds, h, layer_width, kind="quad", jitter=0.0,
+               seed=0):
     """Omega tiled at pitch h plus ceil(layer_width/h) Gamma rings.
 
-    kind: quad/tri/mixed in 2D, hex in 3D (mesh.py:153-165).
+    kind: quad/tri/mixed in 2D (mesh.py:153-165); hex or tet in 3D.  "tet"
+    (new, BASELINE configs #4/#5; the reference has no tetrahedra) splits
+    every cube into the 6 Kuhn tets.  jitter (tet only) moves every vertex
+    coordinate by a seeded uniform offset in [-jitter*h, jitter*h], except
+    along axes where the vertex lies on the outer boundary or on an
+    Omega/Gamma interface plane, so the regions stay exact boxes.
     """
     if h <= 0.0:
         raise ValueError("h must be positive")
     if layer_width < 0.0:
         raise ValueError("layer_width must be nonnegative")
     rings = int(math.ceil(layer_width / h - 1e-9)) if layer_width > 0.0 else 0
-    return _build(dim, omega_bounds, h, rings, kind, layer_width)
+    return _build(dim, omega_bounds, h, rings, kind, layer_width, jitter,
+                  seed)
 
 
-def _build(dim, omega_bounds, h, rings, kind, layer_width):
+def _build(dim, omega_bounds, h, rings, kind, layer_width, jitter=0.0,
+           seed=0):
     if dim == 2 and kind not in ("quad", "tri", "mixed"):
         raise ValueError(f"2D mesh kind must be quad/tri/mixed, got {kind!r}")
-    if dim == 3 and kind != "hex":
-        raise ValueError("3D meshes are hex only")
+    if dim == 3 and kind not in ("hex", "tet"):
+        raise ValueError("3D meshes are hex or tet")
+    if jitter and kind != "tet":
+        raise ValueError("jitter is supported for tet meshes only")
+    if not 0.0 <= jitter <= 0.2:
+        raise ValueError("jitter must lie in [0, 0.2] (tets stay valid)")
     if dim not in (2, 3):
         raise ValueError("dim must be 2 or 3")
     box = _as_bounds(omega_bounds, dim)
@@ -223,7 +263,24 @@ def _build(dim, omega_bounds, h, rings, kind, layer_width):
             out = out * nv[k] + g[:, k]
         return out
 
-    if dim == 3:
+    if dim == 3 and kind == "tet":
+        corners = [((v & 1), (v >> 1) & 1, (v >> 2) & 1) for v in range(8)]
+        cn = np.stack([nid(c) for c in corners], axis=1)      # (ncell, 8)
+        # 6 tets per cube, cube-major (cell-lex order of the elements)
+        tets = np.array([kuhn_corners(p) for p in range(6)])  # (6, 4)
+        en = cn[:, tets].reshape(-1, 4)
+        kinds = np.full(en.shape[0], 3, np.int8)
+        protos = np.tile(np.arange(6, dtype=np.int8), len(cidx))
+        cells = np.repeat(cidx, 6, axis=0)
+        regions = np.repeat(region_c, 6)
+        if jitter > 0.0:
+            rng = np.random.default_rng(seed)
+            gidx = np.indices(tuple(nv[::-1])).reshape(dim, -1)[::-1].T
+            off = rng.uniform(-jitter * h, jitter * h, size=nodes.shape)
+            fixed = ((gidx == 0) | (gidx == nv[None, :] - 1)
+                     | (gidx == rings) | (gidx == rings + n_omega[None, :]))
+            nodes = nodes + np.where(fixed, 0.0, off)
+    elif dim == 3:
         corners = [((v & 1), (v >> 1) & 1, (v >> 2) & 1) for v in range(8)]
         en = np.stack([nid(c) for c in corners], axis=1)
         kinds = np.full(len(cidx), 2, np.int8)
@@ -272,13 +329,14 @@ def _build(dim, omega_bounds, h, rings, kind, layer_width):
               cells.astype(np.int32), np.ascontiguousarray(coords),
               np.ascontiguousarray(lo), np.ascontiguousarray(hi))
     return Mesh(dim, nodes, en, h, box, rings, kind, layer_width,
-                tuple(int(x) for x in nc), origin, arrays)
+                tuple(int(x) for x in nc), origin, arrays, jitter, seed)
 
 
 def refine(mesh):
     """Uniform refinement: h halves, ring count doubles."""
     return _build(mesh.dim, mesh.omega_bounds, mesh.h / 2.0,
-                  mesh.gamma_layers * 2, mesh.kind, mesh.layer_width)
+                  mesh.gamma_layers * 2, mesh.kind, mesh.layer_width,
+                  mesh.jitter, mesh.seed)
 
 
 def partition_geometric(mesh, n_parts):

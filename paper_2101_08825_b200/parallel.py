@@ -371,7 +371,7 @@ def pair_counts(mesh, params, dmesh):
     import torch
 
     from . import _native as N
-    from .assembly import stencil_radius
+    from .assembly import stencil_pad, stencil_radius
     n = mesh.n_elements
     dev = dmesh.device
     outer = torch.arange(n, dtype=torch.int64, device=dev)
@@ -380,7 +380,8 @@ def pair_counts(mesh, params, dmesh):
     reach = params.delta + params.eps
     N.check(N.lib().mf_count_candidates(
         ctypes.byref(dmesh.struct), N.ptr(outer), n, N.ptr(mask),
-        stencil_radius(reach, mesh.h), float(reach), N.ptr(counts),
+        stencil_radius(reach + stencil_pad(mesh), mesh.h), float(reach),
+        N.ptr(counts),
         N.stream_ptr()), "mf_count_candidates")
     return counts.cpu().numpy()
 
