@@ -62,7 +62,21 @@ CONFIGS = {
                  "default"),
     "R5": (3, ((0.0, 1.0),) * 3, 1 / 128, 4 / 128, 1 / 512, 2.0, "hex", 2,
            "default"),
+    # BASELINE config #4 as written: 6-tet P1 cubes, 4-point tet rule
+    "R4-tet": (3, ((0.0, 1.0),) * 3, 1 / 64, 0.1, 1 / 128, 2.0, "tet", 2,
+               "tet4"),
+    "R4-tet-small": (3, ((0.0, 0.25),) * 3, 1 / 64, 0.1, 1 / 128, 2.0,
+                     "tet", 2, "tet4"),
+    # BASELINE config #5 (jittered tets, delta = 4h, eps = h/4, 11-point
+    # rule) at half its resolution (64^3 cubes instead of 128^3; the full
+    # size is ~1.3e11 pairs and a 47 GB matrix)
+    "R5-tet-64": (3, ((0.0, 1.0),) * 3, 1 / 64, 4 / 64, 1 / 256, 2.0, "tet",
+                  2, "tet11"),
+    "R5-tet-small": (3, ((0.0, 0.25),) * 3, 1 / 64, 4 / 64, 1 / 256, 2.0,
+                     "tet", 2, "tet11"),
 }
+# vertex jitter (fraction of h, seeded) per workload (tet meshes only)
+JITTER = {"R5-tet-64": 0.1, "R5-tet-small": 0.1}
 
 METRIC = "interacting element-pairs/sec (full nonlocal stiffness assembly)"
 
@@ -78,7 +92,8 @@ def build_problem(name):
                                        build_mesh)
     dim, om, h, delta, eps, kappa, kind, lmax, rule = CONFIGS[name]
     kp = KernelParams(dim, delta, eps, kappa)
-    mesh = build_mesh(dim, om, h, delta + eps, kind)
+    mesh = build_mesh(dim, om, h, delta + eps, kind,
+                      jitter=JITTER.get(name, 0.0), seed=0)
     space = FESpace(mesh, 1)
     cfg = AssemblyConfig(L_max=lmax, outer_rule=rule, inner_rule=rule,
                          strategy="general")
@@ -88,7 +103,12 @@ def build_problem(name):
 def config_json(name, mesh, space, n_gpus, slab_info=None,
                 strategy="general"):
     dim, om, h, delta, eps, kappa, kind, lmax, rule = CONFIGS[name]
-    d = {"workload": name, "strategy": strategy, "dim": dim, "mesh": f"{kind} structured",
+    mdesc = f"{kind} structured"
+    if kind == "tet":
+        mdesc = "6-tet (Kuhn) cubes" + (
+            f", vertices jittered +-{JITTER[name]}h (seed 0)"
+            if name in JITTER else "")
+    d = {"workload": name, "strategy": strategy, "dim": dim, "mesh": mdesc,
          "cells": list(mesh.grid_ncells), "elements": mesh.n_elements,
          "n_dofs": space.n_dofs, "fe_degree": 1, "h": h, "delta": delta,
          "eps": eps, "kappa": kappa, "L_max": lmax,
@@ -179,7 +199,19 @@ def flop_model(name, counters):
     full = int(counters[N.CNT_EV_FULL])
     plat = int(counters[N.CNT_EV_PLATEAU]) + int(counters[N.CNT_EV_UPPER])
     rule = CONFIGS[name][8]
-    if dim == 3:
+    if CONFIGS[name][6] == "tet":
+        nq = {"tet1": 1, "tet4": 4, "tet11": 11}[rule]
+        nq1 = nq2 = nq
+        nl = 4
+        canon_ev = nq2 * nq1 * (3 * dim - 1 + 3) + 2 * nq2 * nq1 * nl \
+            + 2 * nq2 * nl * nl
+        canon_pair = 2 * nq1 * nl * nl
+        # per point pair: 3 sub, 3 mul, 2 add, 4 FMA; per q2: ~40 (map,
+        # pullback, weights)
+        f_full = nq2 * (nq1 * (8 + 8) + 40)
+        f_plat = nq2 * 40
+        f_pair = 2 * nl * nl * nq1 + nq1 * nl + 60
+    elif dim == 3:
         no = ni = 2 if rule == "gauss2" else 3
         nq1, nq2, nl = ni ** 3, no ** 3, 8
         canon_ev = nq2 * nq1 * (3 * dim - 1 + 3) + 2 * nq2 * nq1 * nl \

@@ -8,6 +8,8 @@
 #include <cstring>
 #include <string>
 
+#include <algorithm>
+
 #include "mf_common.cuh"
 
 cudaError_t mf_launch_candidates(const MfMesh &, const int64_t *, int64_t,
@@ -39,7 +41,8 @@ cudaError_t mf_launch_hex(const AsmParams &, cudaStream_t);
 cudaError_t mf_launch_2d(const AsmParams &, cudaStream_t);
 bool mf_hex_supported(const AsmParams &);
 bool mf_2d_supported(const AsmParams &);
-cudaError_t mf_launch_tet(const AsmParams &, cudaStream_t);
+cudaError_t mf_launch_tet(const AsmParams &, double *, cudaStream_t);
+size_t mf_tet_scratch_doubles(const AsmParams &, int64_t);
 bool mf_tet_supported(const AsmParams &);
 cudaError_t mf_launch_asym(const MfPattern &, const double *, double *,
                            cudaStream_t);
@@ -281,15 +284,25 @@ int mf_general_core(const MfMesh *mesh, const MfRules *rules,
       return fail(MF_ERR_UNSUPPORTED,
                   "tetrahedra need a pure P1 tet mesh, L_max <= 6 and "
                   "1/4/11-point tet rules");
-    for (int c = 0; c < ncolors; c++) {
+    // per-plane G partials of one colour: stream-ordered scratch owned by
+    // this call (freed on the stream after the last launch)
+    int64_t nmax = 0;
+    for (int c = 0; c < ncolors; c++)
+      nmax = std::max<int64_t>(nmax, color_ptr[c + 1] - color_ptr[c]);
+    double *gscr = nullptr;
+    cudaError_t e = cudaMallocAsync(
+        &gscr, sizeof(double) * mf_tet_scratch_doubles(P, nmax), s);
+    if (e != cudaSuccess) return cuda_status(e, "mf_general_core scratch");
+    for (int c = 0; c < ncolors && e == cudaSuccess; c++) {
       int64_t n = color_ptr[c + 1] - color_ptr[c];
       if (n <= 0) continue;
       P.inner = inner_sorted + color_ptr[c];
       P.n_inner = n;
-      cudaError_t e = mf_launch_tet(P, s);
-      if (e != cudaSuccess) return cuda_status(e, "mf_general_core");
+      e = mf_launch_tet(P, gscr, s);
     }
-    return MF_OK;
+    cudaError_t ef = cudaFreeAsync(gscr, s);
+    if (e != cudaSuccess) return cuda_status(e, "mf_general_core");
+    return cuda_status(ef, "mf_general_core scratch");
   }
   bool use_hex = !force_generic && mf_hex_supported(P);
   bool use_2d = !force_generic && !use_hex && mf_2d_supported(P);

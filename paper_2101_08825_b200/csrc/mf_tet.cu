@@ -14,11 +14,12 @@
 //     weights times |det|, shapes by pulling back through the outer
 //     element's inverse map (the reference's _event_tri in 3D).
 //
-// Execution follows mf_2d.cu: one thread per INNER element m of the
-// current colour (48 colours: cell parity x 6 protos, so same-colour
-// elements share no DOF and the scatter is race- and atomic-free).  Per
-// pair the thread walks Algorithm 1 depth first with one geometry per
-// level, accumulates V[q1][j] = sum_events sum_q2 gamma w_q2 phi_j(x_q2) and
+// Execution: one thread per (INNER element m of the current colour, stencil
+// z-plane) -- 48 colours (cell parity x 6 protos), so same-colour elements
+// share no DOF; planes of one parity share no outer vertex (see k_tet), so
+// the scatter is race- and atomic-free and deterministic.  Per pair the
+// thread walks Algorithm 1 depth first with one geometry per level,
+// accumulates V[q1][j] = sum_events sum_q2 gamma w_q2 phi_j(x_q2) and
 // contracts it with the inner shapes once per pair; A22 is folded once per
 // element from G[q1] = sum_pairs sum_j V[q1][j].  L_max events are split
 // into dead / plateau / full like the other kernels; point pairs are
@@ -34,13 +35,6 @@ constexpr int kTetLevels = 6;
 __constant__ int8_t c_tet_corner[6][4] = {{0, 1, 3, 7}, {0, 5, 1, 7},
                                           {0, 3, 2, 7}, {0, 2, 6, 7},
                                           {0, 4, 5, 7}, {0, 6, 4, 7}};
-// children of the red refinement over {x0..x3, m01, m02, m03, m12, m13, m23}
-__constant__ int8_t c_tet_child[8][4] = {{0, 4, 5, 6}, {4, 1, 7, 8},
-                                         {5, 7, 2, 9}, {6, 8, 9, 3},
-                                         {4, 5, 6, 8}, {4, 5, 7, 8},
-                                         {5, 6, 8, 9}, {5, 7, 8, 9}};
-__constant__ int8_t c_tet_edge[6][2] = {{0, 1}, {0, 2}, {0, 3},
-                                        {1, 2}, {1, 3}, {2, 3}};
 
 MF_DEV void tet_bbox(const double *g, double *lo, double *hi) {
 #pragma unroll
@@ -50,20 +44,47 @@ MF_DEV void tet_bbox(const double *g, double *lo, double *hi) {
   }
 }
 
-// vertex v of child b of parent tet g (exact midpoints, mf_oracle.c)
+// child b of parent tet g (exact midpoints, oracle tet_children); written
+// with static indices so that g and c stay in registers
 MF_DEV void tet_child(const double *g, int b, double *c) {
+  double m[6][3];  // m01 m02 m03 m12 m13 m23
 #pragma unroll
-  for (int v = 0; v < 4; v++) {
-    const int p = c_tet_child[b][v];
-    if (p < 4) {
+  for (int k = 0; k < 3; k++) {
+    m[0][k] = xmul(0.5, xadd(g[k], g[3 + k]));
+    m[1][k] = xmul(0.5, xadd(g[k], g[6 + k]));
+    m[2][k] = xmul(0.5, xadd(g[k], g[9 + k]));
+    m[3][k] = xmul(0.5, xadd(g[3 + k], g[6 + k]));
+    m[4][k] = xmul(0.5, xadd(g[3 + k], g[9 + k]));
+    m[5][k] = xmul(0.5, xadd(g[6 + k], g[9 + k]));
+  }
+#define MF_V(v, src)                               \
+  {                                                \
+    _Pragma("unroll") for (int k = 0; k < 3; k++) \
+      c[3 * (v) + k] = (src)[k];                   \
+  }
+  switch (b) {
+    case 0: MF_V(0, g) MF_V(1, m[0]) MF_V(2, m[1]) MF_V(3, m[2]) break;
+    case 1: MF_V(0, m[0]) MF_V(1, g + 3) MF_V(2, m[3]) MF_V(3, m[4]) break;
+    case 2: MF_V(0, m[1]) MF_V(1, m[3]) MF_V(2, g + 6) MF_V(3, m[5]) break;
+    case 3: MF_V(0, m[2]) MF_V(1, m[4]) MF_V(2, m[5]) MF_V(3, g + 9) break;
+    case 4: MF_V(0, m[0]) MF_V(1, m[1]) MF_V(2, m[2]) MF_V(3, m[4]) break;
+    case 5: MF_V(0, m[0]) MF_V(1, m[1]) MF_V(2, m[3]) MF_V(3, m[4]) break;
+    case 6: MF_V(0, m[1]) MF_V(1, m[2]) MF_V(2, m[4]) MF_V(3, m[5]) break;
+    default: MF_V(0, m[1]) MF_V(1, m[3]) MF_V(2, m[4]) MF_V(3, m[5])
+  }
+#undef MF_V
+}
+
+// node with path `code` (3 bits per level below the root), recomputed from
+// the root with exact midpoints
+MF_DEV void tet_path(const double *root, uint32_t code, int L, double *g) {
 #pragma unroll
-      for (int k = 0; k < 3; k++) c[3 * v + k] = g[3 * p + k];
-    } else {
-      const int a = c_tet_edge[p - 4][0], e = c_tet_edge[p - 4][1];
+  for (int u = 0; u < 12; u++) g[u] = root[u];
+  for (int l = 2; l <= L; l++) {
+    double c[12];
+    tet_child(g, (code >> (3 * (l - 2))) & 7, c);
 #pragma unroll
-      for (int k = 0; k < 3; k++)
-        c[3 * v + k] = xmul(0.5, xadd(g[3 * a + k], g[3 * e + k]));
-    }
+    for (int u = 0; u < 12; u++) g[u] = c[u];
   }
 }
 
@@ -88,7 +109,7 @@ struct OuterTet {
 // full event on sub-tet g (oracle event_tet)
 template <int NQO, int NQ1, bool SHARP>
 MF_DEV void tet_full(const AsmParams &P, const double *g, const OuterTet &O,
-                     const double (*y)[3], const double *s_pts,
+                     const double (*y)[3][32], int lane, const double *s_pts,
                      const double *s_w, double (*V)[4]) {
   double e[3][3];
   const double det = fabs(tet_edges(g, e));
@@ -114,8 +135,9 @@ MF_DEV void tet_full(const AsmParams &P, const double *g, const OuterTet &O,
     unsigned shm = 0;
 #pragma unroll
     for (int q1 = 0; q1 < NQ1; q1++) {
-      const double dx = xsub(x[0], y[q1][0]), dy = xsub(x[1], y[q1][1]),
-                   dz = xsub(x[2], y[q1][2]);
+      const double dx = xsub(x[0], y[q1][0][lane]),
+                   dy = xsub(x[1], y[q1][1][lane]),
+                   dz = xsub(x[2], y[q1][2][lane]);
       const double dd = xadd(xadd(xmul(dx, dx), xmul(dy, dy)), xmul(dz, dz));
       if (SHARP) {
         mu[q1] = dd < P.dp2 ? 256.0 : 0.0;
@@ -174,31 +196,39 @@ MF_DEV void tet_plateau(const AsmParams &P, const double *g,
 enum : int { ACT_NONE = 0, ACT_SPLIT = 1, ACT_UPPER = 2, ACT_PLAT = 3,
              ACT_DEAD = 4, ACT_FULL = 5 };
 
+// A warp = 32 inner elements (lanes) of the current colour x ONE stencil
+// z-plane dz (blockIdx.y); a launch covers the planes of one parity.  The
+// lanes walk identical offset sequences (converged on unjittered meshes).
+// Same-parity planes are >= 2 cells apart, so their outer tets share no
+// vertex: the A21 scatter of one launch is race-free, and the launches run
+// in a fixed order (deterministic).  Each warp leaves its per-element G
+// partial in gscr[plane][element]; k_tet_a22 sums the planes in order and
+// folds A22.  Warps are independent (no block barrier after the start), so
+// the short planes at |dz| ~ R do not idle behind the long central ones.
+constexpr int kTetWarps = 4;
+
 template <int NQO, int NQ1>
-__global__ void __launch_bounds__(128, 2) k_tet(AsmParams P) {
-  __shared__ double s_phiw[NQ1][4], s_phi[NQ1][4];
+__global__ void __launch_bounds__(32 * kTetWarps, 2)
+    k_tet(AsmParams P, int pass, double *gscr) {
+  __shared__ double s_phiw[NQ1][4];
   __shared__ double s_opts[3 * NQO], s_ow[NQO];
+  __shared__ double s_y[kTetWarps][NQ1][3][32];  // inner points, lane-major
   const MfMesh &M = P.mesh;
   const MfRules &Rr = P.rules;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < NQ1 * 4; i += blockDim.x) {
     const int q = i / 4, j = i % 4;
-    const double ph = Rr.phi_tri_in[q * 4 + j];
-    s_phi[q][j] = ph;
-    s_phiw[q][j] = Rr.tri_in_w[q] * ph;
+    s_phiw[q][j] = Rr.tri_in_w[q] * Rr.phi_tri_in[q * 4 + j];
   }
   for (int i = threadIdx.x; i < NQO; i += blockDim.x) {
 #pragma unroll
     for (int k = 0; k < 3; k++) s_opts[3 * i + k] = Rr.tri_out_pts[3 * i + k];
     s_ow[i] = Rr.tri_out_w[i];
   }
-  __syncthreads();
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= P.n_inner) return;
-  const int64_t m = P.inner[t];
-
-  // inner element: exact points (oracle inner_data) and |det|
-  double y[NQ1][3];
-  double ilo[3], ihi[3], scale_in;
+  const int64_t t = ((int64_t)blockIdx.x * kTetWarps + w) * 32 + lane;
+  const bool valid = t < P.n_inner;
+  const int64_t m = valid ? P.inner[t] : P.inner[0];
+  double scale_in;
   {
     const double *c = M.elem_coords + m * M.nv_max * 3;
     double cg[12];
@@ -206,51 +236,56 @@ __global__ void __launch_bounds__(128, 2) k_tet(AsmParams P) {
     for (int u = 0; u < 12; u++) cg[u] = c[u];
     double e[3][3];
     scale_in = fabs(tet_edges(cg, e));
-#pragma unroll
+    // exact inner points (oracle inner_data)
     for (int q = 0; q < NQ1; q++) {
       const double p0 = Rr.tri_in_pts[3 * q], p1 = Rr.tri_in_pts[3 * q + 1],
                    p2 = Rr.tri_in_pts[3 * q + 2];
 #pragma unroll
       for (int k = 0; k < 3; k++)
-        y[q][k] = xadd(xadd(xadd(cg[k], xmul(p0, e[0][k])),
-                            xmul(p1, e[1][k])),
-                       xmul(p2, e[2][k]));
+        s_y[w][q][k][lane] = xadd(xadd(xadd(cg[k], xmul(p0, e[0][k])),
+                                       xmul(p1, e[1][k])),
+                                  xmul(p2, e[2][k]));
     }
+  }
+  __syncthreads();
+  const int Rs = P.R;
+  const int pidx = pass + 2 * (int)blockIdx.y;  // plane index dz + R
+  const int dz = pidx - Rs;
+  if (!valid) return;
+  double ilo[3], ihi[3];
 #pragma unroll
-    for (int k = 0; k < 3; k++) {
-      ilo[k] = M.elem_lo[m * 3 + k];
-      ihi[k] = M.elem_hi[m * 3 + k];
-    }
+  for (int k = 0; k < 3; k++) {
+    ilo[k] = M.elem_lo[m * 3 + k];
+    ihi[k] = M.elem_hi[m * 3 + k];
   }
   double G[NQ1];
 #pragma unroll
   for (int q = 0; q < NQ1; q++) G[q] = 0.0;
-  unsigned long long c_ev = 0, c_pairs = 0, c_up = 0, c_pl = 0, c_dead = 0,
-                     c_full = 0;
+  unsigned c_ev = 0, c_pairs = 0, c_up = 0, c_pl = 0, c_dead = 0, c_full = 0;
   int cx, cy, cz;
   cell_coords(M.elem_cell[m], M.ncx, M.ncy, cx, cy, cz);
   const int64_t *mdofs = M.elem_dofs + m * M.nloc_max;
-  const int Rs = P.R;
-  // implicit-pattern geometry of this element's 4 rows
-  const int tin = (int)(m % 6);
-  int64_t rowbase[4];
-  int rxlo[4], rylo[4], rzlo[4], rwx[4], rwy[4];
+  const int z2 = cz + dz;
+  if (z2 >= 0 && z2 < M.ncz) {
+    // implicit-pattern geometry of this element's 4 rows
+    const int tin = (int)(m % 6);
+    int64_t rowz[4];
+    int rxlo[4], rylo[4], rwx[4], rwy[4];
 #pragma unroll
-  for (int i = 0; i < 4; i++) {
-    const int v = c_tet_corner[tin][i];
-    const int gx = cx + (v & 1), gy = cy + ((v >> 1) & 1),
-              gz = cz + ((v >> 2) & 1);
-    rxlo[i] = max(gx - P.pat.K, 0);
-    rwx[i] = min(gx + P.pat.K, P.pat.NX - 1) - rxlo[i] + 1;
-    rylo[i] = max(gy - P.pat.K, 0);
-    rwy[i] = min(gy + P.pat.K, P.pat.NY - 1) - rylo[i] + 1;
-    rzlo[i] = max(gz - P.pat.K, 0);
-    rowbase[i] = P.pat.rowptr[mdofs[i]];
-  }
-
-  for (int dz = -Rs; dz <= Rs; dz++) {
-    const int z2 = cz + dz;
-    if (z2 < 0 || z2 >= M.ncz) continue;
+    for (int i = 0; i < 4; i++) {
+      const int v = c_tet_corner[tin][i];
+      const int gx = cx + (v & 1), gy = cy + ((v >> 1) & 1),
+                gz = cz + ((v >> 2) & 1);
+      rxlo[i] = max(gx - P.pat.K, 0);
+      rwx[i] = min(gx + P.pat.K, P.pat.NX - 1) - rxlo[i] + 1;
+      rylo[i] = max(gy - P.pat.K, 0);
+      rwy[i] = min(gy + P.pat.K, P.pat.NY - 1) - rylo[i] + 1;
+      const int rzlo = max(gz - P.pat.K, 0);
+      // row base shifted to the z layer of this plane's outer cubes
+      rowz[i] = P.pat.rowptr[mdofs[i]] +
+                (int64_t)(z2 - rzlo) * rwy[i] * rwx[i];
+    }
+    const double(*y)[3][32] = s_y[w];
     for (int dy = -Rs; dy <= Rs; dy++) {
       const int y2 = cy + dy;
       if (y2 < 0 || y2 >= M.ncy) continue;
@@ -289,15 +324,17 @@ __global__ void __launch_bounds__(128, 2) k_tet(AsmParams P) {
 #pragma unroll
             for (int j = 0; j < 4; j++) V[q][j] = 0.0;
           double SP[4] = {0.0, 0.0, 0.0, 0.0};
-          unsigned long long ev = 0;
-          double geo[kTetLevels + 1][12];
-          int child[kTetLevels + 1];
-#pragma unroll
-          for (int u = 0; u < 12; u++) geo[1][u] = root[u];
+          unsigned ev = 0;
+          // Algorithm 1, depth first over a path code (3 bits per level
+          // below the root); the node is recomputed from the root
+          uint32_t code = 0;
           int L = 1;
+          double g[12];
+#pragma unroll
+          for (int u = 0; u < 12; u++) g[u] = root[u];
           for (;;) {
             double slo[3], shi[3];
-            tet_bbox(geo[L], slo, shi);
+            tet_bbox(g, slo, shi);
             int act = ACT_NONE;
             if (L < P.L_min) {
               act = ACT_SPLIT;
@@ -330,31 +367,28 @@ __global__ void __launch_bounds__(128, 2) k_tet(AsmParams P) {
               const bool full =
                   act == ACT_FULL || (act == ACT_UPPER && !P.shortcuts);
               if (plateau)
-                tet_plateau<NQO>(P, geo[L], O, s_opts, s_ow, SP);
+                tet_plateau<NQO>(P, g, O, s_opts, s_ow, SP);
               else if (full && P.eps > 0.0)
-                tet_full<NQO, NQ1, false>(P, geo[L], O, y, s_opts, s_ow, V);
+                tet_full<NQO, NQ1, false>(P, g, O, y, lane, s_opts, s_ow, V);
               else if (full)
-                tet_full<NQO, NQ1, true>(P, geo[L], O, y, s_opts, s_ow, V);
+                tet_full<NQO, NQ1, true>(P, g, O, y, lane, s_opts, s_ow, V);
             }
             if (act == ACT_SPLIT) {
-              ++L;
-              child[L] = 0;
-              tet_child(geo[L - 1], 0, geo[L]);
+              ++L;  // first child: code bits of level L stay 0
+              double c[12];
+              tet_child(g, 0, c);
+#pragma unroll
+              for (int u = 0; u < 12; u++) g[u] = c[u];
               continue;
             }
-            bool done = false;
-            for (;;) {
-              if (L == 1) {
-                done = true;
-                break;
-              }
-              if (++child[L] < 8) {
-                tet_child(geo[L - 1], child[L], geo[L]);
-                break;
-              }
+            // next sibling, climbing while the current level is exhausted
+            while (L > 1 && ((code >> (3 * (L - 2))) & 7) == 7) {
+              code &= ~(7u << (3 * (L - 2)));
               --L;
             }
-            if (done) break;
+            if (L == 1) break;
+            code += 1u << (3 * (L - 2));
+            tet_path(root, code, L, g);
           }
           if (ev) {
             c_ev += ev;
@@ -372,11 +406,10 @@ __global__ void __launch_bounds__(128, 2) k_tet(AsmParams P) {
                 for (int q = 0; q < NQ1; q++) b = fma(s_phiw[q][i], V[q][j], b);
                 const int v = c_tet_corner[tout][j];
                 const int gx = x2 + (v & 1), gy = y2 + ((v >> 1) & 1),
-                          gz = z2 + ((v >> 2) & 1);
+                          gzo = (v >> 2) & 1;
                 const int64_t slot =
-                    rowbase[i] +
-                    ((int64_t)(gz - rzlo[i]) * rwy[i] + (gy - rylo[i])) *
-                        rwx[i] +
+                    rowz[i] +
+                    ((int64_t)gzo * rwy[i] + (gy - rylo[i])) * rwx[i] +
                     (gx - rxlo[i]);
                 P.vals[slot] += sc * b;
               }
@@ -393,8 +426,45 @@ __global__ void __launch_bounds__(128, 2) k_tet(AsmParams P) {
       }
     }
   }
-  // A22 of the element
-  const double sc = P.scale * scale_in;
+  double *gp = gscr + ((int64_t)pidx * P.n_inner + t) * NQ1;
+#pragma unroll
+  for (int q = 0; q < NQ1; q++) gp[q] = G[q];
+  const unsigned mask = __activemask();
+  const unsigned v[6] = {c_ev, c_pairs, c_up, c_pl, c_dead, c_full};
+  const int slot[6] = {MF_CNT_EVENTS, MF_CNT_PAIRS, MF_CNT_EV_UPPER,
+                       MF_CNT_EV_PLATEAU, MF_CNT_EV_DEAD, MF_CNT_EV_FULL};
+  const bool leader = lane == __ffs(mask) - 1;
+#pragma unroll
+  for (int k = 0; k < 6; k++) {
+    const unsigned s = __reduce_add_sync(mask, v[k]);
+    if (leader && s) atomicAdd(P.counters + slot[k], (unsigned long long)s);
+  }
+}
+
+// A22 of each element from the plane partials of G, summed in plane order
+template <int NQ1>
+__global__ void __launch_bounds__(128) k_tet_a22(AsmParams P,
+                                                 const double *gscr) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= P.n_inner) return;
+  const MfMesh &M = P.mesh;
+  const MfRules &Rr = P.rules;
+  const int64_t m = P.inner[t];
+  double Gt[NQ1];
+#pragma unroll
+  for (int q = 0; q < NQ1; q++) Gt[q] = 0.0;
+  for (int p = 0; p <= 2 * P.R; p++) {
+    const double *gp = gscr + ((int64_t)p * P.n_inner + t) * NQ1;
+#pragma unroll
+    for (int q = 0; q < NQ1; q++) Gt[q] += gp[q];
+  }
+  double cg[12];
+  const double *c = M.elem_coords + m * M.nv_max * 3;
+#pragma unroll
+  for (int u = 0; u < 12; u++) cg[u] = c[u];
+  double e[3][3];
+  const double sc = P.scale * fabs(tet_edges(cg, e));
+  const int64_t *mdofs = M.elem_dofs + m * M.nloc_max;
 #pragma unroll
   for (int i = 0; i < 4; i++) {
     const int64_t r = mdofs[i];
@@ -403,24 +473,27 @@ __global__ void __launch_bounds__(128, 2) k_tet(AsmParams P) {
       double b = 0.0;
 #pragma unroll
       for (int q = 0; q < NQ1; q++)
-        b = fma(G[q] * s_phiw[q][i], s_phi[q][j], b);
+        b = fma(Gt[q] * (Rr.tri_in_w[q] * Rr.phi_tri_in[q * 4 + i]),
+                Rr.phi_tri_in[q * 4 + j], b);
       P.vals[pat_index(P.pat, r, mdofs[j])] += sc * b;
     }
   }
-  unsigned long long *C = P.counters;
-  counter_add(C + MF_CNT_EVENTS, c_ev);
-  counter_add(C + MF_CNT_PAIRS, c_pairs);
-  counter_add(C + MF_CNT_EV_UPPER, c_up);
-  counter_add(C + MF_CNT_EV_PLATEAU, c_pl);
-  counter_add(C + MF_CNT_EV_DEAD, c_dead);
-  counter_add(C + MF_CNT_EV_FULL, c_full);
 }
 
 template <int NQO, int NQ1>
-cudaError_t launch(const AsmParams &P, cudaStream_t s) {
-  const int block = 128;
-  const int64_t grid = (P.n_inner + block - 1) / block;
-  k_tet<NQO, NQ1><<<(unsigned)grid, block, 0, s>>>(P);
+cudaError_t launch(const AsmParams &P, double *gscr, cudaStream_t s) {
+  const unsigned gx = (unsigned)((P.n_inner + 32 * kTetWarps - 1) /
+                                 (32 * kTetWarps));
+  for (int pass = 0; pass < 2; pass++) {
+    const int planes = pass == 0 ? P.R + 1 : P.R;
+    if (planes < 1) continue;
+    k_tet<NQO, NQ1><<<dim3(gx, planes), 32 * kTetWarps, 0, s>>>(P, pass,
+                                                                 gscr);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  k_tet_a22<NQ1><<<(unsigned)((P.n_inner + 127) / 128), 128, 0, s>>>(P,
+                                                                    gscr);
   return cudaGetLastError();
 }
 
@@ -434,10 +507,15 @@ bool mf_tet_supported(const AsmParams &P) {
   return (no == 1 || no == 4 || no == 11) && (ni == 1 || ni == 4 || ni == 11);
 }
 
-cudaError_t mf_launch_tet(const AsmParams &P, cudaStream_t s) {
+size_t mf_tet_scratch_doubles(const AsmParams &P, int64_t n_colour_max) {
+  return (size_t)(2 * P.R + 1) * (size_t)n_colour_max *
+         (size_t)P.rules.nq_tri_in;
+}
+
+cudaError_t mf_launch_tet(const AsmParams &P, double *gscr, cudaStream_t s) {
   const int no = P.rules.nq_tri_out, ni = P.rules.nq_tri_in;
 #define MF_T(NO_, NI_) \
-  if (no == NO_ && ni == NI_) return launch<NO_, NI_>(P, s);
+  if (no == NO_ && ni == NI_) return launch<NO_, NI_>(P, gscr, s);
   MF_T(1, 1) MF_T(4, 1) MF_T(11, 1)
   MF_T(1, 4) MF_T(4, 4) MF_T(11, 4)
   MF_T(1, 11) MF_T(4, 11) MF_T(11, 11)
