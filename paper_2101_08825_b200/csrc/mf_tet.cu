@@ -31,6 +31,13 @@ namespace {
 
 constexpr int kTetLevels = 6;
 
+// per-thread pair state kept in shared memory, lane-major (stride = block
+// size, conflict-free): outer root vertices, the outer inverse map and the
+// inner box -- read rarely, so they need not occupy registers
+constexpr int kTetThreads = 128;
+enum : int { ST_ROOT = 0, ST_V0 = 12, ST_INV = 15, ST_ILO = 24, ST_IHI = 27,
+             ST_N = 30 };
+
 // cube corners (bit k = axis k) of Kuhn tet p (mesh.py kuhn_corners)
 __constant__ int8_t c_tet_corner[6][4] = {{0, 1, 3, 7}, {0, 5, 1, 7},
                                           {0, 3, 2, 7}, {0, 2, 6, 7},
@@ -76,10 +83,10 @@ MF_DEV void tet_child(const double *g, int b, double *c) {
 }
 
 // node with path `code` (3 bits per level below the root), recomputed from
-// the root with exact midpoints
-MF_DEV void tet_path(const double *root, uint32_t code, int L, double *g) {
+// the root (shared-memory state st) with exact midpoints
+MF_DEV void tet_path(const double *st, uint32_t code, int L, double *g) {
 #pragma unroll
-  for (int u = 0; u < 12; u++) g[u] = root[u];
+  for (int u = 0; u < 12; u++) g[u] = st[(ST_ROOT + u) * kTetThreads];
   for (int l = 2; l <= L; l++) {
     double c[12];
     tet_child(g, (code >> (3 * (l - 2))) & 7, c);
@@ -103,7 +110,9 @@ MF_DEV double tet_edges(const double *g, double (*e)[3]) {
 }
 
 struct OuterTet {
-  double v0[3], inv[9];
+  const double *p;  // &s_state[0][threadIdx.x]
+  MF_DEV double v0(int k) const { return p[(ST_V0 + k) * kTetThreads]; }
+  MF_DEV double inv(int k) const { return p[(ST_INV + k) * kTetThreads]; }
 };
 
 // full event on sub-tet g (oracle event_tet)
@@ -124,10 +133,11 @@ MF_DEV void tet_full(const AsmParams &P, const double *g, const OuterTet &O,
       x[k] = xadd(xadd(xadd(g[k], xmul(p0, e[0][k])), xmul(p1, e[1][k])),
                   xmul(p2, e[2][k]));
     const double w2 = s_w[q2] * f;
-    const double d0 = x[0] - O.v0[0], d1 = x[1] - O.v0[1], d2 = x[2] - O.v0[2];
-    const double rx = O.inv[0] * d0 + O.inv[1] * d1 + O.inv[2] * d2;
-    const double ry = O.inv[3] * d0 + O.inv[4] * d1 + O.inv[5] * d2;
-    const double rz = O.inv[6] * d0 + O.inv[7] * d1 + O.inv[8] * d2;
+    const double d0 = x[0] - O.v0(0), d1 = x[1] - O.v0(1),
+                 d2 = x[2] - O.v0(2);
+    const double rx = O.inv(0) * d0 + O.inv(1) * d1 + O.inv(2) * d2;
+    const double ry = O.inv(3) * d0 + O.inv(4) * d1 + O.inv(5) * d2;
+    const double rz = O.inv(6) * d0 + O.inv(7) * d1 + O.inv(8) * d2;
     const double s1 = rx * w2, s2 = ry * w2, s3 = rz * w2;
     const double s0 = w2 - s1 - s2 - s3;
     double mu[NQ1];
@@ -181,11 +191,11 @@ MF_DEV void tet_plateau(const AsmParams &P, const double *g,
     double d[3];
 #pragma unroll
     for (int k = 0; k < 3; k++)
-      d[k] = g[k] + p0 * e[0][k] + p1 * e[1][k] + p2 * e[2][k] - O.v0[k];
+      d[k] = g[k] + p0 * e[0][k] + p1 * e[1][k] + p2 * e[2][k] - O.v0(k);
     const double w2 = s_w[q2] * f;
-    const double rx = O.inv[0] * d[0] + O.inv[1] * d[1] + O.inv[2] * d[2];
-    const double ry = O.inv[3] * d[0] + O.inv[4] * d[1] + O.inv[5] * d[2];
-    const double rz = O.inv[6] * d[0] + O.inv[7] * d[1] + O.inv[8] * d[2];
+    const double rx = O.inv(0) * d[0] + O.inv(1) * d[1] + O.inv(2) * d[2];
+    const double ry = O.inv(3) * d[0] + O.inv(4) * d[1] + O.inv(5) * d[2];
+    const double rz = O.inv(6) * d[0] + O.inv(7) * d[1] + O.inv(8) * d[2];
     SP[0] += w2 * (1.0 - rx - ry - rz);
     SP[1] += w2 * rx;
     SP[2] += w2 * ry;
@@ -205,14 +215,20 @@ enum : int { ACT_NONE = 0, ACT_SPLIT = 1, ACT_UPPER = 2, ACT_PLAT = 3,
 // partial in gscr[plane][element]; k_tet_a22 sums the planes in order and
 // folds A22.  Warps are independent (no block barrier after the start), so
 // the short planes at |dz| ~ R do not idle behind the long central ones.
-constexpr int kTetWarps = 4;
+constexpr int kTetWarps = kTetThreads / 32;
+#ifndef MF_TET_MINB
+#define MF_TET_MINB 2
+#endif
 
 template <int NQO, int NQ1>
-__global__ void __launch_bounds__(32 * kTetWarps, 2)
+__global__ void __launch_bounds__(32 * kTetWarps, MF_TET_MINB)
     k_tet(AsmParams P, int pass, double *gscr) {
   __shared__ double s_phiw[NQ1][4];
   __shared__ double s_opts[3 * NQO], s_ow[NQO];
   __shared__ double s_y[kTetWarps][NQ1][3][32];  // inner points, lane-major
+  extern __shared__ double s_dyn[];  // s_state[ST_N][kTetThreads]
+  double(*s_state)[kTetThreads] =
+      reinterpret_cast<double(*)[kTetThreads]>(s_dyn);
   const MfMesh &M = P.mesh;
   const MfRules &Rr = P.rules;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -252,11 +268,11 @@ __global__ void __launch_bounds__(32 * kTetWarps, 2)
   const int pidx = pass + 2 * (int)blockIdx.y;  // plane index dz + R
   const int dz = pidx - Rs;
   if (!valid) return;
-  double ilo[3], ihi[3];
+  double *st = &s_state[0][threadIdx.x];
 #pragma unroll
   for (int k = 0; k < 3; k++) {
-    ilo[k] = M.elem_lo[m * 3 + k];
-    ihi[k] = M.elem_hi[m * 3 + k];
+    st[(ST_ILO + k) * kTetThreads] = M.elem_lo[m * 3 + k];
+    st[(ST_IHI + k) * kTetThreads] = M.elem_hi[m * 3 + k];
   }
   double G[NQ1];
 #pragma unroll
@@ -298,25 +314,31 @@ __global__ void __launch_bounds__(32 * kTetWarps, 2)
           if (!(elem_gap<3>(M.elem_lo, M.elem_hi, l, m) < P.dpe)) continue;
           c_pairs++;
           const int tout = (int)(l % 6);
-          OuterTet O;
-          double root[12];
+          const OuterTet O{st};
+          double g[12];
           {
             const double *c = M.elem_coords + l * M.nv_max * 3;
 #pragma unroll
-            for (int u = 0; u < 12; u++) root[u] = c[u];
+            for (int u = 0; u < 12; u++) {
+              g[u] = c[u];
+              st[(ST_ROOT + u) * kTetThreads] = g[u];
+            }
             double e[3][3];
-            const double det = tet_edges(root, e);
+            const double det = tet_edges(g, e);
             const double idet = rcp_fast(det);
             // rows (e2 x e3), (e3 x e1), (e1 x e2) over det (oracle tet_inv)
 #pragma unroll
             for (int r = 0; r < 3; r++) {
               const double *u = e[(r + 1) % 3], *v = e[(r + 2) % 3];
-              O.inv[3 * r + 0] = (u[1] * v[2] - u[2] * v[1]) * idet;
-              O.inv[3 * r + 1] = (u[2] * v[0] - u[0] * v[2]) * idet;
-              O.inv[3 * r + 2] = (u[0] * v[1] - u[1] * v[0]) * idet;
+              st[(ST_INV + 3 * r + 0) * kTetThreads] =
+                  (u[1] * v[2] - u[2] * v[1]) * idet;
+              st[(ST_INV + 3 * r + 1) * kTetThreads] =
+                  (u[2] * v[0] - u[0] * v[2]) * idet;
+              st[(ST_INV + 3 * r + 2) * kTetThreads] =
+                  (u[0] * v[1] - u[1] * v[0]) * idet;
             }
 #pragma unroll
-            for (int k = 0; k < 3; k++) O.v0[k] = root[k];
+            for (int k = 0; k < 3; k++) st[(ST_V0 + k) * kTetThreads] = g[k];
           }
           double V[NQ1][4];
 #pragma unroll
@@ -329,12 +351,14 @@ __global__ void __launch_bounds__(32 * kTetWarps, 2)
           // below the root); the node is recomputed from the root
           uint32_t code = 0;
           int L = 1;
-          double g[12];
-#pragma unroll
-          for (int u = 0; u < 12; u++) g[u] = root[u];
           for (;;) {
-            double slo[3], shi[3];
+            double slo[3], shi[3], ilo[3], ihi[3];
             tet_bbox(g, slo, shi);
+#pragma unroll
+            for (int k = 0; k < 3; k++) {
+              ilo[k] = st[(ST_ILO + k) * kTetThreads];
+              ihi[k] = st[(ST_IHI + k) * kTetThreads];
+            }
             int act = ACT_NONE;
             if (L < P.L_min) {
               act = ACT_SPLIT;
@@ -388,7 +412,7 @@ __global__ void __launch_bounds__(32 * kTetWarps, 2)
             }
             if (L == 1) break;
             code += 1u << (3 * (L - 2));
-            tet_path(root, code, L, g);
+            tet_path(st, code, L, g);
           }
           if (ev) {
             c_ev += ev;
@@ -484,11 +508,15 @@ template <int NQO, int NQ1>
 cudaError_t launch(const AsmParams &P, double *gscr, cudaStream_t s) {
   const unsigned gx = (unsigned)((P.n_inner + 32 * kTetWarps - 1) /
                                  (32 * kTetWarps));
+  const size_t dyn = sizeof(double) * ST_N * kTetThreads;
+  cudaError_t ea = cudaFuncSetAttribute(
+      k_tet<NQO, NQ1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+  if (ea != cudaSuccess) return ea;
   for (int pass = 0; pass < 2; pass++) {
     const int planes = pass == 0 ? P.R + 1 : P.R;
     if (planes < 1) continue;
-    k_tet<NQO, NQ1><<<dim3(gx, planes), 32 * kTetWarps, 0, s>>>(P, pass,
-                                                                 gscr);
+    k_tet<NQO, NQ1><<<dim3(gx, planes), kTetThreads, dyn, s>>>(P, pass,
+                                                                gscr);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
