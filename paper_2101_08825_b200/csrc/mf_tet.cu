@@ -36,7 +36,7 @@ constexpr int kTetLevels = 6;
 // inner box -- read rarely, so they need not occupy registers
 constexpr int kTetThreads = 128;
 enum : int { ST_ROOT = 0, ST_V0 = 12, ST_INV = 15, ST_ILO = 24, ST_IHI = 27,
-             ST_N = 30 };
+             ST_PILO = 30, ST_PIHI = 33, ST_N = 36 };
 
 // cube corners (bit k = axis k) of Kuhn tet p (mesh.py kuhn_corners)
 __constant__ int8_t c_tet_corner[6][4] = {{0, 1, 3, 7}, {0, 5, 1, 7},
@@ -241,6 +241,18 @@ __global__ void __launch_bounds__(32 * kTetWarps, MF_TET_MINB)
     for (int k = 0; k < 3; k++) s_opts[3 * i + k] = Rr.tri_out_pts[3 * i + k];
     s_ow[i] = Rr.tri_out_w[i];
   }
+  // outer rule points lie in the sub-tet shrunk about its centroid by
+  // f = 1 - 4 min(barycentric) (their convex hull); + a relative margin
+  __shared__ double s_fo;
+  if (threadIdx.x == 0) {
+    double lmin = 1.0;
+    for (int q = 0; q < NQO; q++) {
+      const double a = Rr.tri_out_pts[3 * q], b = Rr.tri_out_pts[3 * q + 1],
+                   c = Rr.tri_out_pts[3 * q + 2];
+      lmin = fmin(lmin, fmin(fmin(a, b), fmin(c, 1.0 - a - b - c)));
+    }
+    s_fo = fmin(1.0, 1.0 - 4.0 * lmin + 1e-9);
+  }
   const int64_t t = ((int64_t)blockIdx.x * kTetWarps + w) * 32 + lane;
   const bool valid = t < P.n_inner;
   const int64_t m = valid ? P.inner[t] : P.inner[0];
@@ -271,9 +283,19 @@ __global__ void __launch_bounds__(32 * kTetWarps, MF_TET_MINB)
   double *st = &s_state[0][threadIdx.x];
 #pragma unroll
   for (int k = 0; k < 3; k++) {
-    st[(ST_ILO + k) * kTetThreads] = M.elem_lo[m * 3 + k];
-    st[(ST_IHI + k) * kTetThreads] = M.elem_hi[m * 3 + k];
+    const double lo = M.elem_lo[m * 3 + k], hi = M.elem_hi[m * 3 + k];
+    st[(ST_ILO + k) * kTetThreads] = lo;
+    st[(ST_IHI + k) * kTetThreads] = hi;
+    // box of the inner rule points, widened by 1e-9 of the element
+    double pmn = 1e300, pmx = -1e300;
+    for (int q = 0; q < NQ1; q++) {
+      pmn = fmin(pmn, s_y[w][q][k][lane]);
+      pmx = fmax(pmx, s_y[w][q][k][lane]);
+    }
+    st[(ST_PILO + k) * kTetThreads] = pmn - 1e-9 * (hi - lo);
+    st[(ST_PIHI + k) * kTetThreads] = pmx + 1e-9 * (hi - lo);
   }
+  const double fo = s_fo;
   double G[NQ1];
 #pragma unroll
   for (int q = 0; q < NQ1; q++) G[q] = 0.0;
@@ -364,15 +386,31 @@ __global__ void __launch_bounds__(32 * kTetWarps, MF_TET_MINB)
               act = ACT_SPLIT;
             } else if (L == P.L_max) {
               if (aprx_min_d<3>(slo, shi, ilo, ihi) < P.dpe) {
-                if (!P.shortcuts)
+                if (!P.shortcuts) {
                   act = ACT_FULL;
-                else if (box_dead<3>(P, slo, shi, ilo, ihi))
-                  act = ACT_DEAD;
-                else if (aprx_max_lt_dme(P, aprx_max_sq<3>(slo, shi, ilo,
-                                                           ihi)))
-                  act = ACT_PLAT;
-                else
-                  act = ACT_FULL;
+                } else {
+                  // dead / plateau proofs on the point-set boxes (see
+                  // mf_hex.cu classify): every point pair certainly beyond
+                  // delta+eps, or certainly inside delta-eps
+                  double qlo[3], qhi[3], plo[3], phi[3];
+#pragma unroll
+                  for (int k = 0; k < 3; k++) {
+                    const double c =
+                        0.25 * ((g[k] + g[3 + k]) + (g[6 + k] + g[9 + k]));
+                    const double mg = 1e-9 * (shi[k] - slo[k]);
+                    qlo[k] = c + fo * (slo[k] - c) - mg;
+                    qhi[k] = c + fo * (shi[k] - c) + mg;
+                    plo[k] = st[(ST_PILO + k) * kTetThreads];
+                    phi[k] = st[(ST_PIHI + k) * kTetThreads];
+                  }
+                  if (box_dead<3>(P, qlo, qhi, plo, phi))
+                    act = ACT_DEAD;
+                  else if (aprx_max_sq<3>(qlo, qhi, plo, phi) <
+                           P.dm2 * (1.0 - 4e-9))
+                    act = ACT_PLAT;
+                  else
+                    act = ACT_FULL;
+                }
               }
             } else if (aprx_max_lt_dme(P,
                                        aprx_max_sq<3>(slo, shi, ilo, ihi))) {
