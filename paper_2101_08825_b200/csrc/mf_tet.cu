@@ -333,18 +333,43 @@ __global__ void __launch_bounds__(32 * kTetWarps, MF_TET_MINB)
         const int64_t c2 = ((int64_t)z2 * M.ncy + y2) * M.ncx + x2;
         for (int64_t l = M.cell_ptr[c2]; l < M.cell_ptr[c2 + 1]; l++) {
           if (!P.outer_mask[l]) continue;
-          if (!(elem_gap<3>(M.elem_lo, M.elem_hi, l, m) < P.dpe)) continue;
+          // candidate test (_kernels.py:1225-1233) on the box of l's
+          // vertices: elem_lo/hi are exactly their min/max, so this is the
+          // same test without two extra gathers
+          // (tet11 keeps the elem_lo/hi gathers: its register budget is
+          // spent on V[11][4], and the extra live coordinates spill)
+          if constexpr (NQ1 > 4) {
+            if (!(elem_gap<3>(M.elem_lo, M.elem_hi, l, m) < P.dpe)) continue;
+          }
+          double g[12];
+          {
+            const double2 *c2v =
+                reinterpret_cast<const double2 *>(M.elem_coords + l * 12);
+#pragma unroll
+            for (int u = 0; u < 6; u++) {
+              const double2 v = c2v[u];
+              g[2 * u] = v.x;
+              g[2 * u + 1] = v.y;
+            }
+          }
+          if constexpr (NQ1 <= 4) {
+            double lo[3], hi[3], gap = 0.0;
+            tet_bbox(g, lo, hi);
+#pragma unroll
+            for (int k = 0; k < 3; k++) {
+              const double d1 = xsub(lo[k], st[(ST_IHI + k) * kTetThreads]);
+              const double d2 = xsub(st[(ST_ILO + k) * kTetThreads], hi[k]);
+              if (d1 > gap) gap = d1;
+              if (d2 > gap) gap = d2;
+            }
+            if (!(gap < P.dpe)) continue;
+          }
           c_pairs++;
           const int tout = (int)(l % 6);
           const OuterTet O{st};
-          double g[12];
           {
-            const double *c = M.elem_coords + l * M.nv_max * 3;
 #pragma unroll
-            for (int u = 0; u < 12; u++) {
-              g[u] = c[u];
-              st[(ST_ROOT + u) * kTetThreads] = g[u];
-            }
+            for (int u = 0; u < 12; u++) st[(ST_ROOT + u) * kTetThreads] = g[u];
             double e[3][3];
             const double det = tet_edges(g, e);
             const double idet = rcp_fast(det);
