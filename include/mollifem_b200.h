@@ -57,10 +57,12 @@ typedef struct MfRules {
   int32_t nq_box_out, nq_box_in, nq_tri_out, nq_tri_in;
   const double *box_out_pts, *box_out_w;  /* (nq, dim), (nq) */
   const double *box_in_pts, *box_in_w;
-  const double *tri_out_pts, *tri_out_w;  /* (nq, 2), (nq) */
+  /* simplex slots: triangles (nq, 2) in 2D; in 3D the tetrahedron rule
+   * (nq, 3) of the P1 tet element (new; mesh kind 3, kinds_present bit 8) */
+  const double *tri_out_pts, *tri_out_w;  /* (nq, dim), (nq) */
   const double *tri_in_pts, *tri_in_w;
   const double *phi_box_in;               /* (nq_box_in, nl_box) */
-  const double *phi_tri_in;               /* (nq_tri_in, nl_tri) */
+  const double *phi_tri_in;               /* (nq_tri_in, nl_tri); nl = 4 for tets */
   int32_t n1d_box_out, n1d_box_in;
   const double *box_out_x1d, *box_out_w1d;/* (n1d) */
   const double *box_in_x1d, *box_in_w1d;
