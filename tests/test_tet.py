@@ -283,3 +283,30 @@ def test_tet_gpu_rhs_and_solve():
     ref = spla.spsolve(Aff.tocsc(), want)
     assert np.abs(u[space.free] - ref).max() <= 1e-8 * max(
         1.0, np.abs(ref).max())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["tet4_l3_jit", "tet11_l2_jit"])
+def test_tet_gpu_partitions_and_slabs(name):
+    """Partition invariance (parallel_assemble, RCB + ghost regions) and the
+    z-slab decomposition of the multi-GPU path, emulated on one device."""
+    from paper_2101_08825_b200.parallel import emulate_slabs, parallel_assemble
+    mesh, space, kp, cfg = build(name)
+    R = oracle_matrix(name)
+    for n_parts in (2, 3):
+        A, ctxs = parallel_assemble(mesh, space, kp, cfg, n_parts=n_parts)
+        assert A.events == R.events
+        assert rel_frob(A.vals, R.vals) <= 1e-12
+    for world in (2, 3):
+        full, events = emulate_slabs(mesh, space, kp, cfg, world)
+        assert events == R.events
+        assert rel_frob(full.cpu().numpy(), R.vals) <= 1e-12
+
+
+@pytest.mark.gpu
+def test_tet_gpu_deterministic():
+    from paper_2101_08825_b200 import assemble
+    mesh, space, kp, cfg = build("tet4_l3_jit")
+    a = assemble(mesh, space, kp, cfg).vals
+    b = assemble(mesh, space, kp, cfg).vals
+    assert np.array_equal(a, b)
