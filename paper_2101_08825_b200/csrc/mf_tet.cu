@@ -394,6 +394,7 @@ __global__ void __launch_bounds__(32 * kTetWarps, MF_TET_MINB)
             for (int j = 0; j < 4; j++) V[q][j] = 0.0;
           double SP[4] = {0.0, 0.0, 0.0, 0.0};
           unsigned ev = 0;
+          bool live = false;  // some plateau/full event: nonzero block
           // Algorithm 1, depth first over a path code (3 bits per level
           // below the root); the node is recomputed from the root
           uint32_t code = 0;
@@ -453,6 +454,7 @@ __global__ void __launch_bounds__(32 * kTetWarps, MF_TET_MINB)
                   act == ACT_PLAT || (act == ACT_UPPER && P.shortcuts);
               const bool full =
                   act == ACT_FULL || (act == ACT_UPPER && !P.shortcuts);
+              live |= plateau || full;
               if (plateau)
                 tet_plateau<NQO>(P, g, O, s_opts, s_ow, SP);
               else if (full && P.eps > 0.0)
@@ -477,8 +479,10 @@ __global__ void __launch_bounds__(32 * kTetWarps, MF_TET_MINB)
             code += 1u << (3 * (L - 2));
             tet_path(st, code, L, g);
           }
-          if (ev) {
-            c_ev += ev;
+          c_ev += ev;
+          // dead-only pairs have an exactly zero block: adding it would
+          // change no value, so the 16 read-modify-writes are skipped
+          if (live) {
             double spsum = (SP[0] + SP[1]) + (SP[2] + SP[3]);
             const double sc = -P.scale * scale_in;
 #pragma unroll
