@@ -457,6 +457,7 @@ __global__ void __launch_bounds__(128, MF_2D_MINB) k_2d(AsmParams P) {
 #pragma unroll
         for (int j = 0; j < NL; j++) SP[j] = 0.0;
         unsigned long long ev = 0;
+        bool live = false;  // some plateau/full event: nonzero block
         double geo[kMaxLevels + 1][6];
         int child[kMaxLevels + 1];
 #pragma unroll
@@ -494,6 +495,7 @@ __global__ void __launch_bounds__(128, MF_2D_MINB) k_2d(AsmParams P) {
                 act == ACT_PLAT || (act == ACT_UPPER && P.shortcuts);
             const bool full = act == ACT_FULL || (act == ACT_UPPER &&
                                                   !P.shortcuts);
+            live |= plateau || full;
             if constexpr (KIND == 1) {
               if (plateau)
                 tri_plateau(P, geo[L], OT, s_opts, s_ow, SP);
@@ -534,8 +536,9 @@ __global__ void __launch_bounds__(128, MF_2D_MINB) k_2d(AsmParams P) {
           }
           if (done) break;
         }
-        if (ev) {
-          c_ev += ev;
+        c_ev += ev;
+        // dead-only pairs add an exactly zero block: skipped
+        if (live) {
           // plateau part is common to every q1
           double spsum = 0.0;
 #pragma unroll

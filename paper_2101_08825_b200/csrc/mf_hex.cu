@@ -476,6 +476,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MF_HEX_MINB)
 #pragma unroll
       for (int j = 0; j < 8; j++) V[j] = 0.0;
       unsigned ev = 0;
+      bool live = false;  // warp-uniform: some plateau/full event
       {
         Box root;
 #pragma unroll
@@ -487,10 +488,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MF_HEX_MINB)
                                  tmin, tmax);
         if (act == ACT_UPPER || act == ACT_PLAT) {
           ev++;
+          live = true;
           (act == ACT_UPPER ? c_up : c_pl)++;
           event_plateau<NO>(P, s_rt, s_rw, C, 32, lane, V);
         } else if (act == ACT_FULL || act == ACT_UPPER_FULL) {
           ev++;
+          live = true;
           (act == ACT_FULL ? c_full : c_up)++;
           run_full<NO>(P, s_rt, s_rw, C, 32, y, lane, active, V);
         } else if (act == ACT_DEAD) {
@@ -541,6 +544,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MF_HEX_MINB)
               const unsigned mup = __ballot_sync(
                   0xffffffffu, a == ACT_UPPER || a == ACT_UPPER_FULL);
               ev += __popc(mplat) + __popc(mfull) + __popc(mdead);
+              live |= (mplat | mfull) != 0u;
               c_dead += __popc(mdead);
               c_up += __popc(mup);
               c_pl += __popc(mplat & ~mup);
@@ -564,8 +568,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MF_HEX_MINB)
           }
         }
       }
-      if (ev) {
-        c_ev += ev;
+      c_ev += ev;
+      // dead-only pairs have an exactly zero block: skip its contraction
+      // and read-modify-write (adding zeros changes no value)
+      if (live) {
         // b21[i][j] = -jac_in * sum_q1 phiw[q1][i] V[q1][j]
         if (active) {
 #pragma unroll
