@@ -74,9 +74,17 @@ CONFIGS = {
                   2, "tet11"),
     "R5-tet-small": (3, ((0.0, 0.25),) * 3, 1 / 64, 4 / 64, 1 / 256, 2.0,
                      "tet", 2, "tet11"),
+    # BASELINE config #2: unstructured Delaunay P1 mesh of ~200k seeded
+    # jittered points (400^2 Omega lattice + 21 Gamma rings = 442^2 =
+    # 195,364 vertices), delta = 0.05, eps = h/2, 6-point rule, L_max 3
+    "R2": (2, ((0.0, 1.0),) * 2, 1 / 400, 0.05, 1 / 800, 1.0, "delaunay",
+           3, "tri6"),
+    "R2-small": (2, ((0.0, 0.25),) * 2, 1 / 400, 0.05, 1 / 800, 1.0,
+                 "delaunay", 3, "tri6"),
 }
 # vertex jitter (fraction of h, seeded) per workload (tet meshes only)
-JITTER = {"R5-tet-64": 0.1, "R5-tet-small": 0.1}
+JITTER = {"R5-tet-64": 0.1, "R5-tet-small": 0.1, "R2": 0.3,
+          "R2-small": 0.3}
 
 METRIC = "interacting element-pairs/sec (full nonlocal stiffness assembly)"
 
@@ -92,8 +100,13 @@ def build_problem(name):
                                        build_mesh)
     dim, om, h, delta, eps, kappa, kind, lmax, rule = CONFIGS[name]
     kp = KernelParams(dim, delta, eps, kappa)
-    mesh = build_mesh(dim, om, h, delta + eps, kind,
-                      jitter=JITTER.get(name, 0.0), seed=0)
+    if kind == "delaunay":
+        from paper_2101_08825_b200.mesh import build_delaunay_mesh
+        mesh = build_delaunay_mesh(om, h, delta + eps, jitter=JITTER[name],
+                                   seed=0)
+    else:
+        mesh = build_mesh(dim, om, h, delta + eps, kind,
+                          jitter=JITTER.get(name, 0.0), seed=0)
     space = FESpace(mesh, 1)
     cfg = AssemblyConfig(L_max=lmax, outer_rule=rule, inner_rule=rule,
                          strategy="general")
@@ -104,6 +117,10 @@ def config_json(name, mesh, space, n_gpus, slab_info=None,
                 strategy="general"):
     dim, om, h, delta, eps, kappa, kind, lmax, rule = CONFIGS[name]
     mdesc = f"{kind} structured"
+    if kind == "delaunay":
+        mdesc = (f"unstructured Delaunay P1 triangles of "
+                 f"{len(mesh.nodes)} seeded lattice points jittered "
+                 f"+-{JITTER[name]}h (seed 0)")
     if kind == "tet":
         mdesc = "6-tet (Kuhn) cubes" + (
             f", vertices jittered +-{JITTER[name]}h (seed 0)"
@@ -112,7 +129,8 @@ def config_json(name, mesh, space, n_gpus, slab_info=None,
          "cells": list(mesh.grid_ncells), "elements": mesh.n_elements,
          "n_dofs": space.n_dofs, "fe_degree": 1, "h": h, "delta": delta,
          "eps": eps, "kappa": kappa, "L_max": lmax,
-         "rule": "dunavant7" if kind == "tri" else rule,
+         "rule": {"tri": "dunavant7", "delaunay": "dunavant6"}.get(kind,
+                                                                   rule),
          "parallelism": f"z-slab x{n_gpus}" if n_gpus > 1 else "single",
          "l2": "value array > L2 (rewritten every step)"}
     if slab_info:
@@ -225,7 +243,7 @@ def flop_model(name, counters):
         f_plat = 3 * no * 8 + 6 * no + 16
         f_pair = 2 * 2 * nq1 * 64 + 8 * nq1
     else:
-        nq1 = nq2 = 7
+        nq1 = nq2 = 6 if rule == "tri6" else 7
         nl = 3
         canon_ev = nq2 * nq1 * (3 * dim - 1 + 3) + 2 * nq2 * nq1 * nl \
             + 2 * nq2 * nl * nl
@@ -368,7 +386,8 @@ def run_ours(args):
         A = ctx.new_matrix()
         plan = ctx.default_plan()
         counters = torch.zeros(N.MF_NCOUNTERS, dtype=torch.int64, device=dev)
-        n_launch = np.count_nonzero(np.diff(plan.color_ptr)) + 1
+        n_launch = (np.count_nonzero(np.diff(plan.color_ptr))
+                    * launches_per_group(mesh)) + 1
         if args.strategy == "blocked":
             n_launch = 2 + np.count_nonzero(np.diff(plan.color_ptr))
 
@@ -394,7 +413,8 @@ def run_ours(args):
                 "interface_plane_bytes": int(
                     (sa.plan.send_range[1] - sa.plan.send_range[0]) * 8
                     if sa.plan.send_range else 0)}
-        n_launch = np.count_nonzero(np.diff(plan.color_ptr))
+        n_launch = (np.count_nonzero(np.diff(plan.color_ptr))
+                    * launches_per_group(mesh))
 
         def work():
             sa.assemble_local()
@@ -523,7 +543,10 @@ def run_ours(args):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_all, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (structured mesh, reference-realisable stand-in)",
+        "data": ("synthetic (seeded jittered-lattice Delaunay mesh)"
+                 if CONFIGS[name][6] == "delaunay" else
+                 "synthetic (structured mesh, reference-realisable "
+                 "stand-in)"),
         "kernel_ms_per_step": statistics.mean(kern_ms),
         "config": config_json(name, mesh, space, world, slab,
                               args.strategy),
@@ -545,6 +568,18 @@ def run_ours(args):
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def launches_per_group(mesh):
+    """Kernel launches per non-empty colour group of mf_general_core:
+    tets run two parity launches + the A22 fold (mf_tet.cu), Delaunay
+    triangles row_period row-class launches + the fold (k_tri_u), the
+    other kernels one launch."""
+    if mesh.kind == "tet":
+        return 3
+    if getattr(mesh, "unstructured", False):
+        return int(mesh.row_period) + 1
+    return 1
 
 
 def ctx_nnz(mesh, space, kp, cfg):

@@ -30,7 +30,7 @@ extern "C" {
 #define MF_ERR_CUDA 2
 #define MF_ERR_UNSUPPORTED 3
 
-#define MF_ABI_VERSION 1
+#define MF_ABI_VERSION 2
 
 /* Mesh SoA + DOF map (mesh.py:78-88 flat arrays; fe_space.py:131-157). */
 typedef struct MfMesh {
@@ -48,6 +48,15 @@ typedef struct MfMesh {
   const int64_t *cell_ptr;  /* (ncells+1) elements per cell, cell-lex order */
   int32_t ncx, ncy, ncz;    /* cell grid (ncz = 1 in 2D) */
   int32_t kinds_present;    /* bit k set if some element has kind k */
+  /* 0: the reference's structured layout (elements in cell-lex order,
+   *    DOFs from cell + proto offsets).
+   * 1: unstructured P1 triangles (new, BASELINE config #2): elements in
+   *    the bin of their box lower corner, any shape; elem_dofs are lattice
+   *    ids on the pattern grid.  Outer elements binned row_period rows
+   *    apart share no vertex (the kernel splits the stencil rows into
+   *    row_period race-free classes). */
+  int32_t layout;
+  int32_t row_period;
 } MfMesh;
 
 /* Reference-element rules and inner shape tables (assembly.py:333-356).

@@ -15,20 +15,23 @@ from .fe_space import (FESpace, eval_basis, eval_shape_functions,
                        interpolate, l2_error, lifting)
 from .kernel import (KernelParams, gamma_eps, mollifier, scaling_c_delta,
                      scaling_c_delta_eps, xi)
-from .mesh import (BoundingBox, Mesh, PartitionMap, build_mesh,
-                   partition_geometric, refine)
+from .mesh import (BoundingBox, DelaunayMesh, Mesh, PartitionMap,
+                   build_delaunay_mesh, build_mesh, partition_geometric,
+                   refine)
 from .solver import SolveReport, solve
-from .quadrature import (QuadratureRule, dunavant7, gauss_legendre_1d,
+from .quadrature import (QuadratureRule, dunavant6, dunavant7,
+                         gauss_legendre_1d,
                          gauss_lobatto_1d, map_to_physical, rule_for_kind,
                          tensor_product)
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "AssemblyConfig", "BoundingBox", "FESpace", "KernelParams", "Mesh",
+    "AssemblyConfig", "BoundingBox", "DelaunayMesh", "FESpace",
+    "KernelParams", "Mesh",
     "NeighborSets", "PartitionMap", "QuadratureRule", "SparseMatrix",
     "aprx_max_dist", "aprx_min_dist", "assemble", "assemble_rhs",
-    "build_mesh", "dunavant7",
+    "build_delaunay_mesh", "build_mesh", "dunavant6", "dunavant7",
     "eval_basis", "eval_shape_functions", "gamma_eps", "gauss_legendre_1d",
     "gauss_lobatto_1d", "interpolate", "l2_error", "lifting",
     "map_to_physical", "mollifier", "neighbor_sets", "partition_geometric",

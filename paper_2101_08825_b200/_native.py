@@ -27,7 +27,8 @@ class MfMesh(C.Structure):
                 ("elem_hi", C.c_void_p), ("elem_dofs", C.c_void_p),
                 ("elem_cell", C.c_void_p), ("cell_ptr", C.c_void_p),
                 ("ncx", C.c_int32), ("ncy", C.c_int32), ("ncz", C.c_int32),
-                ("kinds_present", C.c_int32)]
+                ("kinds_present", C.c_int32), ("layout", C.c_int32),
+                ("row_period", C.c_int32)]
 
 
 class MfRules(C.Structure):

@@ -104,7 +104,10 @@ def pattern_halfwidth(mesh, params, config, degree):
         f = 2.0 / 3.0 if mesh.kind in ("tri", "mixed") else 0.5
         oe = int(math.floor(params.delta / mesh.h + f + 1e-12))
     else:
-        oe = int(math.floor((params.delta + params.eps + stencil_pad(mesh))
+        # unstructured meshes: coupled vertices may sit further apart in
+        # lattice index than their elements' bins (mesh.DelaunayMesh)
+        pad = float(getattr(mesh, "pattern_pad", stencil_pad(mesh)))
+        oe = int(math.floor((params.delta + params.eps + pad)
                             / mesh.h + 1e-12)) + 1
     return degree * (oe + 1), oe
 
@@ -125,7 +128,10 @@ class PrepTables:
         # simplex slots ("tri_*"): triangles in 2D, tetrahedra in 3D (the
         # tet element is new; its rules are "default" = tet4, tet1/4/11)
         simplex = "tet" if mesh.kind == "tet" else "tri"
-        if simplex == "tet":
+        tri_preset = outer in ("tri6", "tri7") or inner in ("tri6", "tri7")
+        if tri_preset and mesh.kind != "tri":
+            raise ValueError("tri6/tri7 presets need a pure triangle mesh")
+        if simplex == "tet" or tri_preset:
             box_outer = box_inner = "gauss2"   # unused placeholders
         else:
             box_outer, box_inner = outer, inner
@@ -797,13 +803,17 @@ _TRI_PROTOS = np.array([[[0.0, 0.0], [1.0, 0.0], [1.0, 1.0]],
 def resolve_strategy(mesh, config):
     """assembly.py:448-453: "auto" -> blocked on pure quad/tri/hex meshes.
 
-    Tet meshes (new element) always run the general path: jittered meshes
-    have no translation-invariant offset blocks."""
-    if config.strategy == "blocked" and mesh.kind not in ("quad", "tri",
-                                                          "hex"):
-        raise ValueError("blocked strategy needs a pure quad/tri/hex mesh")
+    Tet and Delaunay meshes (new) always run the general path: their
+    elements have no translation-invariant offset blocks."""
+    unstructured = getattr(mesh, "unstructured", False)
+    if config.strategy == "blocked" and (
+            unstructured or mesh.kind not in ("quad", "tri", "hex")):
+        raise ValueError("blocked strategy needs a pure structured "
+                         "quad/tri/hex mesh")
     if config.strategy != "auto":
         return config.strategy
+    if unstructured:
+        return "general"
     return "blocked" if mesh.kind in ("quad", "tri", "hex") else "general"
 
 

@@ -125,7 +125,7 @@ struct OuterBox {
 };
 
 // ---- triangle events (Dunavant outer rule in shared memory) ----
-template <int NQ1, bool SHARP>
+template <int NQO, int NQ1, bool SHARP>
 MF_DEV void tri_full(const AsmParams &P, const double *g, const OuterTri &O,
                      const double (*y)[2], const double *s_pts,
                      const double *s_w, double (*V)[3]) {
@@ -134,7 +134,7 @@ MF_DEV void tri_full(const AsmParams &P, const double *g, const OuterTri &O,
   const double det = e10 * e21 - e11 * e20;
   const double f = det * P.cde * (1.0 / 256.0);
 #pragma unroll 1
-  for (int q2 = 0; q2 < 7; q2++) {
+  for (int q2 = 0; q2 < NQO; q2++) {
     const double px = s_pts[2 * q2], py = s_pts[2 * q2 + 1];
     const double x0 = xadd(xadd(g[0], xmul(px, e10)), xmul(py, e20));
     const double x1 = xadd(xadd(g[1], xmul(px, e11)), xmul(py, e21));
@@ -178,6 +178,7 @@ MF_DEV void tri_full(const AsmParams &P, const double *g, const OuterTri &O,
   }
 }
 
+template <int NQO>
 MF_DEV void tri_plateau(const AsmParams &P, const double *g,
                         const OuterTri &O, const double *s_pts,
                         const double *s_w, double *SP) {
@@ -186,7 +187,7 @@ MF_DEV void tri_plateau(const AsmParams &P, const double *g,
   const double det = e10 * e21 - e11 * e20;
   const double f = det * P.cde;
 #pragma unroll 1
-  for (int q2 = 0; q2 < 7; q2++) {
+  for (int q2 = 0; q2 < NQO; q2++) {
     const double px = s_pts[2 * q2], py = s_pts[2 * q2 + 1];
     const double x0 = g[0] + px * e10 + py * e20;
     const double x1 = g[1] + px * e11 + py * e21;
@@ -498,12 +499,12 @@ __global__ void __launch_bounds__(128, MF_2D_MINB) k_2d(AsmParams P) {
             live |= plateau || full;
             if constexpr (KIND == 1) {
               if (plateau)
-                tri_plateau(P, geo[L], OT, s_opts, s_ow, SP);
+                tri_plateau<7>(P, geo[L], OT, s_opts, s_ow, SP);
               else if (full && P.eps > 0.0)
-                tri_full<NQ1, false>(P, geo[L], OT, y, s_opts, s_ow,
+                tri_full<7, NQ1, false>(P, geo[L], OT, y, s_opts, s_ow,
                                      reinterpret_cast<double(*)[3]>(V));
               else if (full)
-                tri_full<NQ1, true>(P, geo[L], OT, y, s_opts, s_ow,
+                tri_full<7, NQ1, true>(P, geo[L], OT, y, s_opts, s_ow,
                                     reinterpret_cast<double(*)[3]>(V));
             } else {
               if (plateau)
@@ -590,6 +591,291 @@ __global__ void __launch_bounds__(128, MF_2D_MINB) k_2d(AsmParams P) {
   counter_add(C + MF_CNT_EV_FULL, c_full);
 }
 
+// ---- unstructured P1 triangles (mesh layout 1, BASELINE config #2) ----
+//
+// Delaunay triangles of any shape (mesh.py build_delaunay_mesh), binned by
+// the lattice cell of their box lower corner; elem_dofs are lattice ids on
+// the implicit pattern grid.  One thread = one INNER element m of the
+// current colour (a greedy vertex-disjoint colouring) x ONE stencil bin
+// row dy (blockIdx.y); a launch covers the rows of one class
+// (dy + R) mod row_period.  Outer elements binned row_period rows apart
+// share no vertex (emax <= (row_period - 1) h, checked by the mesh
+// builder), and same-colour inner elements share no vertex, so the A21
+// read-modify-writes of one launch never collide: no atomics, a fixed
+// launch order, deterministic.  The outer elements of a bin row are one
+// contiguous id range (bin-lex order).  Each thread leaves its G partial in
+// gscr[row][element]; k_tri_u_a22 sums the rows in order and folds A22.
+// Algorithm 1 and the events are those of k_2d<1> (the reference's
+// _event_tri is valid for arbitrary affine triangles, _kernels.py:146-181).
+template <int NQO, int NQ1>
+__global__ void __launch_bounds__(128, MF_2D_MINB)
+    k_tri_u(AsmParams P, int cls, double *gscr) {
+  constexpr int NL = 3;
+  __shared__ double s_phiw[NQ1][NL];
+  __shared__ double s_opts[2 * NQO], s_ow[NQO];
+  const MfMesh &M = P.mesh;
+  const MfRules &Rr = P.rules;
+  for (int i = threadIdx.x; i < NQ1 * NL; i += blockDim.x) {
+    const int q = i / NL, j = i % NL;
+    s_phiw[q][j] = Rr.tri_in_w[q] * Rr.phi_tri_in[q * NL + j];
+  }
+  for (int i = threadIdx.x; i < NQO; i += blockDim.x) {
+    s_opts[2 * i] = Rr.tri_out_pts[2 * i];
+    s_opts[2 * i + 1] = Rr.tri_out_pts[2 * i + 1];
+    s_ow[i] = Rr.tri_out_w[i];
+  }
+  __syncthreads();
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= P.n_inner) return;
+  const int Rs = P.R;
+  const int pidx = cls + M.row_period * (int)blockIdx.y;  // dy + R
+  const int dy = pidx - Rs;
+  const int64_t m = P.inner[t];
+  double G[NQ1];
+#pragma unroll
+  for (int q = 0; q < NQ1; q++) G[q] = 0.0;
+  unsigned c_ev = 0, c_pairs = 0, c_up = 0, c_pl = 0, c_dead = 0, c_full = 0;
+  const int cell = M.elem_cell[m];
+  const int cx = cell % M.ncx, cy = cell / M.ncx;
+  const int y2 = cy + dy;
+  if (y2 >= 0 && y2 < M.ncy) {
+    // inner element: exact points (_inner_data) and measure factor
+    double y[NQ1][2];
+    double ilo[2], ihi[2];
+    ilo[0] = M.elem_lo[m * 2];
+    ilo[1] = M.elem_lo[m * 2 + 1];
+    ihi[0] = M.elem_hi[m * 2];
+    ihi[1] = M.elem_hi[m * 2 + 1];
+    double scale_in;
+    {
+      const double *c = M.elem_coords + m * M.nv_max * 2;
+      const double e10 = xsub(c[2], c[0]), e11 = xsub(c[3], c[1]);
+      const double e20 = xsub(c[4], c[0]), e21 = xsub(c[5], c[1]);
+      scale_in = e10 * e21 - e11 * e20;
+#pragma unroll
+      for (int q = 0; q < NQ1; q++) {
+        const double p0 = Rr.tri_in_pts[2 * q], p1 = Rr.tri_in_pts[2 * q + 1];
+        y[q][0] = xadd(xadd(c[0], xmul(p0, e10)), xmul(p1, e20));
+        y[q][1] = xadd(xadd(c[1], xmul(p0, e11)), xmul(p1, e21));
+      }
+    }
+    // rows of the element's 3 vertices on the implicit pattern
+    // (assembly.py:197-223): entry (r, c) = rowptr[r] + (gy_c - ylo) Wx +
+    // (gx_c - xlo)
+    const int64_t *mdofs = M.elem_dofs + m * M.nloc_max;
+    const int NX = P.pat.NX, K = P.pat.K;
+    int64_t rowbase[NL];
+    int rxlo[NL], rylo[NL], rwx[NL];
+#pragma unroll
+    for (int i = 0; i < NL; i++) {
+      const int d = (int)mdofs[i];
+      const int gx = d % NX, gy = d / NX;
+      rxlo[i] = max(gx - K, 0);
+      rwx[i] = min(gx + K, NX - 1) - rxlo[i] + 1;
+      rylo[i] = max(gy - K, 0);
+      rowbase[i] = P.pat.rowptr[d];
+    }
+    const int64_t l0 = M.cell_ptr[(int64_t)y2 * M.ncx + max(cx - Rs, 0)];
+    const int64_t l1 =
+        M.cell_ptr[(int64_t)y2 * M.ncx + min(cx + Rs, M.ncx - 1) + 1];
+    for (int64_t l = l0; l < l1; l++) {
+      if (!P.outer_mask[l]) continue;
+      if (!(elem_gap<2>(M.elem_lo, M.elem_hi, l, m) < P.dpe)) continue;
+      c_pairs++;
+      const int64_t *ldofs = M.elem_dofs + l * M.nloc_max;
+      int64_t slot[NL][NL];
+#pragma unroll
+      for (int j = 0; j < NL; j++) {
+        const int d = (int)ldofs[j];
+        const int gx = d % NX, gy = d / NX;
+#pragma unroll
+        for (int i = 0; i < NL; i++) {
+          slot[i][j] = rowbase[i] + (int64_t)(gy - rylo[i]) * rwx[i] +
+                       (gx - rxlo[i]);
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(P.vals + slot[i][j]));
+        }
+      }
+      OuterTri OT;
+      double geo[kMaxLevels + 1][6];
+      {
+        const double *c = M.elem_coords + l * M.nv_max * 2;
+#pragma unroll
+        for (int u = 0; u < 6; u++) geo[1][u] = c[u];
+        const double e10 = c[2] - c[0], e11 = c[3] - c[1];
+        const double e20 = c[4] - c[0], e21 = c[5] - c[1];
+        const double idet = rcp_fast(e10 * e21 - e11 * e20);
+        OT.v0[0] = c[0];
+        OT.v0[1] = c[1];
+        OT.inv[0] = e21 * idet;
+        OT.inv[1] = -e20 * idet;
+        OT.inv[2] = -e11 * idet;
+        OT.inv[3] = e10 * idet;
+      }
+      double V[NQ1][NL];
+#pragma unroll
+      for (int q = 0; q < NQ1; q++)
+#pragma unroll
+        for (int j = 0; j < NL; j++) V[q][j] = 0.0;
+      double SP[NL] = {0.0, 0.0, 0.0};
+      unsigned ev = 0;
+      bool live = false;  // some plateau/full event: nonzero block
+      int child[kMaxLevels + 1];
+      int L = 1;
+      for (;;) {
+        double slo[2], shi[2];
+        sub_bbox<1>(geo[L], slo, shi);
+        int act = ACT_NONE;
+        if (L < P.L_min) {
+          act = ACT_SPLIT;
+        } else if (L == P.L_max) {
+          if (aprx_min_d<2>(slo, shi, ilo, ihi) < P.dpe) {
+            if (!P.shortcuts)
+              act = ACT_FULL;
+            else if (box_dead<2>(P, slo, shi, ilo, ihi))
+              act = ACT_DEAD;
+            else if (aprx_max_lt_dme(P, aprx_max_sq<2>(slo, shi, ilo, ihi)))
+              act = ACT_PLAT;
+            else
+              act = ACT_FULL;
+          }
+        } else if (aprx_max_lt_dme(P, aprx_max_sq<2>(slo, shi, ilo, ihi))) {
+          act = ACT_UPPER;
+        } else if (aprx_min_d<2>(slo, shi, ilo, ihi) < P.dpe) {
+          act = ACT_SPLIT;
+        }
+        if (act >= ACT_UPPER) {
+          ev++;
+          if (act == ACT_UPPER) c_up++;
+          if (act == ACT_DEAD) c_dead++;
+          if (act == ACT_PLAT) c_pl++;
+          if (act == ACT_FULL) c_full++;
+          const bool plateau =
+              act == ACT_PLAT || (act == ACT_UPPER && P.shortcuts);
+          const bool full =
+              act == ACT_FULL || (act == ACT_UPPER && !P.shortcuts);
+          live |= plateau || full;
+          if (plateau)
+            tri_plateau<NQO>(P, geo[L], OT, s_opts, s_ow, SP);
+          else if (full && P.eps > 0.0)
+            tri_full<NQO, NQ1, false>(P, geo[L], OT, y, s_opts, s_ow, V);
+          else if (full)
+            tri_full<NQO, NQ1, true>(P, geo[L], OT, y, s_opts, s_ow, V);
+        }
+        if (act == ACT_SPLIT) {
+          ++L;
+          child[L] = 0;
+          make_child<1>(geo[L - 1], 0, geo[L]);
+          continue;
+        }
+        bool done = false;
+        for (;;) {
+          if (L == 1) {
+            done = true;
+            break;
+          }
+          if (++child[L] < 4) {
+            make_child<1>(geo[L - 1], child[L], geo[L]);
+            break;
+          }
+          --L;
+        }
+        if (done) break;
+      }
+      c_ev += ev;
+      // dead-only pairs add an exactly zero block: skipped
+      if (live) {
+        const double spsum = (SP[0] + SP[1]) + SP[2];
+        const double sc = -P.scale * scale_in;
+#pragma unroll
+        for (int i = 0; i < NL; i++) {
+          double mi = 0.0;
+#pragma unroll
+          for (int q = 0; q < NQ1; q++) mi += s_phiw[q][i];
+#pragma unroll
+          for (int j = 0; j < NL; j++) {
+            double b = mi * SP[j];
+#pragma unroll
+            for (int q = 0; q < NQ1; q++) b = fma(s_phiw[q][i], V[q][j], b);
+            P.vals[slot[i][j]] += sc * b;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < NQ1; q++) {
+          double sg = spsum;
+#pragma unroll
+          for (int j = 0; j < NL; j++) sg += V[q][j];
+          G[q] += sg;
+        }
+      }
+    }
+  }
+  double *gp = gscr + ((int64_t)pidx * P.n_inner + t) * NQ1;
+#pragma unroll
+  for (int q = 0; q < NQ1; q++) gp[q] = G[q];
+  const unsigned mask = __activemask();
+  const unsigned v[6] = {c_ev, c_pairs, c_up, c_pl, c_dead, c_full};
+  const int cslot[6] = {MF_CNT_EVENTS, MF_CNT_PAIRS, MF_CNT_EV_UPPER,
+                        MF_CNT_EV_PLATEAU, MF_CNT_EV_DEAD, MF_CNT_EV_FULL};
+  const bool leader = (threadIdx.x & 31) == __ffs(mask) - 1;
+#pragma unroll
+  for (int k = 0; k < 6; k++) {
+    const unsigned sum = __reduce_add_sync(mask, v[k]);
+    if (leader && sum) atomicAdd(P.counters + cslot[k], (unsigned long long)sum);
+  }
+}
+
+// A22 of each element from the row partials of G, summed in row order
+template <int NQ1>
+__global__ void __launch_bounds__(128) k_tri_u_a22(AsmParams P,
+                                                   const double *gscr) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= P.n_inner) return;
+  const MfMesh &M = P.mesh;
+  const MfRules &Rr = P.rules;
+  const int64_t m = P.inner[t];
+  double Gt[NQ1];
+#pragma unroll
+  for (int q = 0; q < NQ1; q++) Gt[q] = 0.0;
+  for (int p = 0; p <= 2 * P.R; p++) {
+    const double *gp = gscr + ((int64_t)p * P.n_inner + t) * NQ1;
+#pragma unroll
+    for (int q = 0; q < NQ1; q++) Gt[q] += gp[q];
+  }
+  const double *c = M.elem_coords + m * M.nv_max * 2;
+  const double e10 = xsub(c[2], c[0]), e11 = xsub(c[3], c[1]);
+  const double e20 = xsub(c[4], c[0]), e21 = xsub(c[5], c[1]);
+  const double sc = P.scale * (e10 * e21 - e11 * e20);
+  const int64_t *mdofs = M.elem_dofs + m * M.nloc_max;
+#pragma unroll
+  for (int i = 0; i < 3; i++) {
+    const int64_t r = mdofs[i];
+#pragma unroll
+    for (int j = 0; j < 3; j++) {
+      double b = 0.0;
+#pragma unroll
+      for (int q = 0; q < NQ1; q++)
+        b = fma(Gt[q] * (Rr.tri_in_w[q] * Rr.phi_tri_in[q * 3 + i]),
+                Rr.phi_tri_in[q * 3 + j], b);
+      P.vals[pat_index(P.pat, r, mdofs[j])] += sc * b;
+    }
+  }
+}
+
+template <int NQO, int NQ1>
+cudaError_t launch_tri_u(const AsmParams &P, double *gscr, cudaStream_t s) {
+  const unsigned gx = (unsigned)((P.n_inner + 127) / 128);
+  const int per = P.mesh.row_period, rows = 2 * P.R + 1;
+  for (int cls = 0; cls < per; cls++) {
+    const int n = (rows - cls + per - 1) / per;
+    if (n < 1) continue;
+    k_tri_u<NQO, NQ1><<<dim3(gx, n), 128, 0, s>>>(P, cls, gscr);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  k_tri_u_a22<NQ1><<<gx, 128, 0, s>>>(P, gscr);
+  return cudaGetLastError();
+}
+
 template <int KIND, int NO, int NI>
 cudaError_t launch(const AsmParams &P, cudaStream_t s) {
   const int block = 128;
@@ -603,6 +889,7 @@ cudaError_t launch(const AsmParams &P, cudaStream_t s) {
 bool mf_2d_supported(const AsmParams &P) {
   const MfMesh &M = P.mesh;
   if (M.dim != 2 || M.degree != 1 || P.L_max > kMaxLevels) return false;
+  if (M.layout != 0) return false;  // unstructured: k_tri_u
   const MfRules &R = P.rules;
   if (M.kinds_present == 2) {  // pure triangle mesh
     return M.nloc_max == 3 && R.nq_tri_out == 7 && R.nq_tri_in == 7;
@@ -623,5 +910,30 @@ cudaError_t mf_launch_2d(const AsmParams &P, cudaStream_t s) {
   MF_Q(1, 2) MF_Q(2, 2) MF_Q(3, 2) MF_Q(4, 2)
   MF_Q(1, 3) MF_Q(2, 3) MF_Q(3, 3) MF_Q(4, 3)
 #undef MF_Q
+  return cudaErrorNotSupported;
+}
+
+bool mf_tri_u_supported(const AsmParams &P) {
+  const MfMesh &M = P.mesh;
+  if (M.layout != 1 || M.dim != 2 || M.degree != 1 || M.kinds_present != 2)
+    return false;
+  if (M.nloc_max != 3 || M.row_period < 2 || P.L_max > kMaxLevels)
+    return false;
+  const int no = P.rules.nq_tri_out, ni = P.rules.nq_tri_in;
+  return (no == 6 || no == 7) && (ni == 6 || ni == 7);
+}
+
+size_t mf_tri_u_scratch_doubles(const AsmParams &P, int64_t n_colour_max) {
+  return (size_t)(2 * P.R + 1) * (size_t)n_colour_max *
+         (size_t)P.rules.nq_tri_in;
+}
+
+cudaError_t mf_launch_tri_u(const AsmParams &P, double *gscr,
+                            cudaStream_t s) {
+  const int no = P.rules.nq_tri_out, ni = P.rules.nq_tri_in;
+  if (no == 6 && ni == 6) return launch_tri_u<6, 6>(P, gscr, s);
+  if (no == 6 && ni == 7) return launch_tri_u<6, 7>(P, gscr, s);
+  if (no == 7 && ni == 6) return launch_tri_u<7, 6>(P, gscr, s);
+  if (no == 7 && ni == 7) return launch_tri_u<7, 7>(P, gscr, s);
   return cudaErrorNotSupported;
 }

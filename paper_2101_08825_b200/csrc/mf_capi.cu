@@ -44,6 +44,9 @@ bool mf_2d_supported(const AsmParams &);
 cudaError_t mf_launch_tet(const AsmParams &, double *, cudaStream_t);
 size_t mf_tet_scratch_doubles(const AsmParams &, int64_t);
 bool mf_tet_supported(const AsmParams &);
+cudaError_t mf_launch_tri_u(const AsmParams &, double *, cudaStream_t);
+size_t mf_tri_u_scratch_doubles(const AsmParams &, int64_t);
+bool mf_tri_u_supported(const AsmParams &);
 cudaError_t mf_launch_asym(const MfPattern &, const double *, double *,
                            cudaStream_t);
 cudaError_t mf_launch_norm(const MfPattern &, const double *, double *,
@@ -278,27 +281,33 @@ int mf_general_core(const MfMesh *mesh, const MfRules *rules,
   cudaStream_t s = S(stream);
 
   const bool force_generic = (flags & MF_FLAG_FORCE_GENERIC) != 0;
-  if (mesh->kinds_present & 8) {
+  const bool tet = (mesh->kinds_present & 8) != 0;
+  if (tet && !mf_tet_supported(P))
     // tetrahedra (new element) have one kernel, mf_tet.cu
-    if (!mf_tet_supported(P))
-      return fail(MF_ERR_UNSUPPORTED,
-                  "tetrahedra need a pure P1 tet mesh, L_max <= 6 and "
-                  "1/4/11-point tet rules");
-    // per-plane G partials of one colour: stream-ordered scratch owned by
-    // this call (freed on the stream after the last launch)
+    return fail(MF_ERR_UNSUPPORTED,
+                "tetrahedra need a pure P1 tet mesh, L_max <= 6 and "
+                "1/4/11-point tet rules");
+  if (mesh->layout != 0 && (mesh->layout != 1 || mesh->row_period < 2))
+    return fail(MF_ERR_ARG, "bad mesh layout / row_period");
+  const bool tri_u = !tet && !force_generic && mf_tri_u_supported(P);
+  if (tet || tri_u) {
+    // row-split kernels (mf_tet.cu planes, mf_2d.cu k_tri_u bin rows):
+    // per-row G partials of one colour live in stream-ordered scratch
+    // owned by this call (freed on the stream after the last launch)
     int64_t nmax = 0;
     for (int c = 0; c < ncolors; c++)
       nmax = std::max<int64_t>(nmax, color_ptr[c + 1] - color_ptr[c]);
+    const size_t nd = tet ? mf_tet_scratch_doubles(P, nmax)
+                          : mf_tri_u_scratch_doubles(P, nmax);
     double *gscr = nullptr;
-    cudaError_t e = cudaMallocAsync(
-        &gscr, sizeof(double) * mf_tet_scratch_doubles(P, nmax), s);
+    cudaError_t e = cudaMallocAsync(&gscr, sizeof(double) * nd, s);
     if (e != cudaSuccess) return cuda_status(e, "mf_general_core scratch");
     for (int c = 0; c < ncolors && e == cudaSuccess; c++) {
       int64_t n = color_ptr[c + 1] - color_ptr[c];
       if (n <= 0) continue;
       P.inner = inner_sorted + color_ptr[c];
       P.n_inner = n;
-      e = mf_launch_tet(P, gscr, s);
+      e = tet ? mf_launch_tet(P, gscr, s) : mf_launch_tri_u(P, gscr, s);
     }
     cudaError_t ef = cudaFreeAsync(gscr, s);
     if (e != cudaSuccess) return cuda_status(e, "mf_general_core");

@@ -71,7 +71,9 @@ class DeviceMesh:
             ncx=int(nc[0]), ncy=int(nc[1]),
             ncz=int(nc[2]) if mesh.dim == 3 else 1,
             kinds_present=int(np.bitwise_or.reduce(
-                1 << np.unique(mesh.elem_kind).astype(np.int64))))
+                1 << np.unique(mesh.elem_kind).astype(np.int64))),
+            layout=1 if getattr(mesh, "unstructured", False) else 0,
+            row_period=int(getattr(mesh, "row_period", 2)))
 
 
 class DeviceRules:
@@ -101,7 +103,10 @@ def _nproto(mesh):
 
 
 def ncolors_of(mesh):
-    """Colours of `color_of`: 16 (2 protos), 48 for Kuhn tets (6 protos)."""
+    """Colours of `color_of`: 16 (2 protos), 48 for Kuhn tets (6 protos),
+    the greedy colour count of an unstructured mesh."""
+    if getattr(mesh, "unstructured", False):
+        return int(mesh.n_colors)
     return 8 * _nproto(mesh)
 
 
@@ -109,7 +114,10 @@ def color_of(mesh):
     """Colour id per element: cell parity bits * nproto + proto.
 
     Elements of one colour have one proto and lie in cells of one parity
-    (two apart on some axis), so they share no DOF (race-free scatter)."""
+    (two apart on some axis), so they share no DOF (race-free scatter).
+    Unstructured meshes carry a greedy vertex-disjoint colouring."""
+    if getattr(mesh, "unstructured", False):
+        return np.asarray(mesh.elem_color, dtype=np.int64)
     c = mesh.elem_cell.astype(np.int64)
     col = (c[:, 0] & 1) | ((c[:, 1] & 1) << 1)
     if mesh.dim == 3:

@@ -14,8 +14,9 @@ import math
 
 import numpy as np
 
-__all__ = ["BoundingBox", "Element", "Mesh", "PartitionMap", "build_mesh",
-           "refine", "partition_geometric"]
+__all__ = ["BoundingBox", "DelaunayMesh", "Element", "Mesh", "PartitionMap",
+           "build_delaunay_mesh", "build_mesh", "refine",
+           "partition_geometric"]
 
 KIND_CODE = {"quad": 0, "tri": 1, "hex": 2, "tet": 3}
 KIND_NAME = {0: "quad", 1: "tri", 2: "hex", 3: "tet"}
@@ -370,3 +371,183 @@ def partition_geometric(mesh, n_parts):
         boxes.append(BoundingBox(mesh.elem_lo[ids].min(axis=0),
                                  mesh.elem_hi[ids].max(axis=0)))
     return PartitionMap(n_parts, owner, boxes)
+
+
+# ---------------------------------------------------------------------------
+# unstructured Delaunay triangle meshes (BASELINE config #2; new -- the
+# reference builds structured meshes only, mesh.py:153-178)
+
+class DelaunayMesh(Mesh):
+    """Delaunay P1 triangulation of jittered lattice points.
+
+    Every vertex is drawn from one lattice node of pitch h (uniform offset
+    in [-jitter*h, jitter*h] per axis) and keeps that node's lattice index
+    as its id, so the DOF numbering and the implicit box pattern of the
+    structured path apply unchanged.  The triangulation itself is
+    unstructured: connectivity, valence and element shapes come from
+    scipy's Delaunay (qhull).  Elements are binned by the lattice cell of
+    their bounding-box lower corner and stored in bin-lex order, which is
+    the cell ordering the neighbour search and the kernels walk.
+
+    Extra attributes over `Mesh`:
+      unstructured  True
+      emax          largest element box side (<= 2h is asserted)
+      elem_color    greedy colouring: elements of one colour share no vertex
+      n_colors      number of colours
+      row_period    stencil rows this far apart hold outer elements that
+                    share no vertex (3, since emax <= 2h)
+    """
+
+    unstructured = True
+    row_period = 3
+
+    @property
+    def stencil_pad(self):
+        # element boxes reach emax beyond the lower corner that bins them
+        return self.emax
+
+    @property
+    def pattern_pad(self):
+        # coupled vertices lie within reach + 2 emax of each other, and a
+        # vertex within jitter*h of its lattice node
+        return 2.0 * self.emax + 2.0 * self.jitter * self.h
+
+
+def _greedy_colors(elem_nodes, n_nodes, seed=0):
+    """Jones-Plassmann colouring of the element/vertex-sharing graph:
+    each round, every uncoloured element whose random priority beats all
+    its uncoloured neighbours takes the smallest colour no neighbour has.
+    Deterministic for a seed; about max-degree+1 colours at most."""
+    n, nv = elem_nodes.shape
+    flat = elem_nodes.ravel()
+    eid = np.repeat(np.arange(n), nv)
+    order = np.argsort(flat, kind="stable")
+    vptr = np.searchsorted(flat[order], np.arange(n_nodes + 1))
+    ve = eid[order]
+    # element pairs sharing a vertex
+    cnt = np.diff(vptr)
+    src, dst = [], []
+    for k in range(1, int(cnt.max()) if cnt.size else 1):
+        has = np.nonzero(cnt > k)[0]
+        for j in range(k):
+            a = ve[vptr[has] + k]
+            b = ve[vptr[has] + j]
+            src += [a, b]
+            dst += [b, a]
+    src = np.concatenate(src) if src else np.zeros(0, np.int64)
+    dst = np.concatenate(dst) if dst else np.zeros(0, np.int64)
+    # (pairs sharing two vertices appear twice; harmless below)
+    rng = np.random.default_rng(seed)
+    prio = rng.permutation(n)
+    color = np.full(n, -1, dtype=np.int64)
+    while True:
+        unc = color < 0
+        if not unc.any():
+            break
+        # keep only edges out of uncoloured elements
+        keep = unc[src]
+        src, dst = src[keep], dst[keep]
+        # an uncoloured neighbour with higher priority -> wait this round
+        blocked = np.zeros(n, dtype=bool)
+        sel = unc[dst] & (prio[dst] > prio[src])
+        blocked[src[sel]] = True
+        pick = unc & ~blocked
+        # colours used by coloured neighbours (bit mask, < 63 colours)
+        used = np.zeros(n, dtype=np.int64)
+        cs = ~unc[dst] & pick[src]
+        np.bitwise_or.at(used, src[cs], np.int64(1) << color[dst[cs]])
+        ids = np.nonzero(pick)[0]
+        u = used[ids]
+        low = ~u & (u + 1)               # lowest clear bit = smallest free
+        color[ids] = np.log2(low.astype(np.float64)).astype(np.int64)
+    return color
+
+
+def build_delaunay_mesh(omega_bounds, h, layer_width, jitter=0.3, seed=0):
+    """Unstructured Delaunay P1 mesh of Omega plus ceil(layer_width/h)
+    Gamma rings (BASELINE config #2: seeded uniform jittered vertices).
+
+    Lattice nodes of pitch h are moved by a seeded uniform offset in
+    [-jitter*h, jitter*h] per axis; nodes on the outer boundary or on the
+    Omega/Gamma interface keep that coordinate and move along their line
+    by at most jitter*h/2.  Each interface segment is then a Gabriel edge
+    (its diametral circle, radius <= (1+jitter)h/2, holds no other node),
+    so it is a Delaunay edge and every triangle lies in Omega or in Gamma;
+    the builder checks this, the orientation and emax <= 2h.
+    """
+    from scipy.spatial import Delaunay
+    if not 0.0 <= jitter <= 0.35:
+        raise ValueError("jitter must lie in [0, 0.35]")
+    if h <= 0.0 or layer_width < 0.0:
+        raise ValueError("need h > 0 and layer_width >= 0")
+    dim = 2
+    box = _as_bounds(omega_bounds, dim)
+    side = box.hi - box.lo
+    n_omega = np.rint(side / h).astype(int)
+    if np.any(n_omega < 1) or np.any(
+            np.abs(n_omega * h - side) > 1e-9 * np.maximum(1.0, side)):
+        raise ValueError(f"omega side lengths {side.tolist()} are not "
+                         f"integer multiples of h={h}")
+    rings = int(math.ceil(layer_width / h - 1e-9)) if layer_width > 0.0 else 0
+    nc = n_omega + 2 * rings
+    nv = nc + 1
+    origin = box.lo - rings * h
+    gy, gx = np.meshgrid(np.arange(nv[1]), np.arange(nv[0]), indexing="ij")
+    gidx = np.stack([gx.ravel(), gy.ravel()], axis=1)     # lattice-lex ids
+    base = origin[None, :] + h * gidx
+    rng = np.random.default_rng(seed)
+    off = rng.uniform(-jitter * h, jitter * h, size=base.shape)
+    fixed = ((gidx == 0) | (gidx == nv[None, :] - 1) | (gidx == rings)
+             | (gidx == rings + n_omega[None, :]))
+    online = fixed.any(axis=1, keepdims=True)
+    off = np.where(fixed, 0.0, np.where(online, 0.5 * off, off))
+    nodes = base + off
+    tri = Delaunay(nodes)
+    en = np.ascontiguousarray(tri.simplices.astype(np.int64))
+    c = nodes[en]
+    det = ((c[:, 1, 0] - c[:, 0, 0]) * (c[:, 2, 1] - c[:, 0, 1])
+           - (c[:, 1, 1] - c[:, 0, 1]) * (c[:, 2, 0] - c[:, 0, 0]))
+    flip = det < 0.0
+    en[flip] = en[flip][:, [0, 2, 1]]                    # counter-clockwise
+    # canonical vertex order: smallest id first (rotation keeps the
+    # orientation), so the element arrays depend only on the triangulation
+    first = np.argmin(en, axis=1)
+    rot = (first[:, None] + np.arange(3)[None, :]) % 3
+    en = np.take_along_axis(en, rot, axis=1)
+    if np.any(np.abs(det) < 1e-6 * h * h):
+        raise RuntimeError("degenerate Delaunay triangle")
+    c = nodes[en]
+    lo = c.min(axis=1)
+    hi = c.max(axis=1)
+    emax = float((hi - lo).max())
+    if emax > 2.0 * h:
+        raise RuntimeError(f"element extent {emax / h:.3f} h exceeds 2h")
+    cen = c.mean(axis=1)
+    in_omega = np.all((cen > box.lo) & (cen < box.hi), axis=1)
+    vin = np.all((c >= box.lo - 1e-12) & (c <= box.hi + 1e-12), axis=(1, 2))
+    vstrict = np.all((c > box.lo) & (c < box.hi), axis=2).any(axis=1)
+    if np.any(in_omega & ~vin) or np.any(~in_omega & vstrict):
+        raise RuntimeError("a triangle straddles the Omega/Gamma interface")
+    # bin by the lattice cell of the box lower corner; bin-lex order
+    cell = np.floor((lo - origin[None, :]) / h).astype(np.int64)
+    cell = np.clip(cell, 0, nc[None, :] - 1)
+    order = np.lexsort((en[:, 2], en[:, 1], en[:, 0], cell[:, 0],
+                        cell[:, 1]))
+    en, c, lo, hi, cell = en[order], c[order], lo[order], hi[order], \
+        cell[order]
+    in_omega = in_omega[order]
+    n = en.shape[0]
+    arrays = (np.full(n, 1, np.int8), np.zeros(n, np.int8),
+              np.where(in_omega, 0, 1).astype(np.int8),
+              cell.astype(np.int32), np.ascontiguousarray(c),
+              np.ascontiguousarray(lo), np.ascontiguousarray(hi))
+    m = DelaunayMesh(dim, nodes, en, h, box, rings, "tri", layer_width,
+                     tuple(int(x) for x in nc), origin, arrays, jitter, seed)
+    m.emax = emax
+    # lattice planes a vertex sits above its element's bin row (top axis)
+    m.dof_spill = int((en // nv[0] - cell[:, 1:2]).max())
+    if (en // nv[0] - cell[:, 1:2]).min() < 0:
+        raise RuntimeError("a vertex lies below its element's bin row")
+    m.elem_color = _greedy_colors(en, nodes.shape[0], seed)
+    m.n_colors = int(m.elem_color.max()) + 1
+    return m

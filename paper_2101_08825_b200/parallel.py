@@ -16,7 +16,8 @@ Two layers:
    its inner element (_kernels.py:483-486), so rank r writes only the DOF
    planes of its layers; those rows are a contiguous range of the
    implicit pattern (DOF ids are z-major), so each rank allocates only its
-   row block.  The single shared DOF plane between consecutive slabs is
+   row block.  The shared DOF plane(s) between consecutive slabs (one on
+   structured meshes, `dof_spill` on Delaunay meshes) are
    summed with one send/recv per interface (rank r -> r+1, added in rank
    order), after which every rank owns a disjoint row block; `gather`
    collects the blocks on rank 0 (NCCL has no gatherv, so grouped
@@ -209,8 +210,13 @@ class SlabPlan:
         nplanes = int(dims[-1])
         lo, hi = layers[rank]
         self.layers = (lo, hi)
-        # DOF planes touched by this slab's elements: [d*lo, d*hi]
-        self.touch_planes = (d * lo, min(d * hi, nplanes - 1))
+        # an element of cell layer c touches DOF planes [d*c, d*c + spill]:
+        # spill = d on structured meshes; on Delaunay meshes vertices may
+        # sit up to mesh.dof_spill lattice planes above the element's bin
+        spill = int(getattr(mesh, "dof_spill", d))
+        self.spill = spill
+        # DOF planes touched by this slab's elements: [d*lo, d*(hi-1)+spill]
+        self.touch_planes = (d * lo, min(d * (hi - 1) + spill, nplanes - 1))
         # owned planes: [d*lo, d*hi) ; the last rank also owns the top
         own_hi = d * hi if rank < self.world - 1 else nplanes
         self.own_planes = (d * lo, own_hi)
@@ -222,17 +228,23 @@ class SlabPlan:
                            int(rowptr[self.rows_touch[1]]))
         self.vals_own = (int(rowptr[self.rows_own[0]]),
                          int(rowptr[self.rows_own[1]]))
-        # the shared plane with the next rank (= its first owned plane)
+        # the planes shared with the next rank: its first spill - d + 1
+        # owned planes (one plane on structured meshes)
+        nshare = spill - d + 1
         if rank < self.world - 1:
+            nxt_hi = layers[rank + 1][1]
+            if d * hi + nshare > (d * nxt_hi if rank + 1 < self.world - 1
+                                  else nplanes):
+                raise ValueError("slab too thin for the element spill")
             p = d * hi
             self.send_range = (int(rowptr[p * plane]),
-                               int(rowptr[(p + 1) * plane]))
+                               int(rowptr[(p + nshare) * plane]))
         else:
             self.send_range = None
         if rank > 0:
             p = d * lo
             self.recv_range = (int(rowptr[p * plane]),
-                               int(rowptr[(p + 1) * plane]))
+                               int(rowptr[(p + nshare) * plane]))
         else:
             self.recv_range = None
 
