@@ -23,6 +23,12 @@
 namespace {
 
 constexpr int kMaxLevels = 6;
+#ifndef MF_TRI_QUEUE
+#define MF_TRI_QUEUE 1
+#endif
+#ifndef MF_TRI_U_FLAT
+#define MF_TRI_U_FLAT 1
+#endif
 #ifndef MF_2D_MINB
 #define MF_2D_MINB 2
 #endif
@@ -675,10 +681,21 @@ __global__ void __launch_bounds__(128, MF_2D_MINB)
       rylo[i] = max(gy - K, 0);
       rowbase[i] = P.pat.rowptr[d];
     }
+#if MF_TRI_U_FLAT
     const int64_t l0 = M.cell_ptr[(int64_t)y2 * M.ncx + max(cx - Rs, 0)];
     const int64_t l1 =
         M.cell_ptr[(int64_t)y2 * M.ncx + min(cx + Rs, M.ncx - 1) + 1];
     for (int64_t l = l0; l < l1; l++) {
+#else
+    // walk the row by relative bin offset dx, so the lanes of a warp visit
+    // partners at the same offset at the same time (similar pair geometry,
+    // similar Algorithm-1 paths)
+    for (int dx = -Rs; dx <= Rs; dx++) {
+      const int x2 = cx + dx;
+      if (x2 < 0 || x2 >= M.ncx) continue;
+      const int64_t c2 = (int64_t)y2 * M.ncx + x2;
+      for (int64_t l = M.cell_ptr[c2]; l < M.cell_ptr[c2 + 1]; l++) {
+#endif
       if (!P.outer_mask[l]) continue;
       if (!(elem_gap<2>(M.elem_lo, M.elem_hi, l, m) < P.dpe)) continue;
       c_pairs++;
@@ -807,6 +824,9 @@ __global__ void __launch_bounds__(128, MF_2D_MINB)
           G[q] += sg;
         }
       }
+#if !MF_TRI_U_FLAT
+      }
+#endif
     }
   }
   double *gp = gscr + ((int64_t)pidx * P.n_inner + t) * NQ1;
@@ -861,14 +881,344 @@ __global__ void __launch_bounds__(128) k_tri_u_a22(AsmParams P,
   }
 }
 
+// ---- k_tri_q: k_tri_u with warp-cooperative full events ----
+//
+// Unstructured pairs take different Algorithm-1 paths, so the lanes of a
+// k_tri_u warp diverge (ncu: ~6.6 of 32 threads active).  Here each lane
+// walks its pair's tree (classification, dead events and the cheap plateau
+// events inline) and only RECORDS its full L_max events as a bit mask over
+// the 4^(L_max-1) <= 16 leaf sub-triangles.  The warp then integrates all
+// recorded events of its 32 pairs together, 32 events per round, every
+// lane running the identical 36/49-point-pair event code; each event's
+// V contribution goes through shared memory back to its owner lane, which
+// adds them in queue order (owner lane, then leaf index) -- deterministic.
+// Requires eps > 0, shortcuts on and L_max <= 3 (else k_tri_u runs).
+constexpr int kTriQWarps = 4;
+
+template <int NQO, int NQ1>
+__global__ void __launch_bounds__(32 * kTriQWarps, MF_2D_MINB)
+    k_tri_q(AsmParams P, int cls, double *gscr) {
+  constexpr int NL = 3;
+  constexpr int NV = NQ1 * NL;
+  __shared__ double s_phiw[NQ1][NL];
+  __shared__ double s_opts[2 * NQO], s_ow[NQO];
+  // per-lane pair state, lane-major: inner points, outer root + inverse
+  __shared__ double s_y[kTriQWarps][NQ1][2][32];
+  __shared__ double s_root[kTriQWarps][6][32];   // outer root triangle
+  __shared__ double s_res[kTriQWarps][NV][32];   // per-event V (round)
+  __shared__ int s_off[kTriQWarps][33];
+  __shared__ unsigned s_mask[kTriQWarps][32];
+  const MfMesh &M = P.mesh;
+  const MfRules &Rr = P.rules;
+  for (int i = threadIdx.x; i < NQ1 * NL; i += blockDim.x) {
+    const int q = i / NL, j = i % NL;
+    s_phiw[q][j] = Rr.tri_in_w[q] * Rr.phi_tri_in[q * NL + j];
+  }
+  for (int i = threadIdx.x; i < NQO; i += blockDim.x) {
+    s_opts[2 * i] = Rr.tri_out_pts[2 * i];
+    s_opts[2 * i + 1] = Rr.tri_out_pts[2 * i + 1];
+    s_ow[i] = Rr.tri_out_w[i];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = t < P.n_inner;
+  const int Rs = P.R;
+  const int pidx = cls + M.row_period * (int)blockIdx.y;  // dy + R
+  const int dy = pidx - Rs;
+  const int64_t m = valid ? P.inner[t] : P.inner[0];
+  double G[NQ1];
+#pragma unroll
+  for (int q = 0; q < NQ1; q++) G[q] = 0.0;
+  unsigned c_ev = 0, c_pairs = 0, c_up = 0, c_pl = 0, c_dead = 0, c_full = 0;
+  const int cell = M.elem_cell[m];
+  const int cx = cell % M.ncx, cy = cell / M.ncx;
+  const int y2 = cy + dy;
+  // candidate range of this lane's stencil row (empty for idle lanes)
+  int64_t l = 0, l1 = 0;
+  if (valid && y2 >= 0 && y2 < M.ncy) {
+    l = M.cell_ptr[(int64_t)y2 * M.ncx + max(cx - Rs, 0)];
+    l1 = M.cell_ptr[(int64_t)y2 * M.ncx + min(cx + Rs, M.ncx - 1) + 1];
+  }
+  double ilo[2], ihi[2], scale_in;
+  ilo[0] = M.elem_lo[m * 2];
+  ilo[1] = M.elem_lo[m * 2 + 1];
+  ihi[0] = M.elem_hi[m * 2];
+  ihi[1] = M.elem_hi[m * 2 + 1];
+  {
+    const double *c = M.elem_coords + m * M.nv_max * 2;
+    const double e10 = xsub(c[2], c[0]), e11 = xsub(c[3], c[1]);
+    const double e20 = xsub(c[4], c[0]), e21 = xsub(c[5], c[1]);
+    scale_in = e10 * e21 - e11 * e20;
+    for (int q = 0; q < NQ1; q++) {
+      const double p0 = Rr.tri_in_pts[2 * q], p1 = Rr.tri_in_pts[2 * q + 1];
+      s_y[w][q][0][lane] = xadd(xadd(c[0], xmul(p0, e10)), xmul(p1, e20));
+      s_y[w][q][1][lane] = xadd(xadd(c[1], xmul(p0, e11)), xmul(p1, e21));
+    }
+  }
+  const int64_t *mdofs = M.elem_dofs + m * M.nloc_max;
+  const int NX = P.pat.NX, K = P.pat.K;
+  const int nleaf_bits = 2 * (P.L_max - 1);
+  for (;;) {
+    // ---- phase A: next candidate pair of this lane, walked alone ----
+    bool have = false;
+    while (l < l1) {
+      if (P.outer_mask[l] && elem_gap<2>(M.elem_lo, M.elem_hi, l, m) < P.dpe) {
+        have = true;
+        break;
+      }
+      l++;
+    }
+    if (!__any_sync(0xffffffffu, have)) break;
+    unsigned fmask = 0;
+    unsigned ev = 0;
+    double SP[NL] = {0.0, 0.0, 0.0};
+    bool live = false;
+    if (have) {
+      c_pairs++;
+      const int64_t *ldofs = M.elem_dofs + l * M.nloc_max;
+#pragma unroll
+      for (int j = 0; j < NL; j++) {
+        const int d = (int)ldofs[j];
+        const int gx = d % NX, gy = d / NX;
+#pragma unroll
+        for (int i = 0; i < NL; i++) {
+          const int rd = (int)mdofs[i];
+          const int rgx = rd % NX, rgy = rd / NX;
+          const int xlo = max(rgx - K, 0);
+          const int wx = min(rgx + K, NX - 1) - xlo + 1;
+          const int64_t sl = P.pat.rowptr[rd] +
+                             (int64_t)(gy - max(rgy - K, 0)) * wx + (gx - xlo);
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(P.vals + sl));
+        }
+      }
+      OuterTri OT;
+      double geo[kMaxLevels + 1][6];
+      {
+        const double *c = M.elem_coords + l * M.nv_max * 2;
+#pragma unroll
+        for (int u = 0; u < 6; u++) {
+          geo[1][u] = c[u];
+          s_root[w][u][lane] = c[u];
+        }
+        const double e10 = c[2] - c[0], e11 = c[3] - c[1];
+        const double e20 = c[4] - c[0], e21 = c[5] - c[1];
+        const double idet = rcp_fast(e10 * e21 - e11 * e20);
+        OT.v0[0] = c[0];
+        OT.v0[1] = c[1];
+        OT.inv[0] = e21 * idet;
+        OT.inv[1] = -e20 * idet;
+        OT.inv[2] = -e11 * idet;
+        OT.inv[3] = e10 * idet;
+      }
+      int child[kMaxLevels + 1];
+      int L = 1;
+      for (;;) {
+        double slo[2], shi[2];
+        sub_bbox<1>(geo[L], slo, shi);
+        int act = ACT_NONE;
+        if (L < P.L_min) {
+          act = ACT_SPLIT;
+        } else if (L == P.L_max) {
+          if (aprx_min_d<2>(slo, shi, ilo, ihi) < P.dpe) {
+            if (box_dead<2>(P, slo, shi, ilo, ihi))
+              act = ACT_DEAD;
+            else if (aprx_max_lt_dme(P, aprx_max_sq<2>(slo, shi, ilo, ihi)))
+              act = ACT_PLAT;
+            else
+              act = ACT_FULL;
+          }
+        } else if (aprx_max_lt_dme(P, aprx_max_sq<2>(slo, shi, ilo, ihi))) {
+          act = ACT_UPPER;
+        } else if (aprx_min_d<2>(slo, shi, ilo, ihi) < P.dpe) {
+          act = ACT_SPLIT;
+        }
+        if (act >= ACT_UPPER) {
+          ev++;
+          if (act == ACT_UPPER) c_up++;
+          if (act == ACT_DEAD) c_dead++;
+          if (act == ACT_PLAT) c_pl++;
+          if (act == ACT_FULL) {
+            c_full++;
+            int leaf = 0;
+            for (int k = 2; k <= L; k++) leaf = 4 * leaf + child[k];
+            fmask |= 1u << leaf;
+          }
+          if (act == ACT_PLAT || act == ACT_UPPER) {
+            live = true;
+            tri_plateau<NQO>(P, geo[L], OT, s_opts, s_ow, SP);
+          }
+        }
+        if (act == ACT_SPLIT) {
+          ++L;
+          child[L] = 0;
+          make_child<1>(geo[L - 1], 0, geo[L]);
+          continue;
+        }
+        bool done = false;
+        for (;;) {
+          if (L == 1) {
+            done = true;
+            break;
+          }
+          if (++child[L] < 4) {
+            make_child<1>(geo[L - 1], child[L], geo[L]);
+            break;
+          }
+          --L;
+        }
+        if (done) break;
+      }
+      live |= fmask != 0;
+    }
+    // ---- phase B: the warp's full events, 32 per round, converged ----
+    const int cnt = __popc(fmask);
+    int off = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, off, d);
+      if (lane >= d) off += v;
+    }
+    const int total = __shfl_sync(0xffffffffu, off, 31);
+    off -= cnt;  // exclusive prefix
+    s_off[w][lane] = off;
+    s_mask[w][lane] = fmask;
+    if (lane == 31) s_off[w][32] = total;
+    __syncwarp();
+    double V[NQ1][NL];
+#pragma unroll
+    for (int q = 0; q < NQ1; q++)
+#pragma unroll
+      for (int j = 0; j < NL; j++) V[q][j] = 0.0;
+    for (int base = 0; base < total; base += 32) {
+      const int g = base + lane;
+      if (g < total) {
+        // owner lane o: s_off[w][o] <= g < s_off[w][o + 1]
+        int o = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1)
+          if (s_off[w][o + step] <= g) o += step;
+        const unsigned om = s_mask[w][o];
+        const int leaf = __fns(om, 0, g - s_off[w][o] + 1);
+        double gg[6];
+#pragma unroll
+        for (int u = 0; u < 6; u++) gg[u] = s_root[w][u][o];
+        // the owner's outer inverse map, recomputed from its root exactly
+        // as in phase A
+        OuterTri O;
+        {
+          const double e10 = gg[2] - gg[0], e11 = gg[3] - gg[1];
+          const double e20 = gg[4] - gg[0], e21 = gg[5] - gg[1];
+          const double idet = rcp_fast(e10 * e21 - e11 * e20);
+          O.v0[0] = gg[0];
+          O.v0[1] = gg[1];
+          O.inv[0] = e21 * idet;
+          O.inv[1] = -e20 * idet;
+          O.inv[2] = -e11 * idet;
+          O.inv[3] = e10 * idet;
+        }
+        for (int b = nleaf_bits - 2; b >= 0; b -= 2) {
+          double c[6];
+          make_child<1>(gg, (leaf >> b) & 3, c);
+#pragma unroll
+          for (int u = 0; u < 6; u++) gg[u] = c[u];
+        }
+        double yy[NQ1][2];
+#pragma unroll
+        for (int q = 0; q < NQ1; q++) {
+          yy[q][0] = s_y[w][q][0][o];
+          yy[q][1] = s_y[w][q][1][o];
+        }
+        double Ve[NQ1][NL];
+#pragma unroll
+        for (int q = 0; q < NQ1; q++)
+#pragma unroll
+          for (int j = 0; j < NL; j++) Ve[q][j] = 0.0;
+        tri_full<NQO, NQ1, false>(P, gg, O, yy, s_opts, s_ow, Ve);
+#pragma unroll
+        for (int q = 0; q < NQ1; q++)
+#pragma unroll
+          for (int j = 0; j < NL; j++) s_res[w][q * NL + j][lane] = Ve[q][j];
+      }
+      __syncwarp();
+      // owner: add this round's results of its own events, queue order
+      const int a = max(off, base), b = min(off + cnt, base + 32);
+      for (int k = a; k < b; k++) {
+#pragma unroll
+        for (int q = 0; q < NQ1; q++)
+#pragma unroll
+          for (int j = 0; j < NL; j++) V[q][j] += s_res[w][q * NL + j][k - base];
+      }
+      __syncwarp();
+    }
+    if (have) {
+      c_ev += ev;
+      // dead-only pairs add an exactly zero block: skipped
+      if (live) {
+        const int64_t *ldofs = M.elem_dofs + l * M.nloc_max;
+        const double spsum = (SP[0] + SP[1]) + SP[2];
+        const double sc = -P.scale * scale_in;
+#pragma unroll
+        for (int i = 0; i < NL; i++) {
+          const int rd = (int)mdofs[i];
+          const int rgx = rd % NX, rgy = rd / NX;
+          const int xlo = max(rgx - K, 0);
+          const int wx = min(rgx + K, NX - 1) - xlo + 1;
+          const int64_t rb = P.pat.rowptr[rd];
+          const int ylo = max(rgy - K, 0);
+          double mi = 0.0;
+#pragma unroll
+          for (int q = 0; q < NQ1; q++) mi += s_phiw[q][i];
+#pragma unroll
+          for (int j = 0; j < NL; j++) {
+            double bsum = mi * SP[j];
+#pragma unroll
+            for (int q = 0; q < NQ1; q++)
+              bsum = fma(s_phiw[q][i], V[q][j], bsum);
+            const int d = (int)ldofs[j];
+            const int gx = d % NX, gy = d / NX;
+            P.vals[rb + (int64_t)(gy - ylo) * wx + (gx - xlo)] += sc * bsum;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < NQ1; q++) {
+          double sg = spsum;
+#pragma unroll
+          for (int j = 0; j < NL; j++) sg += V[q][j];
+          G[q] += sg;
+        }
+      }
+      l++;
+    }
+  }
+  if (valid) {
+    double *gp = gscr + ((int64_t)pidx * P.n_inner + t) * NQ1;
+#pragma unroll
+    for (int q = 0; q < NQ1; q++) gp[q] = G[q];
+  }
+  const unsigned v[6] = {c_ev, c_pairs, c_up, c_pl, c_dead, c_full};
+  const int cslot[6] = {MF_CNT_EVENTS, MF_CNT_PAIRS, MF_CNT_EV_UPPER,
+                        MF_CNT_EV_PLATEAU, MF_CNT_EV_DEAD, MF_CNT_EV_FULL};
+#pragma unroll
+  for (int k = 0; k < 6; k++) {
+    const unsigned sum = __reduce_add_sync(0xffffffffu, v[k]);
+    if (lane == 0 && sum) atomicAdd(P.counters + cslot[k], (unsigned long long)sum);
+  }
+}
+
 template <int NQO, int NQ1>
 cudaError_t launch_tri_u(const AsmParams &P, double *gscr, cudaStream_t s) {
   const unsigned gx = (unsigned)((P.n_inner + 127) / 128);
   const int per = P.mesh.row_period, rows = 2 * P.R + 1;
+  const bool queue = MF_TRI_QUEUE && P.eps > 0.0 && P.shortcuts &&
+                     P.L_max <= 3;
   for (int cls = 0; cls < per; cls++) {
     const int n = (rows - cls + per - 1) / per;
     if (n < 1) continue;
-    k_tri_u<NQO, NQ1><<<dim3(gx, n), 128, 0, s>>>(P, cls, gscr);
+    if (queue)
+      k_tri_q<NQO, NQ1><<<dim3(gx, n), 32 * kTriQWarps, 0, s>>>(P, cls, gscr);
+    else
+      k_tri_u<NQO, NQ1><<<dim3(gx, n), 128, 0, s>>>(P, cls, gscr);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
