@@ -895,6 +895,20 @@ __global__ void __launch_bounds__(128) k_tri_u_a22(AsmParams P,
 // Requires eps > 0, shortcuts on and L_max <= 3 (else k_tri_u runs).
 constexpr int kTriQWarps = 4;
 
+// d = gy*NX + gx for a lattice id d < 2^24 (checked on the host): float
+// quotient, then one exact integer correction step
+MF_DEV void lattice_split(int d, int NX, float inv_nx, int &gx, int &gy) {
+  gy = __float2int_rz(__int2float_rn(d) * inv_nx);
+  gx = d - gy * NX;
+  if (gx < 0) {
+    gx += NX;
+    gy--;
+  } else if (gx >= NX) {
+    gx -= NX;
+    gy++;
+  }
+}
+
 template <int NQO, int NQ1>
 __global__ void __launch_bounds__(32 * kTriQWarps, MF_2D_MINB)
     k_tri_q(AsmParams P, int cls, double *gscr) {
@@ -908,6 +922,9 @@ __global__ void __launch_bounds__(32 * kTriQWarps, MF_2D_MINB)
   __shared__ double s_res[kTriQWarps][NV][32];   // per-event V (round)
   __shared__ int s_off[kTriQWarps][33];
   __shared__ unsigned s_mask[kTriQWarps][32];
+  // the lane's 3 pattern rows: rowptr base shifted to (ylo, xlo), width
+  __shared__ long long s_rb[kTriQWarps][NL][32];
+  __shared__ int s_wx[kTriQWarps][NL][32];
   const MfMesh &M = P.mesh;
   const MfRules &Rr = P.rules;
   for (int i = threadIdx.x; i < NQ1 * NL; i += blockDim.x) {
@@ -958,6 +975,19 @@ __global__ void __launch_bounds__(32 * kTriQWarps, MF_2D_MINB)
   }
   const int64_t *mdofs = M.elem_dofs + m * M.nloc_max;
   const int NX = P.pat.NX, K = P.pat.K;
+  const float inv_nx = 1.0f / (float)NX;
+  // entry (r, c) = rowptr[r] + (gy_c - ylo) Wx + (gx_c - xlo)
+  //             = rb + gy_c Wx + gx_c  with rb = rowptr[r] - ylo Wx - xlo
+#pragma unroll
+  for (int i = 0; i < NL; i++) {
+    int rgx, rgy;
+    lattice_split((int)mdofs[i], NX, inv_nx, rgx, rgy);
+    const int xlo = max(rgx - K, 0);
+    const int wx = min(rgx + K, NX - 1) - xlo + 1;
+    s_rb[w][i][lane] = (long long)P.pat.rowptr[mdofs[i]] -
+                       (long long)max(rgy - K, 0) * wx - xlo;
+    s_wx[w][i][lane] = wx;
+  }
   const int nleaf_bits = 2 * (P.L_max - 1);
   for (;;) {
     // ---- phase A: next candidate pair of this lane, walked alone ----
@@ -979,16 +1009,12 @@ __global__ void __launch_bounds__(32 * kTriQWarps, MF_2D_MINB)
       const int64_t *ldofs = M.elem_dofs + l * M.nloc_max;
 #pragma unroll
       for (int j = 0; j < NL; j++) {
-        const int d = (int)ldofs[j];
-        const int gx = d % NX, gy = d / NX;
+        int gx, gy;
+        lattice_split((int)ldofs[j], NX, inv_nx, gx, gy);
 #pragma unroll
         for (int i = 0; i < NL; i++) {
-          const int rd = (int)mdofs[i];
-          const int rgx = rd % NX, rgy = rd / NX;
-          const int xlo = max(rgx - K, 0);
-          const int wx = min(rgx + K, NX - 1) - xlo + 1;
-          const int64_t sl = P.pat.rowptr[rd] +
-                             (int64_t)(gy - max(rgy - K, 0)) * wx + (gx - xlo);
+          const int64_t sl = s_rb[w][i][lane] +
+                             (int64_t)gy * s_wx[w][i][lane] + gx;
           asm volatile("prefetch.global.L2 [%0];" ::"l"(P.vals + sl));
         }
       }
@@ -1158,14 +1184,14 @@ __global__ void __launch_bounds__(32 * kTriQWarps, MF_2D_MINB)
         const int64_t *ldofs = M.elem_dofs + l * M.nloc_max;
         const double spsum = (SP[0] + SP[1]) + SP[2];
         const double sc = -P.scale * scale_in;
+        int cgx[NL], cgy[NL];
+#pragma unroll
+        for (int j = 0; j < NL; j++)
+          lattice_split((int)ldofs[j], NX, inv_nx, cgx[j], cgy[j]);
 #pragma unroll
         for (int i = 0; i < NL; i++) {
-          const int rd = (int)mdofs[i];
-          const int rgx = rd % NX, rgy = rd / NX;
-          const int xlo = max(rgx - K, 0);
-          const int wx = min(rgx + K, NX - 1) - xlo + 1;
-          const int64_t rb = P.pat.rowptr[rd];
-          const int ylo = max(rgy - K, 0);
+          const int64_t rb = s_rb[w][i][lane];
+          const int wx = s_wx[w][i][lane];
           double mi = 0.0;
 #pragma unroll
           for (int q = 0; q < NQ1; q++) mi += s_phiw[q][i];
@@ -1175,9 +1201,7 @@ __global__ void __launch_bounds__(32 * kTriQWarps, MF_2D_MINB)
 #pragma unroll
             for (int q = 0; q < NQ1; q++)
               bsum = fma(s_phiw[q][i], V[q][j], bsum);
-            const int d = (int)ldofs[j];
-            const int gx = d % NX, gy = d / NX;
-            P.vals[rb + (int64_t)(gy - ylo) * wx + (gx - xlo)] += sc * bsum;
+            P.vals[rb + (int64_t)cgy[j] * wx + cgx[j]] += sc * bsum;
           }
         }
 #pragma unroll
@@ -1269,6 +1293,7 @@ bool mf_tri_u_supported(const AsmParams &P) {
     return false;
   if (M.nloc_max != 3 || M.row_period < 2 || P.L_max > kMaxLevels)
     return false;
+  if (P.pat.n >= (1 << 24)) return false;  // lattice_split range
   const int no = P.rules.nq_tri_out, ni = P.rules.nq_tri_in;
   return (no == 6 || no == 7) && (ni == 6 || ni == 7);
 }

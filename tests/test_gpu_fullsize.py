@@ -1,0 +1,112 @@
+"""Full-size BASELINE workloads on the GPU, checked by size-independent
+properties and by oracle rows (SURVEY.md 8(c) "partial oracle for huge
+configs": the reference's slab mechanism, parallel.py:161-171 --
+outer = all elements, inner = a sample -- gives exact rows for DOFs whose
+elements are all in the sample).
+
+  * pair counts equal SURVEY.md 8(a)'s reference candidate counts;
+  * A 1 = 0 (test_assembly.py:49-55), via the device matvec;
+  * the pre-symmetrisation asymmetry is a small fraction of ||A||_inf;
+  * rows of seeded interior DOFs equal the oracle's (1e-10 relative);
+plus edge cases of the C-ABI entry: empty inner sets, empty outer masks,
+L_min = L_max = 1, and event counts monotone in L_max
+(test_assembly.py:136-142).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import Golden, rel_frob
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+def _sample_rows(mesh, space, kp, cfg, A, n_rows=4, seed=0):
+    """Oracle rows of seeded free DOFs vs the device values of A."""
+    import oracle
+    from paper_2101_08825_b200.assembly import HostPattern
+    rng = np.random.default_rng(seed)
+    rows = rng.choice(space.free, n_rows, replace=False)
+    inner = np.nonzero(np.isin(space.element_dofs, rows).any(axis=1))[0]
+    mask = np.zeros(mesh.n_elements, np.uint8)
+    mask[inner] = 1
+    R = HostPattern.for_space(mesh, space, kp, cfg)
+    oracle.run_general(mesh, space, kp, cfg, R, inner_mask=mask)
+    R.vals *= 2.0
+    dv = A.vals_device
+    for r in rows:
+        a, b = int(A.rowptr[r]), int(A.rowptr[r + 1])
+        got = dv[a:b].cpu().numpy()
+        err = rel_frob(got, R.vals[a:b])
+        assert err <= TOL, (int(r), err)
+    return rows
+
+
+def _row_sums(A):
+    import torch
+    from paper_2101_08825_b200 import _native as N
+    from paper_2101_08825_b200.assembly import C_byref
+    one = torch.ones(A.n, dtype=torch.float64, device=A.vals_device.device)
+    y = torch.empty_like(one)
+    N.check(N.lib().mf_matvec(C_byref(A._pattern_struct()),
+                              N.ptr(A.vals_device), N.ptr(one), N.ptr(y),
+                              N.stream_ptr()), "mf_matvec")
+    return float(y.abs().max())
+
+
+@pytest.mark.parametrize("name,pairs", [("R4", 1382469544),
+                                        ("R3-16h", 1414361664),
+                                        ("R2", None)])
+def test_full_size_properties(name, pairs):
+    import bench
+    from paper_2101_08825_b200 import _native as N
+    from paper_2101_08825_b200 import assemble
+    mesh, space, kp, cfg = bench.build_problem(name)
+    A = assemble(mesh, space, kp, cfg, keep_on_device=True)
+    if pairs is not None:
+        assert int(A.counters[N.CNT_PAIRS]) == pairs
+    nrm = A.norm_inf()
+    assert _row_sums(A) <= 1e-10 * nrm
+    assert A.presym_asymmetry <= 1e-2 * nrm
+    rows = _sample_rows(mesh, space, kp, cfg, A)
+    print(f"{name}: events={A.events} pairs={A.counters[N.CNT_PAIRS]} "
+          f"|A|inf={nrm:.4e} asym={A.presym_asymmetry:.3e} rows={rows}")
+
+
+def test_empty_inner_and_outer_sets():
+    import torch
+    from paper_2101_08825_b200 import _native as N
+    from paper_2101_08825_b200.assembly import AssemblyContext
+    from paper_2101_08825_b200.device import ColorPlan
+    g = Golden("tri_p1_lmax3")
+    mesh, space, kp, cfg = g.build()
+    ctx = AssemblyContext(mesh, space, kp, cfg)
+    A = ctx.new_matrix()
+    # no inner elements: a valid no-op
+    plan = ColorPlan(mesh, np.zeros(0, np.int64), ctx.device)
+    cnt = ctx.run(A, plan=plan)
+    assert int(cnt.sum()) == 0 and float(A._dvals.abs().max()) == 0.0
+    # no outer elements: every pair is masked out
+    cnt = ctx.run(A, outer_mask=np.zeros(mesh.n_elements, np.uint8),
+                  inner_ids=np.arange(mesh.n_elements))
+    assert int(cnt[N.CNT_PAIRS]) == 0
+    assert float(A._dvals.abs().max()) == 0.0
+    torch.cuda.synchronize()
+
+
+def test_single_level_and_events_monotone():
+    import oracle
+    from paper_2101_08825_b200 import AssemblyConfig, assemble
+    g = Golden("quad_q1_lmax3")
+    mesh, space, kp, _ = g.build()
+    prev = -1
+    for lmax in (1, 2, 3, 4):
+        cfg = AssemblyConfig(L_min=1, L_max=lmax, strategy="general")
+        A = assemble(mesh, space, kp, cfg)
+        R = oracle.assemble_general(mesh, space, kp, cfg)
+        assert A.events == R.events
+        assert rel_frob(A.vals, R.vals) <= TOL
+        assert A.events >= prev
+        prev = A.events
