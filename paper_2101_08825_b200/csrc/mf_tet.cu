@@ -216,12 +216,14 @@ enum : int { ACT_NONE = 0, ACT_SPLIT = 1, ACT_UPPER = 2, ACT_PLAT = 3,
 // folds A22.  Warps are independent (no block barrier after the start), so
 // the short planes at |dz| ~ R do not idle behind the long central ones.
 constexpr int kTetWarps = kTetThreads / 32;
+// blocks per SM: 3 for tet1/tet4 (<= 168 registers, small spill, measured
+// R4-tet 21.7 -> 20.5 s), 2 for tet11 (its V[11][4] would spill heavily)
 #ifndef MF_TET_MINB
-#define MF_TET_MINB 2
+#define MF_TET_MINB(NQ1) ((NQ1) > 4 ? 2 : 3)
 #endif
 
 template <int NQO, int NQ1>
-__global__ void __launch_bounds__(32 * kTetWarps, MF_TET_MINB)
+__global__ void __launch_bounds__(32 * kTetWarps, MF_TET_MINB(NQ1))
     k_tet(AsmParams P, int pass, double *gscr) {
   __shared__ double s_phiw[NQ1][4];
   __shared__ double s_opts[3 * NQO], s_ow[NQO];
