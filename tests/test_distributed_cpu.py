@@ -28,6 +28,13 @@ def _free_port():
     return p
 
 
+def _golden(name):
+    if name.startswith("delaunay_"):
+        from test_delaunay import DGolden     # unstructured (BASELINE #2)
+        return DGolden(name)
+    return Golden(name)
+
+
 def _worker(rank, world, port, name, out_q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -37,7 +44,7 @@ def _worker(rank, world, port, name, out_q):
         from paper_2101_08825_b200.assembly import HostPattern
         from paper_2101_08825_b200.parallel import (SlabPlan, exchange_interfaces,
                                                     gather_rows, slab_layers)
-        g = Golden(name)
+        g = _golden(name)
         mesh, space, kp, cfg = g.build()
         layers = slab_layers(mesh, world)
         A = HostPattern.for_space(mesh, space, kp, cfg)
@@ -62,10 +69,14 @@ def _worker(rank, world, port, name, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name", ["hex_q1_gl3", "tri_p1_lmax3",
-                                  "quad_q2_lmax2"])
-def test_slab_exchange_and_gather_gloo(name, oracle_lib):
-    world = 2
+@pytest.mark.parametrize("name,world", [("hex_q1_gl3", 2),
+                                        ("tri_p1_lmax3", 2),
+                                        ("quad_q2_lmax2", 2),
+                                        ("delaunay_tri6", 2),
+                                        ("delaunay_tri6", 3)])
+def test_slab_exchange_and_gather_gloo(name, world, oracle_lib):
+    """Delaunay slabs share dof_spill = 2 lattice planes per interface
+    (their vertices sit up to two planes above the element's bin row)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -77,7 +88,7 @@ def test_slab_exchange_and_gather_gloo(name, oracle_lib):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    g = Golden(name)
+    g = _golden(name)
     assert events == int(g["events"])
     assert rel_frob(vals, g["vals"]) <= 1e-14
     assert layers[0][0] == 0 and layers[-1][1] > layers[0][1]

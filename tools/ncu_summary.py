@@ -68,3 +68,27 @@ if __name__ == "__main__":
     rep = sys.argv[1]
     details(rep)
     sass(rep)
+
+
+def by_line(rep, top=30):
+    """Top CUDA source lines by stall samples and thread instructions."""
+    out = run([rep, "--page", "source", "--csv", "--print-source",
+               "cuda,sass"])
+    rows = list(csv.reader(io.StringIO(out)))
+    h = None
+    agg = []
+    for r in rows:
+        if r and r[0] == "Line No":
+            h = r
+            continue
+        if h is None or not r or not r[0].strip():
+            continue
+        try:
+            agg.append((int(r[4]), int(r[8]), r[0], r[1][:80]))
+        except (ValueError, IndexError):
+            continue
+    tot_s = sum(a[0] for a in agg) or 1
+    tot_t = sum(a[1] for a in agg) or 1
+    for s, t, ln, src in sorted(agg, reverse=True)[:top]:
+        print(f"  {100 * s / tot_s:5.1f}% stall {100 * t / tot_t:5.1f}% "
+              f"thr-inst  L{ln:5s} {src}")
