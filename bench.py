@@ -74,6 +74,10 @@ CONFIGS = {
                   2, "tet11"),
     "R5-tet-small": (3, ((0.0, 0.25),) * 3, 1 / 64, 4 / 64, 1 / 256, 2.0,
                      "tet", 2, "tet11"),
+    # BASELINE config #5 at full size on one GPU: 128^3 cubes (+5 Gamma
+    # rings) x 6 tets = 15.8M tets, ~1.3e11 pairs, 47 GB matrix
+    "R5-tet": (3, ((0.0, 1.0),) * 3, 1 / 128, 4 / 128, 1 / 512, 2.0, "tet",
+               2, "tet11"),
     # BASELINE config #2: unstructured Delaunay P1 mesh of ~200k seeded
     # jittered points (400^2 Omega lattice + 21 Gamma rings = 442^2 =
     # 195,364 vertices), delta = 0.05, eps = h/2, 6-point rule, L_max 3
@@ -83,7 +87,7 @@ CONFIGS = {
                  "delaunay", 3, "tri6"),
 }
 # vertex jitter (fraction of h, seeded) per workload (tet meshes only)
-JITTER = {"R5-tet-64": 0.1, "R5-tet-small": 0.1, "R2": 0.3,
+JITTER = {"R5-tet-64": 0.1, "R5-tet-small": 0.1, "R5-tet": 0.1, "R2": 0.3,
           "R2-small": 0.3}
 
 METRIC = "interacting element-pairs/sec (full nonlocal stiffness assembly)"

@@ -17,6 +17,7 @@ CPU fallback: without the CUDA library every device call raises.
 """
 
 import math
+import os
 
 import numpy as np
 
@@ -585,15 +586,22 @@ class AssemblyContext:
         import torch
         from . import _native as N
         from .device import ColorPlan, HostStager
-        from .parallel import pair_counts, slab_layers
+        from .parallel import pair_counts, slab_layers, slab_layers_fracs
         mesh, space = self.mesh, self.space
         axis = mesh.dim - 1
         nl = int(mesh.grid_ncells[axis])
-        if nslabs is None:
-            # ~2 GB of values per range keeps the exposed tail copy short
-            nslabs = int(max(1, min(8, nl // 4, -(-A.nnz * 8 // 2**31))))
         work = pair_counts(mesh, self.params, self.dmesh)
-        layers = slab_layers(mesh, nslabs, work)
+        fr = os.environ.get("MF_STREAM_FRACS")
+        if nslabs is None and fr:
+            layers = slab_layers_fracs(mesh, [float(x) for x in
+                                              fr.split(",")], work)
+        else:
+            if nslabs is None:
+                # ~2 GB of values per range keeps the exposed tail copy
+                # short
+                nslabs = int(max(1, min(8, nl // 4,
+                                        -(-A.nnz * 8 // 2**31))))
+            layers = slab_layers(mesh, nslabs, work)
         plan = ColorPlan(mesh, None, self.device, work=work, layers=layers)
         gather = strategy == "blocked" and space.degree == 1
         counters = torch.zeros(N.MF_NCOUNTERS, dtype=torch.int64,

@@ -63,6 +63,10 @@ cudaError_t mf_launch_load(const MfMesh &, const int32_t *, int64_t,
                            const double *, const double *, const double *,
                            int, int, double *, cudaStream_t);
 
+#ifndef MF_KEEP_POOL
+#define MF_KEEP_POOL 0
+#endif
+
 namespace {
 
 thread_local std::string g_err;
@@ -299,6 +303,22 @@ int mf_general_core(const MfMesh *mesh, const MfRules *rules,
       nmax = std::max<int64_t>(nmax, color_ptr[c + 1] - color_ptr[c]);
     const size_t nd = tet ? mf_tet_scratch_doubles(P, nmax)
                           : mf_tri_u_scratch_doubles(P, nmax);
+#if MF_KEEP_POOL
+    {
+      // keep freed scratch in the device's default pool across calls
+      // (release threshold 0 would unmap and remap it at every
+      // synchronisation); per-device setting, idempotent
+      int dev = 0;
+      cudaMemPool_t pool;
+      if (cudaGetDevice(&dev) == cudaSuccess &&
+          cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold,
+                                &keep);
+      }
+      cudaGetLastError();
+    }
+#endif
     double *gscr = nullptr;
     cudaError_t e = cudaMallocAsync(&gscr, sizeof(double) * nd, s);
     if (e != cudaSuccess) return cuda_status(e, "mf_general_core scratch");

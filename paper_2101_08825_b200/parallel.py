@@ -198,6 +198,26 @@ def slab_layers(mesh, world, weights=None):
     return [(cuts[r], cuts[r + 1]) for r in range(world)]
 
 
+def slab_layers_fracs(mesh, fracs, weights=None):
+    """Contiguous top-axis layer ranges whose cumulative work reaches the
+    given fractions (ascending, last = 1.0), at least one layer each."""
+    axis = mesh.dim - 1
+    layer = mesh.elem_cell[:, axis].astype(np.int64)
+    nl = int(mesh.grid_ncells[axis])
+    w = np.bincount(layer, weights=weights, minlength=nl).astype(float)
+    cum = np.cumsum(w)
+    total = cum[-1] if cum[-1] > 0 else 1.0
+    cuts = [0]
+    k = len(fracs)
+    for r, f in enumerate(fracs[:-1], start=1):
+        c = int(np.searchsorted(cum, total * f, side="left")) + 1
+        c = max(c, cuts[-1] + 1)
+        c = min(c, nl - (k - r))
+        cuts.append(c)
+    cuts.append(nl)
+    return [(cuts[r], cuts[r + 1]) for r in range(k)]
+
+
 class SlabPlan:
     """Rows / value ranges of one rank's slab on the implicit pattern."""
 
