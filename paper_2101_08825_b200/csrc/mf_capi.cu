@@ -64,7 +64,7 @@ cudaError_t mf_launch_load(const MfMesh &, const int32_t *, int64_t,
                            int, int, double *, cudaStream_t);
 
 #ifndef MF_KEEP_POOL
-#define MF_KEEP_POOL 0
+#define MF_KEEP_POOL 1
 #endif
 
 namespace {
