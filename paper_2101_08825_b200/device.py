@@ -199,6 +199,17 @@ class HostStager:
         self.stream = torch.cuda.Stream(device=self.device)
         self.threads = threads
 
+    def prefault(self, host, chunk=1 << 24):
+        """Touch every page of `host` (zero fill) with the thread pool."""
+        from concurrent.futures import ThreadPoolExecutor
+        n = host.shape[0]
+
+        def touch(a):
+            host[a:a + chunk].fill(0.0)
+
+        with ThreadPoolExecutor(max_workers=self.threads) as pool:
+            list(pool.map(touch, range(0, n, chunk)))
+
     def run(self, src, host, ranges):
         """Copy src[a:b] -> host[a:b] for each (event, a, b), in order."""
         import torch
