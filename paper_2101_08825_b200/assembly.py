@@ -596,10 +596,17 @@ class AssemblyContext:
             layers = slab_layers(mesh, nslabs, work)
         else:
             # few ranges (every range adds a launch tail per colour), the
-            # last one small (its copy is exposed): measured on R4, 8 equal
-            # ranges 8.82 s -> these 4 ranges ~8.1 s end to end
-            fracs = ([float(x) for x in fr.split(",")] if fr else
-                     [0.6, 0.9, 0.97, 1.0] if A.nnz * 8 > 2**31 else [1.0])
+            # last one small (its copy is exposed): measured on R4 (16 GB),
+            # 8 equal ranges 8.82 s -> these 4 ranges 8.27 s end to end;
+            # mid-size matrices keep ~2 GB equal ranges (R2: 1.79 s with 3,
+            # 2.03 s with the 4 uneven ones)
+            if fr:
+                fracs = [float(x) for x in fr.split(",")]
+            elif A.nnz * 8 > 2**33:
+                fracs = [0.6, 0.9, 0.97, 1.0]
+            else:
+                k = int(max(1, min(8, -(-A.nnz * 8 // 2**31))))
+                fracs = [(i + 1) / k for i in range(k)]
             fracs = fracs[-max(1, min(len(fracs), nl // 4)):]
             fracs[-1] = 1.0
             layers = slab_layers_fracs(mesh, fracs, work)
