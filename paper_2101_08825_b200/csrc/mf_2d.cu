@@ -26,6 +26,9 @@ constexpr int kMaxLevels = 6;
 #ifndef MF_TRI_QUEUE
 #define MF_TRI_QUEUE 1
 #endif
+#ifndef MF_TRI_WALK
+#define MF_TRI_WALK 1
+#endif
 #ifndef MF_TRI_U_FLAT
 #define MF_TRI_U_FLAT 1
 #endif
@@ -913,6 +916,38 @@ MF_DEV void lattice_split(int d, int NX, float inv_nx, int &gx, int &gy) {
 #define MF_TRIQ_MINB 3  // 168 registers: R2 kernels 3.5% faster than 2
 #endif
 
+// Algorithm-1 decision for one sub-triangle at level L (shortcuts on):
+// _kernels.py:224-251 plus the dead / plateau proofs at L_max
+MF_DEV int tri_classify(const AsmParams &P, const double *g, int L,
+                        const double *ilo, const double *ihi) {
+  double slo[2], shi[2];
+  sub_bbox<1>(g, slo, shi);
+  if (L < P.L_min) return ACT_SPLIT;
+  if (L == P.L_max) {
+    if (!(aprx_min_d<2>(slo, shi, ilo, ihi) < P.dpe)) return ACT_NONE;
+    if (box_dead<2>(P, slo, shi, ilo, ihi)) return ACT_DEAD;
+    if (aprx_max_lt_dme(P, aprx_max_sq<2>(slo, shi, ilo, ihi)))
+      return ACT_PLAT;
+    return ACT_FULL;
+  }
+  if (aprx_max_lt_dme(P, aprx_max_sq<2>(slo, shi, ilo, ihi)))
+    return ACT_UPPER;
+  if (aprx_min_d<2>(slo, shi, ilo, ihi) < P.dpe) return ACT_SPLIT;
+  return ACT_NONE;
+}
+
+MF_DEV void outer_map(const double *c, OuterTri &O) {
+  const double e10 = c[2] - c[0], e11 = c[3] - c[1];
+  const double e20 = c[4] - c[0], e21 = c[5] - c[1];
+  const double idet = rcp_fast(e10 * e21 - e11 * e20);
+  O.v0[0] = c[0];
+  O.v0[1] = c[1];
+  O.inv[0] = e21 * idet;
+  O.inv[1] = -e20 * idet;
+  O.inv[2] = -e11 * idet;
+  O.inv[3] = e10 * idet;
+}
+
 template <int NQO, int NQ1>
 __global__ void __launch_bounds__(32 * kTriQWarps, MF_TRIQ_MINB)
     k_tri_q(AsmParams P, int cls, double *gscr) {
@@ -1008,6 +1043,7 @@ __global__ void __launch_bounds__(32 * kTriQWarps, MF_TRIQ_MINB)
     unsigned ev = 0;
     double SP[NL] = {0.0, 0.0, 0.0};
     bool live = false;
+    bool walk = false;
     if (have) {
       c_pairs++;
       const int64_t *ldofs = M.elem_dofs + l * M.nloc_max;
@@ -1022,6 +1058,137 @@ __global__ void __launch_bounds__(32 * kTriQWarps, MF_TRIQ_MINB)
           asm volatile("prefetch.global.L2 [%0];" ::"l"(P.vals + sl));
         }
       }
+#if MF_TRI_WALK
+      // root only; deeper levels are walked by the whole warp below
+      double root[6];
+      {
+        const double *c = M.elem_coords + l * M.nv_max * 2;
+#pragma unroll
+        for (int u = 0; u < 6; u++) {
+          root[u] = c[u];
+          s_root[w][u][lane] = c[u];
+        }
+      }
+      const int act = tri_classify(P, root, 1, ilo, ihi);
+      if (act >= ACT_UPPER) {
+        ev++;
+        if (act == ACT_UPPER) c_up++;
+        if (act == ACT_DEAD) c_dead++;
+        if (act == ACT_PLAT) c_pl++;
+        if (act == ACT_FULL) {
+          c_full++;
+          fmask = 1u;
+        }
+        if (act == ACT_PLAT || act == ACT_UPPER) {
+          live = true;
+          OuterTri OT;
+          outer_map(root, OT);
+          tri_plateau<NQO>(P, root, OT, s_opts, s_ow, SP);
+        }
+      }
+      walk = act == ACT_SPLIT;
+    }
+    // ---- phase W: the split pairs' sub-triangles, walked by the warp ----
+    // A pair split at the root has 4^(L_max-1) <= 16 leaves; lane group g
+    // (nper lanes) takes owner pair g of this round and lane s of the group
+    // evaluates leaf s: its level-2 parent (the group's 4 lanes of one
+    // parent agree on its class; lane k = 0 integrates a parent plateau
+    // event), then the leaf itself.  Full leaves become the owner's fmask
+    // bits, plateau contributions are reduced over the group (fixed
+    // shuffle tree) and added to the owner's SP -- deterministic.
+    unsigned wmask = __ballot_sync(0xffffffffu, walk);
+    if (wmask) {
+      const int nper = 1 << nleaf_bits;  // 4 (L_max 2) or 16 (L_max 3)
+      const int grp = lane / nper, sl = lane % nper;
+      double(*s_ib)[32] = s_res[w];         // owner inner boxes (4 rows)
+      double(*s_sp)[32] = s_res[w] + 4;     // owner plateau sums (3 rows)
+      s_ib[0][lane] = ilo[0];
+      s_ib[1][lane] = ilo[1];
+      s_ib[2][lane] = ihi[0];
+      s_ib[3][lane] = ihi[1];
+      __syncwarp();
+      while (wmask) {
+        const int cnt = __popc(wmask);
+        const int o = grp < cnt ? (int)__fns(wmask, 0, grp + 1) : -1;
+        double spi[NL] = {0.0, 0.0, 0.0};
+        bool fl = false, lv = false;
+        if (o >= 0) {
+          double rt[6], blo[2], bhi[2];
+#pragma unroll
+          for (int u = 0; u < 6; u++) rt[u] = s_root[w][u][o];
+          blo[0] = s_ib[0][o];
+          blo[1] = s_ib[1][o];
+          bhi[0] = s_ib[2][o];
+          bhi[1] = s_ib[3][o];
+          OuterTri O;
+          outer_map(rt, O);
+          double g2[6];
+          make_child<1>(rt, nleaf_bits == 2 ? sl : (sl >> 2), g2);
+          int a = tri_classify(P, g2, 2, blo, bhi);
+          if (nleaf_bits == 4) {
+            if (a == ACT_UPPER) {
+              if ((sl & 3) == 0) {
+                c_ev++;
+                c_up++;
+                lv = true;
+                tri_plateau<NQO>(P, g2, O, s_opts, s_ow, spi);
+              }
+              a = ACT_NONE;
+            } else if (a == ACT_SPLIT) {
+              double g3[6];
+              make_child<1>(g2, sl & 3, g3);
+#pragma unroll
+              for (int u = 0; u < 6; u++) g2[u] = g3[u];
+              a = tri_classify(P, g2, 3, blo, bhi);
+            } else {
+              a = ACT_NONE;
+            }
+          }
+          // a: the leaf's class at L_max (or ACT_NONE)
+          if (a >= ACT_UPPER) {
+            c_ev++;
+            if (a == ACT_DEAD) c_dead++;
+            if (a == ACT_PLAT) {
+              c_pl++;
+              lv = true;
+              tri_plateau<NQO>(P, g2, O, s_opts, s_ow, spi);
+            }
+            if (a == ACT_FULL) {
+              c_full++;
+              fl = true;
+            }
+          }
+        }
+        const unsigned fb = __ballot_sync(0xffffffffu, fl);
+        const unsigned lb = __ballot_sync(0xffffffffu, fl || lv);
+        for (int d = nper >> 1; d >= 1; d >>= 1)
+#pragma unroll
+          for (int k = 0; k < NL; k++)
+            spi[k] += __shfl_xor_sync(0xffffffffu, spi[k], d);
+        if (o >= 0 && sl == 0) {
+          const unsigned gm = (1u << nper) - 1u;
+          const unsigned fg = (fb >> (grp * nper)) & gm;
+          const unsigned lg = (lb >> (grp * nper)) & gm;
+          s_mask[w][o] = fg | (lg ? 0x80000000u : 0u);
+#pragma unroll
+          for (int k = 0; k < NL; k++) s_sp[k][o] = spi[k];
+        }
+        for (int k = 0; k < 32 / nper && wmask; k++) wmask &= wmask - 1;
+      }
+      __syncwarp();
+      if (walk) {
+        const unsigned v = s_mask[w][lane];
+        fmask = v & 0xffffu;
+        live |= (v >> 31) != 0u;
+#pragma unroll
+        for (int k = 0; k < NL; k++) SP[k] += s_sp[k][lane];
+      }
+      __syncwarp();
+    }
+    if (have) {
+      live |= fmask != 0;
+    }
+#else
       OuterTri OT;
       double geo[kMaxLevels + 1][6];
       {
@@ -1101,6 +1268,7 @@ __global__ void __launch_bounds__(32 * kTriQWarps, MF_TRIQ_MINB)
       }
       live |= fmask != 0;
     }
+#endif
     // ---- phase B: the warp's full events, 32 per round, converged ----
     const int cnt = __popc(fmask);
     int off = cnt;
