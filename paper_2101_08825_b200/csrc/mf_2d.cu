@@ -26,12 +26,6 @@ constexpr int kMaxLevels = 6;
 #ifndef MF_TRI_QUEUE
 #define MF_TRI_QUEUE 1
 #endif
-#ifndef MF_TRI_WALK
-#define MF_TRI_WALK 1
-#endif
-#ifndef MF_TRI_U_FLAT
-#define MF_TRI_U_FLAT 1
-#endif
 #ifndef MF_2D_MINB
 #define MF_2D_MINB 2
 #endif
@@ -684,21 +678,10 @@ __global__ void __launch_bounds__(128, MF_2D_MINB)
       rylo[i] = max(gy - K, 0);
       rowbase[i] = P.pat.rowptr[d];
     }
-#if MF_TRI_U_FLAT
     const int64_t l0 = M.cell_ptr[(int64_t)y2 * M.ncx + max(cx - Rs, 0)];
     const int64_t l1 =
         M.cell_ptr[(int64_t)y2 * M.ncx + min(cx + Rs, M.ncx - 1) + 1];
     for (int64_t l = l0; l < l1; l++) {
-#else
-    // walk the row by relative bin offset dx, so the lanes of a warp visit
-    // partners at the same offset at the same time (similar pair geometry,
-    // similar Algorithm-1 paths)
-    for (int dx = -Rs; dx <= Rs; dx++) {
-      const int x2 = cx + dx;
-      if (x2 < 0 || x2 >= M.ncx) continue;
-      const int64_t c2 = (int64_t)y2 * M.ncx + x2;
-      for (int64_t l = M.cell_ptr[c2]; l < M.cell_ptr[c2 + 1]; l++) {
-#endif
       if (!P.outer_mask[l]) continue;
       if (!(elem_gap<2>(M.elem_lo, M.elem_hi, l, m) < P.dpe)) continue;
       c_pairs++;
@@ -827,9 +810,6 @@ __global__ void __launch_bounds__(128, MF_2D_MINB)
           G[q] += sg;
         }
       }
-#if !MF_TRI_U_FLAT
-      }
-#endif
     }
   }
   double *gp = gscr + ((int64_t)pidx * P.n_inner + t) * NQ1;
@@ -1058,7 +1038,6 @@ __global__ void __launch_bounds__(32 * kTriQWarps, MF_TRIQ_MINB)
           asm volatile("prefetch.global.L2 [%0];" ::"l"(P.vals + sl));
         }
       }
-#if MF_TRI_WALK
       // root only; deeper levels are walked by the whole warp below
       double root[6];
       {
@@ -1188,87 +1167,6 @@ __global__ void __launch_bounds__(32 * kTriQWarps, MF_TRIQ_MINB)
     if (have) {
       live |= fmask != 0;
     }
-#else
-      OuterTri OT;
-      double geo[kMaxLevels + 1][6];
-      {
-        const double *c = M.elem_coords + l * M.nv_max * 2;
-#pragma unroll
-        for (int u = 0; u < 6; u++) {
-          geo[1][u] = c[u];
-          s_root[w][u][lane] = c[u];
-        }
-        const double e10 = c[2] - c[0], e11 = c[3] - c[1];
-        const double e20 = c[4] - c[0], e21 = c[5] - c[1];
-        const double idet = rcp_fast(e10 * e21 - e11 * e20);
-        OT.v0[0] = c[0];
-        OT.v0[1] = c[1];
-        OT.inv[0] = e21 * idet;
-        OT.inv[1] = -e20 * idet;
-        OT.inv[2] = -e11 * idet;
-        OT.inv[3] = e10 * idet;
-      }
-      int child[kMaxLevels + 1];
-      int L = 1;
-      for (;;) {
-        double slo[2], shi[2];
-        sub_bbox<1>(geo[L], slo, shi);
-        int act = ACT_NONE;
-        if (L < P.L_min) {
-          act = ACT_SPLIT;
-        } else if (L == P.L_max) {
-          if (aprx_min_d<2>(slo, shi, ilo, ihi) < P.dpe) {
-            if (box_dead<2>(P, slo, shi, ilo, ihi))
-              act = ACT_DEAD;
-            else if (aprx_max_lt_dme(P, aprx_max_sq<2>(slo, shi, ilo, ihi)))
-              act = ACT_PLAT;
-            else
-              act = ACT_FULL;
-          }
-        } else if (aprx_max_lt_dme(P, aprx_max_sq<2>(slo, shi, ilo, ihi))) {
-          act = ACT_UPPER;
-        } else if (aprx_min_d<2>(slo, shi, ilo, ihi) < P.dpe) {
-          act = ACT_SPLIT;
-        }
-        if (act >= ACT_UPPER) {
-          ev++;
-          if (act == ACT_UPPER) c_up++;
-          if (act == ACT_DEAD) c_dead++;
-          if (act == ACT_PLAT) c_pl++;
-          if (act == ACT_FULL) {
-            c_full++;
-            int leaf = 0;
-            for (int k = 2; k <= L; k++) leaf = 4 * leaf + child[k];
-            fmask |= 1u << leaf;
-          }
-          if (act == ACT_PLAT || act == ACT_UPPER) {
-            live = true;
-            tri_plateau<NQO>(P, geo[L], OT, s_opts, s_ow, SP);
-          }
-        }
-        if (act == ACT_SPLIT) {
-          ++L;
-          child[L] = 0;
-          make_child<1>(geo[L - 1], 0, geo[L]);
-          continue;
-        }
-        bool done = false;
-        for (;;) {
-          if (L == 1) {
-            done = true;
-            break;
-          }
-          if (++child[L] < 4) {
-            make_child<1>(geo[L - 1], child[L], geo[L]);
-            break;
-          }
-          --L;
-        }
-        if (done) break;
-      }
-      live |= fmask != 0;
-    }
-#endif
     // ---- phase B: the warp's full events, 32 per round, converged ----
     const int cnt = __popc(fmask);
     int off = cnt;
