@@ -12,8 +12,9 @@ so this element is pinned to reference arithmetic:
     conforming, oriented, region-pure, emax <= 2h, the colouring is
     vertex-disjoint; the C oracle reproduces the reference candidate lists,
     events and values bit for bit;
-  * GPU (through the C-ABI): the row-split kernel k_tri_u and the generic
-    kernel give identical events and values within 1e-10 relative
+  * GPU (through the C-ABI): the warp-cooperative kernel k_tri_q, the
+    inline row-split kernel k_tri_u (no-shortcut / eps = 0 paths) and the
+    generic kernel give identical events and values within 1e-10 relative
     Frobenius norm of the reference, bit-identical run to run; partition
     invariance and the multi-GPU slab emulation; A 1 = 0 and oracle parity
     on a larger mesh; load vector and solve.
@@ -319,3 +320,20 @@ def test_gpu_rhs_and_solve():
     assert np.abs(u[space.free] - ref).max() <= 1e-8 * max(
         1.0, np.abs(ref).max())
     assert l2_error(space, u, u_ex) <= 5e-3
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("lmin,lmax", [(1, 1), (1, 2), (2, 2), (3, 3)])
+def test_gpu_recursion_windows_vs_oracle(lmin, lmax, oracle_lib):
+    """Other [L_min, L_max] windows on the fixture mesh (the k_tri_q walk
+    has separate code for L_max 1/2/3 and forced splits), against the
+    oracle, which reproduces the reference core bit for bit on the
+    fixtures (test_oracle_matches_reference_core)."""
+    from paper_2101_08825_b200 import AssemblyConfig, assemble
+    g, mesh, space, kp, _ = built("delaunay_tri6")
+    cfg = AssemblyConfig(L_min=lmin, L_max=lmax, outer_rule="tri6",
+                         inner_rule="tri6", strategy="general")
+    A = assemble(mesh, space, kp, cfg)
+    R = oracle_lib.assemble_general(mesh, space, kp, cfg)
+    assert A.events == R.events
+    assert rel_frob(A.vals, R.vals) <= TOL
