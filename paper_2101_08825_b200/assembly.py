@@ -600,16 +600,21 @@ class AssemblyContext:
             # 8 equal ranges 8.82 s -> these 4 ranges 8.27 s end to end;
             # mid-size matrices keep ~2 GB equal ranges (R2: 1.79 s with 3,
             # 2.03 s with the 4 uneven ones)
+            # cuts are fractions of the top-axis LAYERS (rows), not of the
+            # pair work: the time per pair varies across the domain, and
+            # what must be small is the byte count of the ranges that
+            # finish last (traced on R4: work-based cuts left 6.5 GB to
+            # copy after the kernels)
             if fr:
                 fracs = [float(x) for x in fr.split(",")]
             elif A.nnz * 8 > 2**33:
-                fracs = [0.6, 0.9, 0.97, 1.0]
+                fracs = [0.5, 0.8, 0.93, 1.0]
             else:
                 k = int(max(1, min(8, -(-A.nnz * 8 // 2**31))))
                 fracs = [(i + 1) / k for i in range(k)]
             fracs = fracs[-max(1, min(len(fracs), nl // 4)):]
             fracs[-1] = 1.0
-            layers = slab_layers_fracs(mesh, fracs, work)
+            layers = slab_layers_fracs(mesh, fracs, None)
         plan = ColorPlan(mesh, None, self.device, work=work, layers=layers)
         gather = strategy == "blocked" and space.degree == 1
         counters = torch.zeros(N.MF_NCOUNTERS, dtype=torch.int64,
@@ -789,6 +794,13 @@ class AssemblyContext:
         if self.config.symmetrize:
             N.check(N.lib().mf_symmetrize(C_byref(pat), N.ptr(A._dvals),
                                            N.stream_ptr()), "mf_symmetrize")
+        # wait on an event first: Event.synchronize releases the GIL, a
+        # blocking .cpu() does not, and the streamed host copies
+        # (run_streamed's worker threads) need it while the kernels run
+        # (tools/overlap_probe.py: 8 GB staged in 3.23 s vs 0.23 s)
+        done = torch.cuda.Event()
+        done.record(torch.cuda.current_stream(self.device))
+        done.synchronize()
         cnt = counters.cpu().numpy()
         A.counters = cnt
         A.events = int(cnt[N.CNT_EVENTS])

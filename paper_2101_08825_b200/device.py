@@ -214,10 +214,20 @@ class HostStager:
         """Copy src[a:b] -> host[a:b] for each (event, a, b), in order."""
         import torch
         from concurrent.futures import ThreadPoolExecutor
+        import os
+        import time
+        trace = os.environ.get("MF_STAGER_TRACE") == "1"
+        t0 = time.perf_counter()
         pending = [None] * self.NBUF     # host-copy futures per buffer
         k = 0
         with ThreadPoolExecutor(max_workers=self.threads) as pool:
-            for ev, a, b in ranges:
+            for ri, (ev, a, b) in enumerate(ranges):
+                if trace:
+                    tw = time.perf_counter()
+                    ev.synchronize()
+                    print(f"[stager] range {ri}: worker reached it at "
+                          f"{tw:.3f}, event done at {time.perf_counter():.3f}"
+                          f" ({(b - a) * 8 / 1e9:.2f} GB)", flush=True)
                 self.stream.wait_event(ev)
                 for c0 in range(a, b, self.CHUNK):
                     c1 = min(b, c0 + self.CHUNK)
@@ -247,3 +257,6 @@ class HostStager:
                 if fl is not None:
                     for f in fl:
                         f.result()
+        if trace:
+            print(f"[stager] started {t0:.3f}, all copies done at "
+                  f"{time.perf_counter():.3f}", flush=True)

@@ -35,6 +35,7 @@ for trial in range(3):
     t4 = time.perf_counter()          # launches queued, copies running
     ctx.finish(A, cnt)
     t5 = T()
+    print(f"  kernels+finish ended at {t5:.3f}", flush=True)
     ctx.join_streamed(A)
     t6 = T()
     print(f"{name} trial {trial}: context+upload {t1 - t0:.3f}s, "
