@@ -596,22 +596,22 @@ class AssemblyContext:
             layers = slab_layers(mesh, nslabs, work)
         else:
             # few ranges (every range adds a launch tail per colour), the
-            # last one small (its copy is exposed): measured on R4 (16 GB),
-            # 8 equal ranges 8.82 s -> these 4 ranges 8.27 s end to end;
-            # mid-size matrices keep ~2 GB equal ranges (R2: 1.79 s with 3,
-            # 2.03 s with the 4 uneven ones)
+            # last one small (its copy is exposed).
             # cuts are fractions of the top-axis LAYERS (rows), not of the
             # pair work: the time per pair varies across the domain, and
             # what must be small is the byte count of the ranges that
             # finish last (traced on R4: work-based cuts left 6.5 GB to
             # copy after the kernels)
+            # With the copies running during the kernels (finish waits on
+            # an event), two ranges suffice: R4 end to end 7.96 s with
+            # [0.5, 0.8, 0.93, 1] -> 7.78 s with [0.9, 1] (one launch tail
+            # per colour less, the last 10% of rows copied in ~45 ms).
             if fr:
                 fracs = [float(x) for x in fr.split(",")]
-            elif A.nnz * 8 > 2**33:
-                fracs = [0.5, 0.8, 0.93, 1.0]
+            elif A.nnz * 8 > 2**30:
+                fracs = [0.9, 1.0]
             else:
-                k = int(max(1, min(8, -(-A.nnz * 8 // 2**31))))
-                fracs = [(i + 1) / k for i in range(k)]
+                fracs = [1.0]
             fracs = fracs[-max(1, min(len(fracs), nl // 4)):]
             fracs[-1] = 1.0
             layers = slab_layers_fracs(mesh, fracs, None)
