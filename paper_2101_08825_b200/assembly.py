@@ -603,13 +603,18 @@ class AssemblyContext:
             # finish last (traced on R4: work-based cuts left 6.5 GB to
             # copy after the kernels)
             # With the copies running during the kernels (finish waits on
-            # an event), two ranges suffice: R4 end to end 7.96 s with
-            # [0.5, 0.8, 0.93, 1] -> 7.78 s with [0.9, 1] (one launch tail
-            # per colour less, the last 10% of rows copied in ~45 ms).
+            # an event), two ranges suffice.  Measured end to end: R4
+            # (16 GB) 7.96 s with [0.5, 0.8, 0.93, 1] -> 7.78 s with
+            # [0.9, 1]; R3-16h (3.2 GB) 0.90 s with [0.5, 1], 1.12 s with
+            # [0.75, 1], 1.18 s with [0.9, 1] (its thread-per-element
+            # launches pay a long per-thread tail on a thin range); R2 is
+            # indifferent (1.55 s).
             if fr:
                 fracs = [float(x) for x in fr.split(",")]
-            elif A.nnz * 8 > 2**30:
+            elif A.nnz * 8 > 2**33:
                 fracs = [0.9, 1.0]
+            elif A.nnz * 8 > 2**30:
+                fracs = [0.5, 1.0]
             else:
                 fracs = [1.0]
             fracs = fracs[-max(1, min(len(fracs), nl // 4)):]
