@@ -135,6 +135,9 @@ int mf_exclusive_scan(const int64_t *counts, int64_t n, int64_t *ptr,
 #define MF_FLAG_FORCE_GENERIC 1   /* bypass the specialised kernels */
 #define MF_FLAG_NO_SHORTCUTS 2    /* integrate proven-plateau/dead events
                                      point by point too */
+#define MF_FLAG_ELEMENT_THREADS 4 /* small structured P1 triangle meshes:
+                                     keep the thread-per-element kernel
+                                     instead of the row-split one */
 size_t mf_general_workspace_bytes(const MfMesh *mesh, const MfRules *rules,
                                   int64_t n_inner);
 int mf_general_core(const MfMesh *mesh, const MfRules *rules,

@@ -17,6 +17,7 @@ CNT_EVENTS, CNT_PAIRS, CNT_EV_UPPER, CNT_EV_PLATEAU, CNT_EV_DEAD, \
     CNT_EV_FULL = range(6)
 FLAG_FORCE_GENERIC = 1
 FLAG_NO_SHORTCUTS = 2
+FLAG_ELEMENT_THREADS = 4
 
 
 class MfMesh(C.Structure):

@@ -63,6 +63,9 @@ cudaError_t mf_launch_load(const MfMesh &, const int32_t *, int64_t,
                            const double *, const double *, const double *,
                            int, int, double *, cudaStream_t);
 
+#ifndef MF_SMALL_TRI_ELEMS
+#define MF_SMALL_TRI_ELEMS 65536
+#endif
 #ifndef MF_KEEP_POOL
 #define MF_KEEP_POOL 1
 #endif
@@ -293,6 +296,19 @@ int mf_general_core(const MfMesh *mesh, const MfRules *rules,
                 "1/4/11-point tet rules");
   if (mesh->layout != 0 && (mesh->layout != 1 || mesh->row_period < 2))
     return fail(MF_ERR_ARG, "bad mesh layout / row_period");
+  // Small structured P1 triangle meshes also take the row-split kernel:
+  // their DOFs are lattice ids and an element spans one cell row, so rows
+  // two apart share no vertex (row_period 2).  Thread per (element, row)
+  // gives 2R+1 times the parallelism of k_2d's thread per element, which
+  // leaves the GPU mostly idle below ~10^5 elements (R1: 3,200 elements).
+  if (mesh->layout == 0 && mesh->dim == 2 && mesh->kinds_present == 2 &&
+      mesh->degree == 1 && mesh->n_elem <= MF_SMALL_TRI_ELEMS &&
+      !(flags & MF_FLAG_ELEMENT_THREADS)) {
+    AsmParams Q = P;
+    Q.mesh.layout = 1;
+    Q.mesh.row_period = 2;
+    if (!force_generic && mf_tri_u_supported(Q)) P = Q;
+  }
   const bool tri_u = !tet && !force_generic && mf_tri_u_supported(P);
   if (tet || tri_u) {
     // row-split kernels (mf_tet.cu planes, mf_2d.cu k_tri_u bin rows):

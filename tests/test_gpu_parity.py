@@ -24,8 +24,9 @@ def _assemble(name, flags=0):
 
 
 @pytest.mark.parametrize("name", golden_names())
-@pytest.mark.parametrize("flags", [0, 1, 2], ids=["auto", "generic",
-                                                   "noshortcut"])
+@pytest.mark.parametrize("flags", [0, 1, 2, 4], ids=["auto", "generic",
+                                                      "noshortcut",
+                                                      "elemthreads"])
 def test_assemble_matches_reference(name, flags):
     g, A = _assemble(name, flags)
     assert np.array_equal(A.rowptr, g["rowptr"]) and A.K == int(g["K"])
