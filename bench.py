@@ -46,6 +46,10 @@ CONFIGS = {
     # name: (dim, omega, h, delta, eps, kappa, kind, L_max, rule)
     "R1": (2, ((0.0, 1.0),) * 2, 1 / 32, 0.1, 1 / 64, 1.0, "tri", 3,
            "default"),
+    # BASELINE config #1 as written: the 3-point triangle rule ("tri3";
+    # the reference maps every triangle preset to Dunavant-7)
+    "R1-tri3": (2, ((0.0, 1.0),) * 2, 1 / 32, 0.1, 1 / 64, 1.0, "tri", 3,
+                "tri3"),
     "R3-2h": (2, ((0.0, 1.0),) * 2, 1 / 512, 2 / 512, 1 / 1024, 1.0, "tri",
               3, "default"),
     "R3-4h": (2, ((0.0, 1.0),) * 2, 1 / 512, 4 / 512, 1 / 1024, 1.0, "tri",
@@ -133,8 +137,9 @@ def config_json(name, mesh, space, n_gpus, slab_info=None,
          "cells": list(mesh.grid_ncells), "elements": mesh.n_elements,
          "n_dofs": space.n_dofs, "fe_degree": 1, "h": h, "delta": delta,
          "eps": eps, "kappa": kappa, "L_max": lmax,
-         "rule": {"tri": "dunavant7", "delaunay": "dunavant6"}.get(kind,
-                                                                   rule),
+         "rule": ({"tri3": "strang3", "tri6": "dunavant6"}.get(rule,
+                                                               "dunavant7")
+                  if kind in ("tri", "delaunay") else rule),
          "parallelism": f"z-slab x{n_gpus}" if n_gpus > 1 else "single",
          "l2": "value array > L2 (rewritten every step)"}
     if slab_info:
@@ -247,7 +252,7 @@ def flop_model(name, counters):
         f_plat = 3 * no * 8 + 6 * no + 16
         f_pair = 2 * 2 * nq1 * 64 + 8 * nq1
     else:
-        nq1 = nq2 = 6 if rule == "tri6" else 7
+        nq1 = nq2 = {"tri6": 6, "tri3": 3}.get(rule, 7)
         nl = 3
         canon_ev = nq2 * nq1 * (3 * dim - 1 + 3) + 2 * nq2 * nq1 * nl \
             + 2 * nq2 * nl * nl

@@ -19,7 +19,7 @@ from .mesh import (BoundingBox, DelaunayMesh, Mesh, PartitionMap,
                    build_delaunay_mesh, build_mesh, partition_geometric,
                    refine)
 from .solver import SolveReport, solve
-from .quadrature import (QuadratureRule, dunavant6, dunavant7,
+from .quadrature import (QuadratureRule, dunavant6, dunavant7, strang3,
                          gauss_legendre_1d,
                          gauss_lobatto_1d, map_to_physical, rule_for_kind,
                          tensor_product)
@@ -31,7 +31,7 @@ __all__ = [
     "KernelParams", "Mesh",
     "NeighborSets", "PartitionMap", "QuadratureRule", "SparseMatrix",
     "aprx_max_dist", "aprx_min_dist", "assemble", "assemble_rhs",
-    "build_delaunay_mesh", "build_mesh", "dunavant6", "dunavant7",
+    "build_delaunay_mesh", "build_mesh", "dunavant6", "dunavant7", "strang3",
     "eval_basis", "eval_shape_functions", "gamma_eps", "gauss_legendre_1d",
     "gauss_lobatto_1d", "interpolate", "l2_error", "lifting",
     "map_to_physical", "mollifier", "neighbor_sets", "partition_geometric",

@@ -129,9 +129,11 @@ class PrepTables:
         # simplex slots ("tri_*"): triangles in 2D, tetrahedra in 3D (the
         # tet element is new; its rules are "default" = tet4, tet1/4/11)
         simplex = "tet" if mesh.kind == "tet" else "tri"
-        tri_preset = outer in ("tri6", "tri7") or inner in ("tri6", "tri7")
+        tri_presets = ("tri3", "tri6", "tri7")
+        tri_preset = outer in tri_presets or inner in tri_presets
         if tri_preset and mesh.kind != "tri":
-            raise ValueError("tri6/tri7 presets need a pure triangle mesh")
+            raise ValueError("tri3/tri6/tri7 presets need a pure triangle "
+                             "mesh")
         if simplex == "tet" or tri_preset:
             box_outer = box_inner = "gauss2"   # unused placeholders
         else:

@@ -1365,7 +1365,7 @@ bool mf_tri_u_supported(const AsmParams &P) {
     return false;
   if (P.pat.n >= (1 << 24)) return false;  // lattice_split range
   const int no = P.rules.nq_tri_out, ni = P.rules.nq_tri_in;
-  return (no == 6 || no == 7) && (ni == 6 || ni == 7);
+  return (no == 3 || no == 6 || no == 7) && (ni == 3 || ni == 6 || ni == 7);
 }
 
 size_t mf_tri_u_scratch_doubles(const AsmParams &P, int64_t n_colour_max) {
@@ -1376,9 +1376,11 @@ size_t mf_tri_u_scratch_doubles(const AsmParams &P, int64_t n_colour_max) {
 cudaError_t mf_launch_tri_u(const AsmParams &P, double *gscr,
                             cudaStream_t s) {
   const int no = P.rules.nq_tri_out, ni = P.rules.nq_tri_in;
-  if (no == 6 && ni == 6) return launch_tri_u<6, 6>(P, gscr, s);
-  if (no == 6 && ni == 7) return launch_tri_u<6, 7>(P, gscr, s);
-  if (no == 7 && ni == 6) return launch_tri_u<7, 6>(P, gscr, s);
-  if (no == 7 && ni == 7) return launch_tri_u<7, 7>(P, gscr, s);
+#define MF_TU(NO_, NI_) \
+  if (no == NO_ && ni == NI_) return launch_tri_u<NO_, NI_>(P, gscr, s);
+  MF_TU(3, 3) MF_TU(3, 6) MF_TU(3, 7)
+  MF_TU(6, 3) MF_TU(6, 6) MF_TU(6, 7)
+  MF_TU(7, 3) MF_TU(7, 6) MF_TU(7, 7)
+#undef MF_TU
   return cudaErrorNotSupported;
 }

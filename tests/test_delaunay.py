@@ -337,3 +337,40 @@ def test_gpu_recursion_windows_vs_oracle(lmin, lmax, oracle_lib):
     R = oracle_lib.assemble_general(mesh, space, kp, cfg)
     assert A.events == R.events
     assert rel_frob(A.vals, R.vals) <= TOL
+
+
+def test_strang3_exact_to_degree_2():
+    from paper_2101_08825_b200.quadrature import rule_for_kind, strang3
+    r = strang3()
+    P, w = r.ref_points, r.weights
+    for i in range(3):
+        for j in range(3 - i):
+            exact = math.factorial(i) * math.factorial(j) / math.factorial(
+                i + j + 2)
+            assert abs(float((w * P[:, 0] ** i * P[:, 1] ** j).sum())
+                       - exact) <= 1e-15
+    assert len(rule_for_kind("tri", "tri3")) == 3
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("flags", [0, 4])
+def test_gpu_tri3_rule_vs_oracle(flags, oracle_lib):
+    """The 3-point rule of BASELINE config #1 as written ("tri3"), on the
+    structured R1-type mesh (row-split kernel; flags 4 -> the generic
+    kernel, k_2d is Dunavant-7 only) and on a Delaunay mesh."""
+    from paper_2101_08825_b200 import (AssemblyConfig, FESpace, KernelParams,
+                                       assemble, build_mesh)
+    h = 1 / 32
+    kp = KernelParams(2, 0.1, h / 2)
+    cfg = AssemblyConfig(L_max=3, outer_rule="tri3", inner_rule="tri3",
+                         strategy="general")
+    mesh = build_mesh(2, ((0.0, 0.5), (0.0, 0.5)), h, kp.delta + kp.eps,
+                      "tri")
+    space = FESpace(mesh, 1)
+    A = assemble(mesh, space, kp, cfg, flags=flags)
+    R = oracle_lib.assemble_general(mesh, space, kp, cfg)
+    assert A.events == R.events and rel_frob(A.vals, R.vals) <= TOL
+    g, dmesh, dspace, dkp, _ = built("delaunay_tri6")
+    A = assemble(dmesh, dspace, dkp, cfg, flags=flags)
+    R = oracle_lib.assemble_general(dmesh, dspace, dkp, cfg)
+    assert A.events == R.events and rel_frob(A.vals, R.vals) <= TOL
