@@ -346,7 +346,10 @@ class SlabAssembler:
         self.local = torch.zeros(b - a, dtype=torch.float64,
                                  device=self.ctx.device)
         self.inner = self.plan.inner_ids(mesh)
-        self.color_plan = ColorPlan(mesh, self.inner, self.ctx.device)
+        # heaviest elements first inside each colour (as the single-GPU
+        # default plan) when the caller has the pair-count weights
+        self.color_plan = ColorPlan(mesh, self.inner, self.ctx.device,
+                                    work=weights)
         self.counters = torch.zeros(8, dtype=torch.int64,
                                     device=self.ctx.device)
 
