@@ -749,6 +749,10 @@ cudaError_t mf_launch_blocked_scatter(const AsmParams &P, int nproto, int R,
 // one constant per proto, computed once.
 namespace {
 
+#ifndef MF_BLOCKED_STENCIL
+#define MF_BLOCKED_STENCIL 1
+#endif
+
 struct Combo {
   int ax, ay, az, t, i;
 };
@@ -782,6 +786,11 @@ MF_DEV int64_t block_id(int R, int np, int dim, int dx, int dy, int dz,
 struct GatherArgs {
   int nproto, R, nloc, dim, kind, ncombo, P2;  // P2 = 2R+5 (padded span)
   int64_t row0, row1;
+  // interior rows (every element holding r or any of its columns exists,
+  // row box unclipped) are translates of one another: their values are
+  // one stencil, gathered once for a reference row and copied
+  const double *stencil;   // NULL: gather every row
+  int in_lo[3], in_hi[3];  // interior DOF box per axis (inclusive)
   const double *B21, *B22;
   const unsigned long long *bev;
   double *T;          // (ncombo, ncombo, P2^dim)
@@ -902,6 +911,14 @@ __global__ void __launch_bounds__(256) k_blocked_gather(AsmParams P,
   const int Wx = xhi - xlo + 1, Wy = yhi - ylo + 1;
   const int nent = Wx * Wy * (zhi - zlo + 1);
   const int64_t p0 = Pt.rowptr[r];
+  if (G.stencil && rx >= G.in_lo[0] && rx <= G.in_hi[0] &&
+      ry >= G.in_lo[1] && ry <= G.in_hi[1] && rz >= G.in_lo[2] &&
+      rz <= G.in_hi[2]) {
+    // the same block lookups in the same order as the reference row:
+    // bit-identical values, written at HBM speed
+    for (int k = lane; k < nent; k += 32) P.vals[p0 + k] = G.stencil[k];
+    return;
+  }
   Combo cb[8];
   dof_combos(G.kind, G.dim, cb);
   // inner elements holding r (uniform per warp)
@@ -988,6 +1005,11 @@ GatherArgs gather_args(const AsmParams &P, int kind, int nproto, int R,
   G.a22full = a22full;
   G.row0 = 0;
   G.row1 = P.pat.n;
+  G.stencil = nullptr;
+  for (int k = 0; k < 3; k++) {
+    G.in_lo[k] = 0;
+    G.in_hi[k] = -1;
+  }
   return G;
 }
 
@@ -1029,7 +1051,52 @@ cudaError_t mf_launch_blocked_gather(const AsmParams &P, int kind, int nproto,
   G.row0 = row0;
   G.row1 = row1;
   const int64_t t = (row1 - row0) * 32;
-  if (t > 0)
-    k_blocked_gather<<<(unsigned)((t + 255) / 256), 256, 0, s>>>(P, G);
-  return cudaGetLastError();
+  if (t <= 0) return cudaGetLastError();
+  // interior DOF box: r - K - 1 >= 0 and r + K <= N - 2 on every axis
+  // (elements around r and around every column c exist; row box unclipped)
+  const MfPattern &Pt = P.pat;
+  const int K = Pt.K, N[3] = {Pt.NX, Pt.NY, Pt.NZ};
+  bool interior = MF_BLOCKED_STENCIL != 0;
+  for (int k = 0; k < 3; k++) {
+    if (k == 2 && P.mesh.dim == 2) {
+      G.in_lo[2] = 0;
+      G.in_hi[2] = 0;
+      continue;
+    }
+    G.in_lo[k] = K + 1;
+    G.in_hi[k] = N[k] - 2 - K;
+    if (G.in_lo[k] > G.in_hi[k]) interior = false;
+  }
+  double *stencil = nullptr;
+  if (interior) {
+    const int span = 2 * K + 1;
+    const int64_t nent = (int64_t)span * span * (P.mesh.dim == 3 ? span : 1);
+    cudaError_t e = cudaMallocAsync(&stencil, sizeof(double) * nent, s);
+    if (e != cudaSuccess) return e;
+    // reference row: the centre of the interior box, gathered into the
+    // scratch (vals pointer shifted so that its row starts at stencil[0])
+    const int cx = (G.in_lo[0] + G.in_hi[0]) / 2;
+    const int cy = (G.in_lo[1] + G.in_hi[1]) / 2;
+    const int cz = (G.in_lo[2] + G.in_hi[2]) / 2;
+    const int64_t r0 = ((int64_t)cz * Pt.NY + cy) * Pt.NX + cx;
+    int64_t p0;
+    e = cudaMemcpyAsync(&p0, Pt.rowptr + r0, sizeof(int64_t),
+                        cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return e;
+    AsmParams Q = P;
+    Q.vals = stencil - p0;
+    GatherArgs G0 = G;
+    G0.row0 = r0;
+    G0.row1 = r0 + 1;
+    k_blocked_gather<<<1, 32, 0, s>>>(Q, G0);
+    G.stencil = stencil;
+  }
+  k_blocked_gather<<<(unsigned)((t + 255) / 256), 256, 0, s>>>(P, G);
+  cudaError_t e = cudaGetLastError();
+  if (stencil) {
+    cudaError_t ef = cudaFreeAsync(stencil, s);
+    if (e == cudaSuccess) e = ef;
+  }
+  return e;
 }

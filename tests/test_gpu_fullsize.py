@@ -132,3 +132,23 @@ def test_full_size_manufactured_solve(name, bound):
     err = l2_error(space, u, u_ex)
     print(f"{name}: CG {rep.iterations} iterations, L2 error {err:.3e}")
     assert err <= bound
+
+
+@pytest.mark.parametrize("name", ["R1", "R3-2h", "R4-small"])
+def test_blocked_interior_stencil_matches_general(name):
+    """The offset-blocked strategy (the reference default on structured
+    meshes) copies one gathered stencil into every interior row; those
+    rows must equal the general path (and the oracle for R1)."""
+    import bench
+    from paper_2101_08825_b200 import AssemblyConfig, assemble
+    mesh, space, kp, cfg = bench.build_problem(name)
+    blk = AssemblyConfig(L_max=cfg.L_max, outer_rule=cfg.outer_rule,
+                         inner_rule=cfg.inner_rule, strategy="blocked")
+    B = assemble(mesh, space, kp, blk)
+    A = assemble(mesh, space, kp, cfg)
+    assert B.events == A.events
+    assert rel_frob(B.vals, A.vals) <= 1e-12
+    if name == "R1":
+        import oracle
+        R = oracle.assemble_general(mesh, space, kp, cfg)
+        assert rel_frob(B.vals, R.vals) <= TOL
