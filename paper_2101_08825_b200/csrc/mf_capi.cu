@@ -133,6 +133,22 @@ int check_pattern(const MfPattern *p) {
   return MF_OK;
 }
 
+// keep freed call-scoped scratch (cudaMallocAsync / cudaFreeAsync) in the
+// device's default pool across calls: release threshold 0 would unmap and
+// remap it at every synchronisation.  Per-device setting, idempotent.
+void keep_pool() {
+#if MF_KEEP_POOL
+  int dev = 0;
+  cudaMemPool_t pool;
+  if (cudaGetDevice(&dev) == cudaSuccess &&
+      cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  cudaGetLastError();
+#endif
+}
+
 constexpr int kGenericBlock = 128;
 constexpr int kGenericMaxGrid = 148 * 4;
 
@@ -319,22 +335,7 @@ int mf_general_core(const MfMesh *mesh, const MfRules *rules,
       nmax = std::max<int64_t>(nmax, color_ptr[c + 1] - color_ptr[c]);
     const size_t nd = tet ? mf_tet_scratch_doubles(P, nmax)
                           : mf_tri_u_scratch_doubles(P, nmax);
-#if MF_KEEP_POOL
-    {
-      // keep freed scratch in the device's default pool across calls
-      // (release threshold 0 would unmap and remap it at every
-      // synchronisation); per-device setting, idempotent
-      int dev = 0;
-      cudaMemPool_t pool;
-      if (cudaGetDevice(&dev) == cudaSuccess &&
-          cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t keep = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold,
-                                &keep);
-      }
-      cudaGetLastError();
-    }
-#endif
+    keep_pool();
     double *gscr = nullptr;
     cudaError_t e = cudaMallocAsync(&gscr, sizeof(double) * nd, s);
     if (e != cudaSuccess) return cuda_status(e, "mf_general_core scratch");
@@ -496,6 +497,7 @@ int mf_gather_offset_blocks(const MfMesh *mesh, const MfPattern *pat,
   P.pat = *pat;
   P.scale = scale;
   P.vals = vals;
+  keep_pool();
   return cuda_status(mf_launch_blocked_gather(P, kind, nproto, R, table,
                                               a22, row0, row1, S(stream)),
                      "mf_gather_offset_blocks");

@@ -752,6 +752,9 @@ namespace {
 #ifndef MF_BLOCKED_STENCIL
 #define MF_BLOCKED_STENCIL 1
 #endif
+#ifndef MF_STENCIL_SYNC
+#define MF_STENCIL_SYNC 0
+#endif
 
 struct Combo {
   int ax, ay, az, t, i;
@@ -791,6 +794,7 @@ struct GatherArgs {
   // one stencil, gathered once for a reference row and copied
   const double *stencil;   // NULL: gather every row
   int in_lo[3], in_hi[3];  // interior DOF box per axis (inclusive)
+  double *row_out;         // non-NULL: write the (single) row here
   const double *B21, *B22;
   const unsigned long long *bev;
   double *T;          // (ncombo, ncombo, P2^dim)
@@ -981,7 +985,10 @@ __global__ void __launch_bounds__(256) k_blocked_gather(AsmParams P,
         if (j >= 0) s += G.a22[melem[u] * ne + cb[u].i * nl + j];
       }
     }
-    P.vals[p0 + k] = P.scale * s;
+    if (G.row_out)
+      G.row_out[k] = P.scale * s;
+    else
+      P.vals[p0 + k] = P.scale * s;
   }
 }
 
@@ -1006,6 +1013,7 @@ GatherArgs gather_args(const AsmParams &P, int kind, int nproto, int R,
   G.row0 = 0;
   G.row1 = P.pat.n;
   G.stencil = nullptr;
+  G.row_out = nullptr;
   for (int k = 0; k < 3; k++) {
     G.in_lo[k] = 0;
     G.in_hi[k] = -1;
@@ -1074,23 +1082,20 @@ cudaError_t mf_launch_blocked_gather(const AsmParams &P, int kind, int nproto,
     cudaError_t e = cudaMallocAsync(&stencil, sizeof(double) * nent, s);
     if (e != cudaSuccess) return e;
     // reference row: the centre of the interior box, gathered into the
-    // scratch (vals pointer shifted so that its row starts at stencil[0])
+    // scratch
     const int cx = (G.in_lo[0] + G.in_hi[0]) / 2;
     const int cy = (G.in_lo[1] + G.in_hi[1]) / 2;
     const int cz = (G.in_lo[2] + G.in_hi[2]) / 2;
     const int64_t r0 = ((int64_t)cz * Pt.NY + cy) * Pt.NX + cx;
-    int64_t p0;
-    e = cudaMemcpyAsync(&p0, Pt.rowptr + r0, sizeof(int64_t),
-                        cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) return e;
-    AsmParams Q = P;
-    Q.vals = stencil - p0;
     GatherArgs G0 = G;
     G0.row0 = r0;
     G0.row1 = r0 + 1;
-    k_blocked_gather<<<1, 32, 0, s>>>(Q, G0);
+    G0.row_out = stencil;
+    k_blocked_gather<<<1, 32, 0, s>>>(P, G0);
     G.stencil = stencil;
+#if MF_STENCIL_SYNC
+    cudaStreamSynchronize(s);
+#endif
   }
   k_blocked_gather<<<(unsigned)((t + 255) / 256), 256, 0, s>>>(P, G);
   cudaError_t e = cudaGetLastError();
