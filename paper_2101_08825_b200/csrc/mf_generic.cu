@@ -752,9 +752,6 @@ namespace {
 #ifndef MF_BLOCKED_STENCIL
 #define MF_BLOCKED_STENCIL 1
 #endif
-#ifndef MF_STENCIL_SYNC
-#define MF_STENCIL_SYNC 0
-#endif
 
 struct Combo {
   int ax, ay, az, t, i;
@@ -1093,9 +1090,6 @@ cudaError_t mf_launch_blocked_gather(const AsmParams &P, int kind, int nproto,
     G0.row_out = stencil;
     k_blocked_gather<<<1, 32, 0, s>>>(P, G0);
     G.stencil = stencil;
-#if MF_STENCIL_SYNC
-    cudaStreamSynchronize(s);
-#endif
   }
   k_blocked_gather<<<(unsigned)((t + 255) / 256), 256, 0, s>>>(P, G);
   cudaError_t e = cudaGetLastError();
