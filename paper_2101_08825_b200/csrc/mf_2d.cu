@@ -899,14 +899,28 @@ MF_DEV void lattice_split(int d, int NX, float inv_nx, int &gx, int &gy) {
 // Algorithm-1 decision for one sub-triangle at level L (shortcuts on):
 // _kernels.py:224-251 plus the dead / plateau proofs at L_max
 MF_DEV int tri_classify(const AsmParams &P, const double *g, int L,
-                        const double *ilo, const double *ihi) {
+                        const double *ilo, const double *ihi,
+                        const double *pilo, const double *pihi, double fo) {
   double slo[2], shi[2];
   sub_bbox<1>(g, slo, shi);
   if (L < P.L_min) return ACT_SPLIT;
   if (L == P.L_max) {
     if (!(aprx_min_d<2>(slo, shi, ilo, ihi) < P.dpe)) return ACT_NONE;
-    if (box_dead<2>(P, slo, shi, ilo, ihi)) return ACT_DEAD;
-    if (aprx_max_lt_dme(P, aprx_max_sq<2>(slo, shi, ilo, ihi)))
+    // dead / plateau proofs on the quadrature POINT sets (see mf_hex.cu
+    // classify): the outer rule points lie in the sub-triangle shrunk
+    // about its centroid by fo = 1 - 3 min(barycentric); pilo/pihi bound
+    // the inner element's points.  Relative margins keep the proofs safe
+    // under rounding; the event is counted either way.
+    double qlo[2], qhi[2];
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+      const double c = (g[k] + g[2 + k] + g[4 + k]) * (1.0 / 3.0);
+      const double mg = 1e-9 * (shi[k] - slo[k]);
+      qlo[k] = c + fo * (slo[k] - c) - mg;
+      qhi[k] = c + fo * (shi[k] - c) + mg;
+    }
+    if (box_dead<2>(P, qlo, qhi, pilo, pihi)) return ACT_DEAD;
+    if (aprx_max_sq<2>(qlo, qhi, pilo, pihi) < P.dm2 * (1.0 - 4e-9))
       return ACT_PLAT;
     return ACT_FULL;
   }
@@ -938,7 +952,10 @@ __global__ void __launch_bounds__(32 * kTriQWarps, MF_TRIQ_MINB)
   // per-lane pair state, lane-major: inner points, outer root + inverse
   __shared__ double s_y[kTriQWarps][NQ1][2][32];
   __shared__ double s_root[kTriQWarps][6][32];   // outer root triangle
-  __shared__ double s_res[kTriQWarps][NV][32];   // per-event V (round)
+  // per-event V of a phase-B round; phase W reuses the first 11 rows for
+  // the owners' inner boxes, plateau sums and point-set boxes
+  constexpr int NRES = NV > 11 ? NV : 11;
+  __shared__ double s_res[kTriQWarps][NRES][32];
   __shared__ int s_off[kTriQWarps][33];
   __shared__ unsigned s_mask[kTriQWarps][32];
   // the lane's 3 pattern rows: rowptr base shifted to (ylo, xlo), width
@@ -991,6 +1008,25 @@ __global__ void __launch_bounds__(32 * kTriQWarps, MF_TRIQ_MINB)
       s_y[w][q][0][lane] = xadd(xadd(c[0], xmul(p0, e10)), xmul(p1, e20));
       s_y[w][q][1][lane] = xadd(xadd(c[1], xmul(p0, e11)), xmul(p1, e21));
     }
+  }
+  // outer point shrink factor and the inner point-set box (proofs)
+  double fo = 1.0;
+  for (int q = 0; q < NQO; q++) {
+    const double a = s_opts[2 * q], b = s_opts[2 * q + 1];
+    fo = fmin(fo, fmin(fmin(a, b), 1.0 - a - b));
+  }
+  fo = fmin(1.0, 1.0 - 3.0 * fo + 1e-9);
+  double pilo[2], pihi[2];
+#pragma unroll
+  for (int k = 0; k < 2; k++) {
+    double mn = 1e300, mx = -1e300;
+    for (int q = 0; q < NQ1; q++) {
+      mn = fmin(mn, s_y[w][q][k][lane]);
+      mx = fmax(mx, s_y[w][q][k][lane]);
+    }
+    const double wd = ihi[k] - ilo[k];
+    pilo[k] = mn - 1e-9 * wd;
+    pihi[k] = mx + 1e-9 * wd;
   }
   const int64_t *mdofs = M.elem_dofs + m * M.nloc_max;
   const int NX = P.pat.NX, K = P.pat.K;
@@ -1048,7 +1084,7 @@ __global__ void __launch_bounds__(32 * kTriQWarps, MF_TRIQ_MINB)
           s_root[w][u][lane] = c[u];
         }
       }
-      const int act = tri_classify(P, root, 1, ilo, ihi);
+      const int act = tri_classify(P, root, 1, ilo, ihi, pilo, pihi, fo);
       if (act >= ACT_UPPER) {
         ev++;
         if (act == ACT_UPPER) c_up++;
@@ -1081,10 +1117,15 @@ __global__ void __launch_bounds__(32 * kTriQWarps, MF_TRIQ_MINB)
       const int grp = lane / nper, sl = lane % nper;
       double(*s_ib)[32] = s_res[w];         // owner inner boxes (4 rows)
       double(*s_sp)[32] = s_res[w] + 4;     // owner plateau sums (3 rows)
+      double(*s_pb)[32] = s_res[w] + 7;     // owner point-set boxes (4)
       s_ib[0][lane] = ilo[0];
       s_ib[1][lane] = ilo[1];
       s_ib[2][lane] = ihi[0];
       s_ib[3][lane] = ihi[1];
+      s_pb[0][lane] = pilo[0];
+      s_pb[1][lane] = pilo[1];
+      s_pb[2][lane] = pihi[0];
+      s_pb[3][lane] = pihi[1];
       __syncwarp();
       while (wmask) {
         const int cnt = __popc(wmask);
@@ -1099,11 +1140,16 @@ __global__ void __launch_bounds__(32 * kTriQWarps, MF_TRIQ_MINB)
           blo[1] = s_ib[1][o];
           bhi[0] = s_ib[2][o];
           bhi[1] = s_ib[3][o];
+          double qlo[2], qhi[2];
+          qlo[0] = s_pb[0][o];
+          qlo[1] = s_pb[1][o];
+          qhi[0] = s_pb[2][o];
+          qhi[1] = s_pb[3][o];
           OuterTri O;
           outer_map(rt, O);
           double g2[6];
           make_child<1>(rt, nleaf_bits == 2 ? sl : (sl >> 2), g2);
-          int a = tri_classify(P, g2, 2, blo, bhi);
+          int a = tri_classify(P, g2, 2, blo, bhi, qlo, qhi, fo);
           if (nleaf_bits == 4) {
             if (a == ACT_UPPER) {
               if ((sl & 3) == 0) {
@@ -1118,7 +1164,7 @@ __global__ void __launch_bounds__(32 * kTriQWarps, MF_TRIQ_MINB)
               make_child<1>(g2, sl & 3, g3);
 #pragma unroll
               for (int u = 0; u < 6; u++) g2[u] = g3[u];
-              a = tri_classify(P, g2, 3, blo, bhi);
+              a = tri_classify(P, g2, 3, blo, bhi, qlo, qhi, fo);
             } else {
               a = ACT_NONE;
             }
