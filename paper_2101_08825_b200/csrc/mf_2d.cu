@@ -548,6 +548,13 @@ __global__ void __launch_bounds__(128, MF_2D_MINB) k_2d(AsmParams P) {
 #pragma unroll
           for (int j = 0; j < NL; j++) spsum += SP[j];
           const double sc = -P.scale * scale_in;
+          // old values loaded together before any store (overlapped
+          // latencies; the compiler cannot prove the slots distinct)
+          double old[NL][NL];
+#pragma unroll
+          for (int i = 0; i < NL; i++)
+#pragma unroll
+            for (int j = 0; j < NL; j++) old[i][j] = P.vals[slot[i][j]];
 #pragma unroll
           for (int i = 0; i < NL; i++) {
             double mi = 0.0;
@@ -558,7 +565,7 @@ __global__ void __launch_bounds__(128, MF_2D_MINB) k_2d(AsmParams P) {
               double b = mi * SP[j];
 #pragma unroll
               for (int q = 0; q < NQ1; q++) b = fma(s_phiw[q][i], V[q][j], b);
-              P.vals[slot[i][j]] += sc * b;
+              P.vals[slot[i][j]] = old[i][j] + sc * b;
             }
           }
 #pragma unroll
@@ -789,6 +796,11 @@ __global__ void __launch_bounds__(128, MF_2D_MINB)
       if (live) {
         const double spsum = (SP[0] + SP[1]) + SP[2];
         const double sc = -P.scale * scale_in;
+        double old[NL][NL];
+#pragma unroll
+        for (int i = 0; i < NL; i++)
+#pragma unroll
+          for (int j = 0; j < NL; j++) old[i][j] = P.vals[slot[i][j]];
 #pragma unroll
         for (int i = 0; i < NL; i++) {
           double mi = 0.0;
@@ -799,7 +811,7 @@ __global__ void __launch_bounds__(128, MF_2D_MINB)
             double b = mi * SP[j];
 #pragma unroll
             for (int q = 0; q < NQ1; q++) b = fma(s_phiw[q][i], V[q][j], b);
-            P.vals[slot[i][j]] += sc * b;
+            P.vals[slot[i][j]] = old[i][j] + sc * b;
           }
         }
 #pragma unroll
@@ -1304,6 +1316,13 @@ __global__ void __launch_bounds__(32 * kTriQWarps, MF_TRIQ_MINB)
 #pragma unroll
         for (int j = 0; j < NL; j++)
           lattice_split((int)ldofs[j], NX, inv_nx, cgx[j], cgy[j]);
+        double old[NL][NL];
+#pragma unroll
+        for (int i = 0; i < NL; i++)
+#pragma unroll
+          for (int j = 0; j < NL; j++)
+            old[i][j] = P.vals[s_rb[w][i][lane] +
+                               (int64_t)cgy[j] * s_wx[w][i][lane] + cgx[j]];
 #pragma unroll
         for (int i = 0; i < NL; i++) {
           const int64_t rb = s_rb[w][i][lane];
@@ -1317,7 +1336,7 @@ __global__ void __launch_bounds__(32 * kTriQWarps, MF_TRIQ_MINB)
 #pragma unroll
             for (int q = 0; q < NQ1; q++)
               bsum = fma(s_phiw[q][i], V[q][j], bsum);
-            P.vals[rb + (int64_t)cgy[j] * wx + cgx[j]] += sc * bsum;
+            P.vals[rb + (int64_t)cgy[j] * wx + cgx[j]] = old[i][j] + sc * bsum;
           }
         }
 #pragma unroll

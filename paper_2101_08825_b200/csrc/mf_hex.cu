@@ -592,8 +592,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MF_HEX_MINB)
         }
         __syncwarp();
         const double sc = -P.scale * jac_in;
-        P.vals[slot0] += sc * b0;
-        P.vals[slot1] += sc * b1;
+        // both old values loaded before either store (distinct rows; the
+        // compiler cannot prove it and would serialise the two RMWs)
+        const double o0 = P.vals[slot0], o1 = P.vals[slot1];
+        P.vals[slot0] = o0 + sc * b0;
+        P.vals[slot1] = o1 + sc * b1;
       }
     }
   }

@@ -30,6 +30,13 @@
 namespace {
 
 constexpr int kTetLevels = 6;
+#ifndef MF_TET_LOADS_FIRST
+#define MF_TET_LOADS_FIRST 1
+#endif
+// loads-first also for larger inner rules (register pressure)
+#ifndef MF_TET_LOADS_FIRST_MAXNQ
+#define MF_TET_LOADS_FIRST_MAXNQ 11
+#endif
 
 // per-thread pair state kept in shared memory, lane-major (stride = block
 // size, conflict-free): outer root vertices, the outer inverse map and the
@@ -487,6 +494,26 @@ __global__ void __launch_bounds__(32 * kTetWarps, MF_TET_MINB(NQ1))
           if (live) {
             double spsum = (SP[0] + SP[1]) + (SP[2] + SP[3]);
             const double sc = -P.scale * scale_in;
+#if MF_TET_LOADS_FIRST
+            // the 16 old values are loaded together before any store, so
+            // their latencies overlap (the compiler cannot hoist them past
+            // the stores itself: it cannot prove the slots distinct)
+            double old[4][4];
+            if constexpr (NQ1 <= MF_TET_LOADS_FIRST_MAXNQ) {
+#pragma unroll
+              for (int j = 0; j < 4; j++) {
+                const int v = c_tet_corner[tout][j];
+                const int gx = x2 + (v & 1), gy = y2 + ((v >> 1) & 1),
+                          gzo = (v >> 2) & 1;
+#pragma unroll
+                for (int i = 0; i < 4; i++)
+                  old[i][j] = P.vals[rowz[i] +
+                                     ((int64_t)gzo * rwy[i] + (gy - rylo[i])) *
+                                         rwx[i] +
+                                     (gx - rxlo[i])];
+              }
+            }
+#endif
 #pragma unroll
             for (int i = 0; i < 4; i++) {
               double mi = 0.0;
@@ -504,7 +531,14 @@ __global__ void __launch_bounds__(32 * kTetWarps, MF_TET_MINB(NQ1))
                     rowz[i] +
                     ((int64_t)gzo * rwy[i] + (gy - rylo[i])) * rwx[i] +
                     (gx - rxlo[i]);
+#if MF_TET_LOADS_FIRST
+                if constexpr (NQ1 <= MF_TET_LOADS_FIRST_MAXNQ)
+                  P.vals[slot] = old[i][j] + sc * b;
+                else
+                  P.vals[slot] += sc * b;
+#else
                 P.vals[slot] += sc * b;
+#endif
               }
             }
 #pragma unroll
