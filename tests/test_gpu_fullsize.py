@@ -152,3 +152,20 @@ def test_blocked_interior_stencil_matches_general(name):
         import oracle
         R = oracle.assemble_general(mesh, space, kp, cfg)
         assert rel_frob(B.vals, R.vals) <= TOL
+
+
+def test_blocked_interior_stencil_quads():
+    """Quad Q1 (4 combos per DOF) through the interior-stencil copy."""
+    from paper_2101_08825_b200 import (AssemblyConfig, FESpace, KernelParams,
+                                       assemble, build_mesh)
+    h = 1 / 64
+    kp = KernelParams(2, 0.1, h / 2)
+    mesh = build_mesh(2, ((0.0, 1.0), (0.0, 0.75)), h, kp.delta + kp.eps,
+                      "quad")
+    space = FESpace(mesh, 1)
+    A = assemble(mesh, space, kp, AssemblyConfig(L_max=3,
+                                                 strategy="general"))
+    B = assemble(mesh, space, kp, AssemblyConfig(L_max=3,
+                                                 strategy="blocked"))
+    assert B.events == A.events
+    assert rel_frob(B.vals, A.vals) <= 1e-12
