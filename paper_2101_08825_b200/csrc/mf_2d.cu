@@ -904,8 +904,12 @@ MF_DEV void lattice_split(int d, int NX, float inv_nx, int &gx, int &gy) {
   }
 }
 
-#ifndef MF_TRIQ_MINB
-#define MF_TRIQ_MINB 3  // 168 registers: R2 kernels 3.5% faster than 2
+// blocks per SM of k_tri_q: 3 (168 registers) for large launches (R2
+// 1.203 vs 1.209 s with 2); small, latency-bound launches run faster with
+// 2 blocks of the 255-register build (R1 31.0 -> 26.4 ms, R2-small 220 ->
+// 196 ms), so launch_tri_u picks by the launch's thread count
+#ifndef MF_TRIQ_SMALL_THREADS
+#define MF_TRIQ_SMALL_THREADS (148 * 384 * 4)
 #endif
 
 // Algorithm-1 decision for one sub-triangle at level L (shortcuts on):
@@ -954,8 +958,8 @@ MF_DEV void outer_map(const double *c, OuterTri &O) {
   O.inv[3] = e10 * idet;
 }
 
-template <int NQO, int NQ1>
-__global__ void __launch_bounds__(32 * kTriQWarps, MF_TRIQ_MINB)
+template <int NQO, int NQ1, int MINB>
+__global__ void __launch_bounds__(32 * kTriQWarps, MINB)
     k_tri_q(AsmParams P, int cls, double *gscr) {
   constexpr int NL = 3;
   constexpr int NV = NQ1 * NL;
@@ -1374,8 +1378,12 @@ cudaError_t launch_tri_u(const AsmParams &P, double *gscr, cudaStream_t s) {
   for (int cls = 0; cls < per; cls++) {
     const int n = (rows - cls + per - 1) / per;
     if (n < 1) continue;
-    if (queue)
-      k_tri_q<NQO, NQ1><<<dim3(gx, n), 32 * kTriQWarps, 0, s>>>(P, cls, gscr);
+    if (queue && (int64_t)P.n_inner * n < MF_TRIQ_SMALL_THREADS)
+      k_tri_q<NQO, NQ1, 2><<<dim3(gx, n), 32 * kTriQWarps, 0, s>>>(P, cls,
+                                                                 gscr);
+    else if (queue)
+      k_tri_q<NQO, NQ1, 3><<<dim3(gx, n), 32 * kTriQWarps, 0, s>>>(P, cls,
+                                                                 gscr);
     else
       k_tri_u<NQO, NQ1><<<dim3(gx, n), 128, 0, s>>>(P, cls, gscr);
     cudaError_t e = cudaGetLastError();
