@@ -121,6 +121,42 @@ def build_problem(name):
     return mesh, space, kp, cfg
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def ref_import():
+    """The unmodified reference package (numba) installed under
+    baseline/_ref; None if it is not installed."""
+    os.environ.setdefault("NUMBA_CACHE_DIR",
+                          os.path.join("/tmp", "mf_numba_cache"))
+    extra = [REF_DIR] + [p for p in (os.environ.get("MF_REF_PATH"),) if p]
+    for p in extra:
+        if os.path.isdir(os.path.join(p, "mollifem")) and p not in sys.path:
+            sys.path.insert(0, p)
+    try:
+        import mollifem
+        import numba  # noqa: F401
+    except ImportError:
+        return None
+    return mollifem
+
+
+def build_reference_problem(mf, name):
+    """The workload built by the reference's own host layer (structured
+    quad/tri/hex meshes only; None for tets and Delaunay meshes, which the
+    reference cannot build)."""
+    dim, om, h, delta, eps, kappa, kind, lmax, rule = CONFIGS[name]
+    if kind not in ("tri", "quad", "hex") or name in JITTER or \
+            rule in ("tri3", "tri6"):
+        return None
+    mesh = mf.build_mesh(dim, om, h, delta + eps, kind)
+    space = mf.FESpace(mesh, 1)
+    kp = mf.KernelParams(dim, delta, eps, kappa)
+    cfg = mf.AssemblyConfig(L_max=lmax, outer_rule=rule, inner_rule=rule,
+                            strategy="general")
+    return mesh, space, kp, cfg
+
+
 def config_json(name, mesh, space, n_gpus, slab_info=None,
                 strategy="general"):
     dim, om, h, delta, eps, kappa, kind, lmax, rule = CONFIGS[name]
@@ -293,7 +329,15 @@ def fp64_peak(device):
 # --------------------------------------------------------------------------
 # CPU leg (oracle port on the host cores)
 
-def cpu_sample(name, mesh, space, kp, cfg, budget_s=20.0, seed=0):
+def cpu_sample(name, mesh, space, kp, cfg, budget_s=20.0, seed=0,
+               use_reference=True):
+    """cpu_baseline of the GPU line: the unmodified reference (numba) on a
+    seeded sample when it is installed and can build the workload, else
+    the oracle port (oracle/mf_oracle.c)."""
+    if use_reference:
+        mf = ref_import()
+        if mf is not None and build_reference_problem(mf, name) is not None:
+            return RefRunner(mf, name).sample(budget_s, seed)
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle
     from paper_2101_08825_b200.assembly import HostPattern
@@ -329,10 +373,178 @@ def cpu_sample(name, mesh, space, kp, cfg, budget_s=20.0, seed=0):
                        "_general_core, no FMA) on all host threads")}
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+class RefRunner:
+    """The unmodified reference (numba, baseline/_ref) on the host cores.
+
+    General path (the per-pair comparison path of the GPU design, SURVEY
+    8(d) CPU plan item 3): a seeded sample of outer elements split over
+    all host threads, each thread calling the reference's own
+    `_run_general(outer_ids=...)` (assembly.py:369-388; nogil numba
+    `_candidates` + `_general_core`), as `parallel_assemble` does with its
+    thread pool (parallel.py:157-178).  Default path (item 2): the
+    reference `assemble()` with strategy "auto" -> offset-blocked
+    (assembly.py:448-473), timed in full on a workload small enough to
+    finish in seconds and reported as pairs/s."""
+
+    def __init__(self, mf, name):
+        from mollifem import assembly as RA
+        self.mf, self.RA, self.name = mf, RA, name
+        t = time.perf_counter()
+        self.mesh, self.space, self.kp, self.cfg = build_reference_problem(
+            mf, name)
+        self.prep = RA._Prep(self.mesh, self.space, self.kp, self.cfg)
+        # one shared value buffer (the sampled rows are a timing workload;
+        # R4's 16.4 GB pattern cannot be replicated per thread)
+        self.A = RA._new_matrix(self.mesh, self.space, self.kp, self.cfg)
+        self.setup_s = time.perf_counter() - t
+        self.threads = os.cpu_count() or 1
+        n = self.mesh.n_elements
+        # JIT warm-up (numba compiles per signature on first call)
+        RA._run_general(self.mesh, self.space, self.kp, self.cfg, self.prep,
+                        self.A, outer_ids=np.arange(min(2, n)))
+        probe = np.random.default_rng(12345).choice(
+            n, min(n, 6 * self.threads), replace=False)
+        self.rate = None
+        pairs, dt, _ = self._run(np.sort(probe))
+        self.rate = pairs / max(dt, 1e-6)
+        self.per_el = max(pairs / len(probe), 1.0)
+
+    def _run(self, sample):
+        from concurrent.futures import ThreadPoolExecutor
+        RA = self.RA
+        reach = self.kp.delta + self.kp.eps
+        mask = np.ones(self.mesh.n_elements, dtype=np.bool_)
+        ptr, _ = RA._candidates(self.mesh, reach, sample, mask)
+        chunks = [c for c in np.array_split(sample, self.threads) if c.size]
+
+        def work(c):
+            return RA._run_general(self.mesh, self.space, self.kp, self.cfg,
+                                   self.prep, self.A, outer_ids=c)
+
+        with ThreadPoolExecutor(max_workers=len(chunks)) as pool:
+            t = time.perf_counter()
+            ev = sum(pool.map(work, chunks))
+            dt = time.perf_counter() - t
+        return int(ptr[-1]), dt, int(ev)
+
+    def sample(self, budget_s, seed):
+        n = self.mesh.n_elements
+        k = int(min(n, max(self.threads, self.rate * budget_s / self.per_el)))
+        rng = np.random.default_rng(seed)
+        s = np.sort(rng.choice(n, k, replace=False))
+        pairs, dt, ev = self._run(s)
+        return {"value": pairs / dt, "unit": "pairs/s",
+                "cores": self.threads, "kind": "reference",
+                "cpu_model": cpu_model(), "seconds": dt,
+                "sample": (f"{k} seeded outer elements (rng {seed}) of "
+                           f"{self.name} = {pairs} pairs, {ev} events; "
+                           "unmodified reference mollifem "
+                           "_run_general (numba _general_core, nogil) on "
+                           f"{len(np.array_split(s, self.threads))} host "
+                           "threads, one shared value buffer")}
+
+    def default_path(self, name="R4-small"):
+        """Reference default assemble() (strategy auto -> blocked) timed in
+        full on `name` (JIT warmed on the same mesh first)."""
+        mf = self.mf
+        rp = build_reference_problem(mf, name)
+        if rp is None:
+            return None
+        mesh, space, kp, cfg = rp
+        auto = mf.AssemblyConfig(L_max=cfg.L_max, outer_rule=cfg.outer_rule,
+                                 inner_rule=cfg.inner_rule, strategy="auto")
+        small = build_reference_problem(mf, "R1") if mesh.dim == 2 else None
+        if small is not None:
+            mf.assemble(small[0], small[1], small[2], auto)
+        else:
+            # warm the blocked JIT on a tiny mesh of the same dim and kind
+            dim, om, h, delta, eps, kappa, kind, lmax, rule = CONFIGS[name]
+            tiny = mf.build_mesh(dim, ((0.0, 4 * h),) * dim, h,
+                                 delta + eps, kind)
+            mf.assemble(tiny, mf.FESpace(tiny, 1), kp, auto)
+        reach = kp.delta + kp.eps
+        ptr, _ = self.RA._candidates(
+            mesh, reach, np.arange(mesh.n_elements),
+            np.ones(mesh.n_elements, dtype=np.bool_))
+        t = time.perf_counter()
+        A = mf.assemble(mesh, space, kp, auto)
+        dt = time.perf_counter() - t
+        pairs = int(ptr[-1])
+        return {"value": pairs / dt, "unit": "pairs/s", "cores": 1,
+                "workload": name, "pairs": pairs, "seconds": dt,
+                "events": int(A.events),
+                "path": "reference default assemble(strategy='auto') -> "
+                        "offset-blocked (_run_blocked), single thread, "
+                        "full assembly incl. _finish"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    name = args.config
+    mf = ref_import()
+    if mf is None or build_reference_problem(mf, name) is None:
+        return run_reference_port(args)
+    runner = RefRunner(mf, name)
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = runner.sample(args.ref_step_budget if i >= args.warmup else 1.0,
+                          seed=i)
+        if i >= args.warmup:
+            vals.append(r)
+    v = statistics.median(x["value"] for x in vals)
+    total_pairs = PAIRS.get(name) or v
+    dflt = None
+    if not args.no_default_path:
+        dname = DEFAULT_PATH_WORKLOAD.get(name, name)
+        dflt = runner.default_path(dname)
+        if dflt is not None and total_pairs:
+            dflt["projected_seconds_full_workload"] = total_pairs / dflt[
+                "value"]
+    cb = dict(vals[0])
+    cb["value"] = v
+    if dflt is not None:
+        cb["default_path"] = dflt
+    line = {"metric": METRIC, "value": v, "unit": "pairs/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": statistics.median(x["seconds"] for x in vals) * 1e3,
+            "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": config_json(name, runner.mesh, runner.space, 1),
+            "cpu_baseline": cb,
+            "e2e": {"value": v, "unit": "pairs/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "projected_full_assembly_s": (total_pairs / v
+                                          if PAIRS.get(name) else None),
+            "note": ("each step = the reference general path on a bounded "
+                     "seeded sample of outer elements (ms_per_step is that "
+                     "sample's wall time); projected_full_assembly_s = all "
+                     "pairs at the sampled rate")}
+    print(json.dumps(line), flush=True)
+
+
+# workload on which the reference default (blocked) path is timed in full
+DEFAULT_PATH_WORKLOAD = {"R4": "R4-small", "R4-gauss2": "R4-small",
+                         "R5": "R4-small", "R3-16h": "R3-2h",
+                         "R3-8h": "R3-2h", "R3-4h": "R3-2h"}
+
+
+def run_reference_port(args):
+    """Fallback when the reference cannot run here (not installed, or a
+    workload it cannot build: tets, Delaunay): the oracle port."""
     name = args.config
     mesh, space, kp, cfg = build_problem(name)
     total_pairs = PAIRS.get(name)
@@ -345,25 +557,28 @@ def run_reference(args):
         total_pairs = int(ptr[-1])
     vals = []
     for i in range(args.warmup + args.steps):
-        r = cpu_sample(name, mesh, space, kp, cfg, budget_s=args.cpu_budget,
-                       seed=i)
+        r = cpu_sample(name, mesh, space, kp, cfg,
+                       budget_s=(args.ref_step_budget if i >= args.warmup
+                                 else 1.0),
+                       seed=i, use_reference=False)
         if i >= args.warmup:
             vals.append(r)
     v = statistics.median(x["value"] for x in vals)
+    cb = dict(vals[0])
+    cb["value"] = v
     line = {"metric": METRIC, "value": v, "unit": "pairs/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": total_pairs / v * 1e3,
+            "ms_per_step": statistics.median(x["seconds"] for x in vals) * 1e3,
             "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
             "config": config_json(name, mesh, space, 1),
-            "cpu_baseline": {"value": v, "unit": "pairs/s",
-                             "cores": vals[0]["cores"], "kind": "port",
-                             "sample": vals[0]["sample"]},
+            "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "pairs/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
-            "note": ("ms_per_step = projected full-assembly time at the "
-                     "sampled rate")}
+            "projected_full_assembly_s": total_pairs / v,
+            "note": ("the reference cannot build this workload (or is not "
+                     "installed): oracle port on a seeded sample")}
     print(json.dumps(line), flush=True)
 
 
@@ -630,6 +845,12 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ref-step-budget", type=float, default=6.0,
+                    help="--impl reference: seconds of CPU work per timed "
+                         "step (warm-up steps use 1 s)")
+    ap.add_argument("--no-default-path", action="store_true",
+                    help="--impl reference: skip timing the reference "
+                         "default (blocked) assemble()")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
