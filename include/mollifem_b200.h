@@ -30,7 +30,7 @@ extern "C" {
 #define MF_ERR_CUDA 2
 #define MF_ERR_UNSUPPORTED 3
 
-#define MF_ABI_VERSION 2
+#define MF_ABI_VERSION 3
 
 /* Mesh SoA + DOF map (mesh.py:78-88 flat arrays; fe_space.py:131-157). */
 typedef struct MfMesh {
@@ -98,7 +98,12 @@ typedef struct MfPattern {
 #define MF_CNT_EV_PLATEAU 3    /* L_max events proven inside delta-eps */
 #define MF_CNT_EV_DEAD 4       /* L_max events proven beyond delta+eps */
 #define MF_CNT_EV_FULL 5       /* L_max events integrated point by point */
-#define MF_NCOUNTERS 8
+#define MF_CNT_OVERFLOW 6      /* nonzero: a specialised kernel dropped
+                                  work it could not hold (more split nodes
+                                  per level than it buffers); the values
+                                  are incomplete and the caller must treat
+                                  the call as failed (MF_ERR_UNSUPPORTED) */
+#define MF_NCOUNTERS 10        /* slots 7-9: debug statistics builds */
 
 /* Neighbour search.  Replaces _count_candidates/_fill_candidates
  * (_kernels.py:1205-1268) as driven by _candidates (assembly.py:157-175):
@@ -147,6 +152,28 @@ int mf_general_core(const MfMesh *mesh, const MfRules *rules,
                     double scale, double *vals, uint64_t *counters,
                     int32_t flags, void *workspace, size_t ws_bytes,
                     void *stream);
+
+/* Explicit candidate lists: the exact argument form of _general_core
+ * (_kernels.py:391-400).  For i < n_outer and k in [cand_ptr[i],
+ * cand_ptr[i+1]) the pair (outer_ids[i], cand_ids[k]) runs Algorithm 1 --
+ * every listed pair, with no gap test, duplicates counted twice, as the
+ * reference does -- and scale*(A21 + A22) is added into vals.  All four
+ * list arrays are device memory (int64); cand_ptr[0] must be 0.  The lists
+ * are transposed on the device to per-inner-element ranges (stable radix
+ * sort: each inner element keeps the caller's pair order), the inner
+ * elements are coloured greedily by shared DOFs on the host (at most 64
+ * colours) and each colour runs as one race-free launch of the generic
+ * kernel.  Only elem_kind/coords/lo/hi/dofs of the mesh are read (the cell
+ * grid may be NULL).  Synchronises `stream` (the list sizes are read back);
+ * scratch is stream-ordered (cudaMallocAsync).  The product-form pair sets
+ * that _run_general builds (outer ids x inner mask, gap < delta+eps) are
+ * faster through mf_general_core, which runs the specialised kernels. */
+int mf_general_core_lists(const MfMesh *mesh, const MfRules *rules,
+                          const MfKernel *kern, const MfPattern *pat,
+                          const int64_t *outer_ids, int64_t n_outer,
+                          const int64_t *cand_ptr, const int64_t *cand_ids,
+                          double scale, double *vals, uint64_t *counters,
+                          int32_t flags, void *stream);
 
 /* Offset-blocked strategy, the reference default on pure meshes
  * (strategy "auto"/"blocked", assembly.py:391-437).  mf_offset_blocks runs

@@ -54,7 +54,7 @@ def lib():
         build()
     L = C.CDLL(_LIB_PATH)
     L.orc_general_core.restype = C.c_int64
-    L.orc_general_core.argtypes = _GENERAL + [_f64p, C.c_void_p]
+    L.orc_general_core.argtypes = _GENERAL + [C.c_void_p, C.c_void_p]
     L.orc_general_core_mt.restype = C.c_int64
     L.orc_general_core_mt.argtypes = _GENERAL + [C.POINTER(C.c_void_p),
                                                  C.c_int, C.c_int64]
@@ -103,9 +103,10 @@ def candidates(mesh, reach, outer_ids, inner_mask):
     return ptr, ids
 
 
-def _general_args(mesh, space, params, config, outer, ptr, ids, A):
+def _general_args(mesh, space, params, config, outer, ptr, ids, A, P=None):
     from paper_2101_08825_b200.assembly import prep_tables
-    P = prep_tables(mesh, space, config)
+    if P is None:
+        P = prep_tables(mesh, space, config)
     return (mesh.dim, space.degree, mesh.elem_kind, mesh.elem_coords,
             mesh.elem_coords.shape[1], mesh.elem_lo, mesh.elem_hi,
             space.element_dofs, space.element_dofs.shape[1], outer,
@@ -132,7 +133,8 @@ def run_general(mesh, space, params, config, A, outer_ids=None,
     ptr, ids = candidates(mesh, params.delta + params.eps, outer, mask)
     args = _general_args(mesh, space, params, config, outer, ptr, ids, A)
     cen = None if census is None else census.ctypes.data_as(C.c_void_p)
-    return int(lib().orc_general_core(*args, A.vals, cen))
+    return int(lib().orc_general_core(
+        *args, np.ascontiguousarray(A.vals).ctypes.data_as(C.c_void_p), cen))
 
 
 def run_general_threads(mesh, space, params, config, A, outer_ids,
@@ -159,6 +161,87 @@ def run_general_threads(mesh, space, params, config, A, outer_ids,
         for b in bufs:
             A.vals += b
     return ev, dt
+
+
+def run_general_tiled(mesh, space, params, config, pat, inner_ids, vals,
+                      base=0, nthreads=None, tile=None):
+    """`_run_general(outer_ids=all, inner_mask=inner_ids)` on host threads.
+
+    The inner elements are cut into tiles of `tile`^dim cells; tiles whose
+    tile coordinates have the same parity bits share no DOF (an element of
+    cell c only touches DOF planes [d*c, d*(c+1)] per axis), so each parity
+    class runs its tiles concurrently (ctypes releases the GIL) into ONE
+    value array without races, and the classes run one after another.
+    Every pair is evaluated by orc_general_core exactly as the serial call
+    would and each value entry receives its pair blocks in a fixed order
+    (parity class, then tile, then the serial order), so the result does
+    not depend on the thread count; it equals the serial run up to the
+    summation order of entries shared by tiles (rounding level).
+
+    pat: a HostPattern (rowptr, grid); vals: float64 array holding the
+    pattern's entries [base, base + len(vals)) -- a window is enough when
+    the inner elements' rows lie inside it.  Returns the event count."""
+    from concurrent.futures import ThreadPoolExecutor
+    from paper_2101_08825_b200.assembly import stencil_pad, stencil_radius
+    L = lib()
+    n = mesh.n_elements
+    dim = mesh.dim
+    inner = np.ascontiguousarray(inner_ids, dtype=np.int64)
+    reach = params.delta + params.eps
+    R = stencil_radius(reach + stencil_pad(mesh), mesh.h)
+    cell = np.asarray(mesh.elem_cell, dtype=np.int64)[:, :dim]
+    if tile is None:
+        # Delaunay vertices may sit dof_spill planes above their bin
+        tile = max(2, int(getattr(mesh, "dof_spill", 1)) + 1)
+    tc = cell[inner] // tile
+    colour = np.zeros(len(inner), dtype=np.int64)
+    for k in range(dim):
+        colour |= (tc[:, k] & 1) << k
+    key = np.zeros(len(inner), dtype=np.int64)
+    for k in range(dim):
+        key = key * (int(tc[:, k].max()) + 1 if len(inner) else 1) + tc[:, k]
+    assert vals.dtype == np.float64 and vals.flags.c_contiguous
+    vptr = vals.ctypes.data - 8 * int(base)
+    PT = prep_tables_cached(mesh, space, config)
+
+    def run_tile(elems):
+        lo = cell[elems].min(axis=0) - R
+        hi = cell[elems].max(axis=0) + R
+        near = np.all((cell >= lo) & (cell <= hi), axis=1)
+        outer = np.nonzero(near)[0].astype(np.int64)
+        mask = np.zeros(n, dtype=np.uint8)
+        mask[elems] = 1
+        ptr, ids = candidates(mesh, reach, outer, mask)
+        args = _general_args(mesh, space, params, config, outer, ptr, ids,
+                             pat, P=PT)
+        return int(L.orc_general_core(*args, C.c_void_p(vptr), None))
+
+    nthreads = nthreads or os.cpu_count() or 1
+    events = 0
+    with ThreadPoolExecutor(max_workers=nthreads) as pool:
+        for c in range(1 << dim):
+            sel = colour == c
+            if not sel.any():
+                continue
+            ks = key[sel]
+            els = inner[sel]
+            order = np.argsort(ks, kind="stable")
+            ks, els = ks[order], els[order]
+            cuts = np.nonzero(np.diff(ks))[0] + 1
+            tiles = np.split(els, cuts)
+            events += sum(pool.map(run_tile, tiles))
+    return events
+
+
+_PREP_CACHE = {}
+
+
+def prep_tables_cached(mesh, space, config):
+    from paper_2101_08825_b200.assembly import prep_tables
+    k = (id(mesh), id(space), repr(config))
+    if k not in _PREP_CACHE:
+        _PREP_CACHE[k] = prep_tables(mesh, space, config)
+    return _PREP_CACHE[k]
 
 
 def asymmetry_inf(A):

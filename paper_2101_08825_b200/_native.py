@@ -12,9 +12,10 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("MF_LIB_PATH") or os.path.join(
     _HERE, "_lib", "libmollifem_b200.so")
 
-MF_NCOUNTERS = 8
+MF_NCOUNTERS = 10
 CNT_EVENTS, CNT_PAIRS, CNT_EV_UPPER, CNT_EV_PLATEAU, CNT_EV_DEAD, \
-    CNT_EV_FULL = range(6)
+    CNT_EV_FULL, CNT_OVERFLOW = range(7)
+ABI_VERSION = 3
 FLAG_FORCE_GENERIC = 1
 FLAG_NO_SHORTCUTS = 2
 FLAG_ELEMENT_THREADS = 4
@@ -72,6 +73,12 @@ _SIGS = {
                                   _P, _P, _P, C.c_int32, C.c_int32,
                                   C.c_double, _P, _P, C.c_int32, _P,
                                   C.c_size_t, _P]),
+    "mf_general_core_lists": (C.c_int, [C.POINTER(MfMesh),
+                                        C.POINTER(MfRules),
+                                        C.POINTER(MfKernel),
+                                        C.POINTER(MfPattern), _P, C.c_int64,
+                                        _P, _P, C.c_double, _P, _P,
+                                        C.c_int32, _P]),
     "mf_offset_block_count": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32]),
     "mf_offset_blocks_workspace_bytes": (C.c_size_t, [C.POINTER(MfRules),
                                                       C.c_int64]),
@@ -150,7 +157,9 @@ def ptr(t):
     return None if t is None else C.c_void_p(t.data_ptr())
 
 
-def stream_ptr(stream=None):
+def stream_ptr(stream=None, device=None):
+    """cudaStream_t of `stream`, else of the current stream of `device`
+    (default: the current device)."""
     import torch
-    s = stream if stream is not None else torch.cuda.current_stream()
+    s = stream if stream is not None else torch.cuda.current_stream(device)
     return C.c_void_p(s.cuda_stream)

@@ -160,6 +160,11 @@ class PrepTables:
         self.box_in_1d = _rule_1d(box_inner)
 
 
+def rule_1d(preset):
+    """(1D points on [-1, 1], weights) of a tensor box rule preset."""
+    return _rule_1d(preset)
+
+
 def _rule_1d(preset):
     from .quadrature import _preset, gauss_legendre_1d, gauss_lobatto_1d
     fam, n = _preset(preset)
@@ -266,7 +271,11 @@ class SparseMatrix(HostPattern):
     After `assemble()` the values live in HBM (`vals_device`) and, unless
     the caller asked for a device-only result, in the host array `vals`
     (the reference contract).  Every method runs on the device through the
-    C-ABI; after mutating the host `vals` call `sync_to_device()`.
+    C-ABI.  While a device copy exists the host array is READ-ONLY, so an
+    in-place edit cannot leave the device copy silently stale: to change
+    values assign a new array (`A.vals = v`, which drops the device copy;
+    the next device method uploads it).  Matrices without a device copy
+    (`copy_pattern()`) have a writable `vals`, as in the reference.
     """
 
     def __init__(self, space, K, allocate=True):
@@ -280,7 +289,9 @@ class SparseMatrix(HostPattern):
         from . import _native as N
         if self._drowptr is None:
             from .device import to_device
-            self._drowptr = to_device(self.rowptr, None)
+            self._drowptr = to_device(
+                self.rowptr,
+                self._dvals.device if self._dvals is not None else None)
         return N.MfPattern(NX=self.NX, NY=self.NY, NZ=self.NZ, K=self.K,
                            n=self.n, rowptr=self._drowptr.data_ptr())
 
@@ -290,17 +301,20 @@ class SparseMatrix(HostPattern):
             self.sync_to_device()
         return self._dvals
 
-    def sync_to_device(self):
+    def sync_to_device(self, device=None):
         from .device import to_device
         if self._vals is None:
             raise RuntimeError("matrix has no values")
-        self._dvals = to_device(self._vals, None)
+        self._dvals = to_device(self._vals, device)
+        _freeze(self._vals)
         return self._dvals
 
     @property
     def vals(self):
         if self._vals is None and self._dvals is not None:
             self._vals = _d2h(self._dvals)
+        if self._dvals is not None:
+            _freeze(self._vals)
         return self._vals
 
     @vals.setter
@@ -312,7 +326,8 @@ class SparseMatrix(HostPattern):
         from . import _native as N
         L = N.lib()
         N.check(getattr(L, name)(C_byref(self._pattern_struct()), *args,
-                                 N.stream_ptr()), name)
+                                 N.stream_ptr(device=self._dvals.device)),
+                name)
 
     def _dev_vec(self, x):
         import torch
@@ -389,18 +404,34 @@ class SparseMatrix(HostPattern):
         return other
 
 
+def _freeze(a):
+    """Host values mirrored on the device are read-only (SparseMatrix)."""
+    if isinstance(a, np.ndarray) and a.flags.writeable:
+        try:
+            a.setflags(write=False)
+        except ValueError:
+            pass
+
+
 def C_byref(s):
     import ctypes
     return ctypes.byref(s)
 
 
+# below this many value bytes a matrix is copied to the host in one plain
+# transfer after the kernels (no staging ring, no overlapped ranges)
+_STREAM_MIN_BYTES = 1 << 28
+
+
 def _d2h(t):
-    """Device float64 vector -> fresh host numpy array (HostStager)."""
+    """Device float64 vector -> fresh host numpy array (HostStager for
+    large arrays, a plain copy below _STREAM_MIN_BYTES)."""
     import torch
     from .device import HostStager
     if t.numel() == 0:
         return np.zeros(0, dtype=np.float64)
-    if t.dtype != torch.float64 or t.dim() != 1:
+    if (t.dtype != torch.float64 or t.dim() != 1
+            or t.numel() * 8 < _STREAM_MIN_BYTES):
         return t.cpu().numpy()
     host = np.empty(t.numel(), dtype=np.float64)
     ev = torch.cuda.Event()
@@ -573,7 +604,7 @@ class AssemblyContext:
             float(scale),
             (vals_window.pointer() if vals_window is not None
              else N.ptr(A._dvals)), N.ptr(counters), int(flags),
-            N.ptr(ws), wsb, N.stream_ptr()), "mf_general_core")
+            N.ptr(ws), wsb, N.stream_ptr(device=self.device)), "mf_general_core")
         return counters
 
     # -- general path with the host copy overlapped -----------------------
@@ -635,7 +666,7 @@ class AssemblyContext:
         nplanes = int(space.grid_dims[-1])
         host = np.empty(A.nnz, dtype=np.float64)
         self._stream_host = host
-        compute = torch.cuda.current_stream()
+        compute = torch.cuda.current_stream(self.device)
         ranges = []
         done_plane = 0
         for s_, (lo, hi) in enumerate(layers):
@@ -705,7 +736,7 @@ class AssemblyContext:
             C_byref(self.dmesh.struct), C_byref(self.drules.struct),
             C_byref(self.kernel_struct()), kcode, nproto, N.ptr(protos), R,
             float(mesh.h), N.ptr(B21), N.ptr(B22), N.ptr(bev), 0, N.ptr(ws),
-            wsb, N.stream_ptr()), "mf_offset_blocks")
+            wsb, N.stream_ptr(device=self.device)), "mf_offset_blocks")
         ev = bev.cpu().numpy()
         ids = np.nonzero(ev > 0)[0]
         t1 = ids % nproto
@@ -736,7 +767,7 @@ class AssemblyContext:
             N.ptr(b["B22"]), N.ptr(b["bev"]), N.ptr(om),
             N.ptr(plan.inner_sorted), cptr.ctypes.data_as(ctypes_void_p()),
             g1 - g0, float(scale), N.ptr(A._dvals), N.ptr(counters),
-            N.stream_ptr()), "mf_scatter_offset_blocks")
+            N.stream_ptr(device=self.device)), "mf_scatter_offset_blocks")
         return counters
 
     def block_a22(self, counters):
@@ -758,7 +789,7 @@ class AssemblyContext:
             C_byref(self.dmesh.struct), kcode, b["nproto"], b["R"],
             N.ptr(b["B21"]), N.ptr(b["B22"]), N.ptr(b["bev"]),
             N.ptr(b["a22"]), N.ptr(b["T"]), N.ptr(counters),
-            N.stream_ptr()), "mf_offset_block_a22")
+            N.stream_ptr(device=self.device)), "mf_offset_block_a22")
 
     def gather_blocks(self, A, row0, row1, scale=2.0):
         """Write vals rows [row0, row1) by the entry-wise gather
@@ -769,7 +800,7 @@ class AssemblyContext:
             C_byref(self.dmesh.struct), C_byref(A._pattern_struct()),
             b["kcode"], b["nproto"], b["R"], N.ptr(b["T"]), N.ptr(b["a22"]),
             int(row0), int(row1), float(scale), N.ptr(A._dvals),
-            N.stream_ptr()), "mf_gather_offset_blocks")
+            N.stream_ptr(device=self.device)), "mf_gather_offset_blocks")
 
     def run_blocked(self, A, scale=2.0, counters=None):
         """Offset-blocked strategy (assembly.py:391-437) on the device:
@@ -796,11 +827,11 @@ class AssemblyContext:
         out = torch.zeros(1, dtype=torch.float64, device=self.device)
         pat = A._pattern_struct()
         N.check(N.lib().mf_asymmetry_inf(C_byref(pat), N.ptr(A._dvals),
-                                          N.ptr(out), N.stream_ptr()),
+                                          N.ptr(out), N.stream_ptr(device=self.device)),
                 "mf_asymmetry_inf")
         if self.config.symmetrize:
             N.check(N.lib().mf_symmetrize(C_byref(pat), N.ptr(A._dvals),
-                                           N.stream_ptr()), "mf_symmetrize")
+                                           N.stream_ptr(device=self.device)), "mf_symmetrize")
         # wait on an event first: Event.synchronize releases the GIL, a
         # blocking .cpu() does not, and the streamed host copies
         # (run_streamed's worker threads) need it while the kernels run
@@ -809,10 +840,22 @@ class AssemblyContext:
         done.record(torch.cuda.current_stream(self.device))
         done.synchronize()
         cnt = counters.cpu().numpy()
+        check_counters(cnt)
         A.counters = cnt
         A.events = int(cnt[N.CNT_EVENTS])
         A.presym_asymmetry = float(out.item())
         return A
+
+
+def check_counters(cnt):
+    """Raise when a kernel flagged dropped work (MF_CNT_OVERFLOW): the
+    values would be incomplete (include/mollifem_b200.h)."""
+    from . import _native as N
+    if int(cnt[N.CNT_OVERFLOW]):
+        raise RuntimeError(
+            "assembly kernel overflow: more split sub-cells per level than "
+            "the specialised kernel buffers; the matrix is incomplete "
+            "(use flags=MF_FLAG_FORCE_GENERIC)")
 
 
 class WindowedValues:
@@ -870,15 +913,24 @@ def assemble(mesh, space, kernel, config=None, *, device=None, flags=0,
     per-pair path (mf_general_core).  keep_on_device=True skips the host copy (the
     values stay in `A.vals_device`; `A.vals` copies them on first use).
     """
+    import torch
+    from .device import _dev
     config = config or AssemblyConfig()
     if config.method == "barycenter":
         raise NotImplementedError(
             "the barycenter baseline (assembly.py:565-635) is outside the "
             "B200 hot path; use the reference package for it")
+    dev = _dev(device)
+    with torch.cuda.device(dev):
+        return _assemble_on(mesh, space, kernel, config, dev, flags,
+                            keep_on_device)
+
+
+def _assemble_on(mesh, space, kernel, config, device, flags, keep_on_device):
     ctx = AssemblyContext(mesh, space, kernel, config, device)
     A = ctx.new_matrix()
     strategy = resolve_strategy(mesh, config)
-    if keep_on_device or config.symmetrize:
+    if keep_on_device or config.symmetrize or A.nnz * 8 < _STREAM_MIN_BYTES:
         counters = (ctx.run_blocked(A) if strategy == "blocked"
                     else ctx.run(A, flags=flags))
         ctx.finish(A, counters)

@@ -10,7 +10,10 @@
 
 #include <algorithm>
 
+#include <vector>
+
 #include "mf_common.cuh"
+#include "mf_lists.cuh"
 
 cudaError_t mf_launch_candidates(const MfMesh &, const int64_t *, int64_t,
                                  const uint8_t *, int, double, int64_t *,
@@ -370,6 +373,159 @@ int mf_general_core(const MfMesh *mesh, const MfRules *rules,
     if (e != cudaSuccess) return cuda_status(e, "mf_general_core");
   }
   return MF_OK;
+}
+
+int mf_general_core_lists(const MfMesh *mesh, const MfRules *rules,
+                          const MfKernel *kern, const MfPattern *pat,
+                          const int64_t *outer_ids, int64_t n_outer,
+                          const int64_t *cand_ptr, const int64_t *cand_ids,
+                          double scale, double *vals, uint64_t *counters,
+                          int32_t flags, void *stream) {
+  if (!mesh) return fail(MF_ERR_ARG, "mesh is NULL");
+  if (mesh->dim != 2 && mesh->dim != 3) return fail(MF_ERR_ARG, "dim 2/3");
+  if (mesh->degree != 1 && mesh->degree != 2)
+    return fail(MF_ERR_ARG, "degree must be 1/2");
+  if (mesh->n_elem < 0 || mesh->nloc_max < 1)
+    return fail(MF_ERR_ARG, "bad mesh sizes");
+  if (mesh->n_elem > 0 && (!mesh->elem_kind || !mesh->elem_coords ||
+                           !mesh->elem_lo || !mesh->elem_hi ||
+                           !mesh->elem_dofs))
+    return fail(MF_ERR_ARG, "mesh array is NULL");
+  if (int rc = check_pattern(pat)) return rc;
+  if (!rules || !kern) return fail(MF_ERR_ARG, "rules/kernel is NULL");
+  if (kern->L_min < 1 || kern->L_min > kern->L_max || kern->L_max > 24)
+    return fail(MF_ERR_ARG, "need 1 <= L_min <= L_max <= 24");
+  if (!(kern->eps >= 0.0 && kern->eps < kern->delta))
+    return fail(MF_ERR_ARG, "need 0 <= eps < delta");
+  if (n_outer < 0) return fail(MF_ERR_ARG, "n_outer < 0");
+  if (!counters || !vals) return fail(MF_ERR_ARG, "vals/counters NULL");
+  if (n_outer == 0) return MF_OK;
+  if (!outer_ids || !cand_ptr || !cand_ids)
+    return fail(MF_ERR_ARG, "NULL list");
+  MF_CHECK_DEV(outer_ids);
+  MF_CHECK_DEV(cand_ptr);
+  MF_CHECK_DEV(cand_ids);
+  MF_CHECK_DEV(counters);
+  MF_CHECK_DEV(mesh->elem_dofs);
+  cudaStream_t s = S(stream);
+  // list bounds and outer ids (host checks: the reference has no bounds
+  // checks at all, a bad id there is a silent out-of-row write)
+  int64_t ends[2];
+  cudaError_t e = cudaMemcpyAsync(&ends[0], cand_ptr, 8,
+                                  cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(&ends[1], cand_ptr + n_outer, 8,
+                        cudaMemcpyDeviceToHost, s);
+  std::vector<int64_t> h_outer(n_outer);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(h_outer.data(), outer_ids, 8 * n_outer,
+                        cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_status(e, "mf_general_core_lists");
+  if (ends[0] != 0 || ends[1] < 0)
+    return fail(MF_ERR_ARG, "cand_ptr must start at 0 and be ascending");
+  for (int64_t v : h_outer)
+    if (v < 0 || v >= mesh->n_elem)
+      return fail(MF_ERR_ARG, "outer id out of range");
+  const int64_t npairs = ends[1];
+  if (npairs == 0) return MF_OK;
+  keep_pool();
+  MfLists Ls;
+  e = mf_lists_build(cand_ptr, cand_ids, outer_ids, n_outer, npairs,
+                     mesh->n_elem, mesh->elem_dofs, mesh->nloc_max, s, Ls);
+  if (e != cudaSuccess) {
+    mf_lists_free(Ls, s);
+    if (e == cudaErrorInvalidValue)
+      return fail(MF_ERR_ARG, "candidate id out of range");
+    return cuda_status(e, "mf_general_core_lists");
+  }
+  // greedy colouring of the inner elements by shared DOFs (64 colours at
+  // most): elements of one colour write disjoint rows, so each colour is
+  // one race-free launch (no atomics, deterministic)
+  const int64_t n_inner = Ls.n_inner;
+  const int nloc = mesh->nloc_max;
+  std::vector<uint64_t> used(pat->n, 0);
+  std::vector<int> colour(n_inner);
+  int ncol = 0;
+  for (int64_t t = 0; t < n_inner; t++) {
+    uint64_t busy = 0;
+    const int64_t *d = Ls.h_dofs.data() + t * nloc;
+    for (int j = 0; j < nloc; j++)
+      if (d[j] >= 0) {
+        if (d[j] >= pat->n) {
+          mf_lists_free(Ls, s);
+          return fail(MF_ERR_ARG, "element DOF outside the pattern");
+        }
+        busy |= used[d[j]];
+      }
+    if (busy == ~0ull) {
+      mf_lists_free(Ls, s);
+      return fail(MF_ERR_UNSUPPORTED, "more than 64 colours");
+    }
+    int c = __builtin_ctzll(~busy);
+    colour[t] = c;
+    ncol = std::max(ncol, c + 1);
+    for (int j = 0; j < nloc; j++)
+      if (d[j] >= 0) used[d[j]] |= 1ull << c;
+  }
+  std::vector<int64_t> cptr(ncol + 1, 0), start(n_inner, 0);
+  for (int64_t t = 0; t < n_inner; t++) cptr[colour[t] + 1]++;
+  for (int c = 0; c < ncol; c++) cptr[c + 1] += cptr[c];
+  for (int64_t t = 1; t < n_inner; t++)
+    start[t] = start[t - 1] + Ls.h_counts[t - 1];
+  std::vector<int32_t> h_inner(n_inner);
+  std::vector<int64_t> h_beg(n_inner), h_end(n_inner);
+  {
+    std::vector<int64_t> fill(cptr.begin(), cptr.end() - 1);
+    for (int64_t t = 0; t < n_inner; t++) {
+      const int64_t pos = fill[colour[t]]++;
+      h_inner[pos] = (int32_t)Ls.h_uniq[t];
+      h_beg[pos] = start[t];
+      h_end[pos] = start[t] + Ls.h_counts[t];
+    }
+  }
+  int32_t *d_inner = nullptr;
+  int64_t *d_be = nullptr;
+  double *gscr = nullptr;
+  const size_t wsb = mf_general_workspace_bytes(mesh, rules, n_inner);
+  e = cudaMallocAsync(&d_inner, 4 * n_inner, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&d_be, 16 * n_inner, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&gscr, wsb, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(gscr, 0, 256, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(d_inner, h_inner.data(), 4 * n_inner,
+                        cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(d_be, h_beg.data(), 8 * n_inner,
+                        cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(d_be + n_inner, h_end.data(), 8 * n_inner,
+                        cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) {
+    AsmParams P = make_params(mesh, rules, kern, pat, nullptr, 1, scale,
+                              vals, counters, flags);
+    P.overflow = reinterpret_cast<int32_t *>(gscr);
+    P.scratch =
+        reinterpret_cast<double *>(reinterpret_cast<char *>(gscr) + 256);
+    P.scratch_stride = nq_in_max(rules);
+    P.list_outer = Ls.list_outer;
+    for (int c = 0; c < ncol && e == cudaSuccess; c++) {
+      const int64_t n = cptr[c + 1] - cptr[c];
+      if (n <= 0) continue;
+      P.inner = d_inner + cptr[c];
+      P.list_begin = d_be + cptr[c];
+      P.list_end = d_be + n_inner + cptr[c];
+      P.n_inner = n;
+      int64_t want = (n + kGenericBlock - 1) / kGenericBlock;
+      int grid = (int)(want < kGenericMaxGrid ? want : kGenericMaxGrid);
+      e = mf_launch_generic(P, grid, kGenericBlock, s);
+    }
+  }
+  if (d_inner) cudaFreeAsync(d_inner, s);
+  if (d_be) cudaFreeAsync(d_be, s);
+  if (gscr) cudaFreeAsync(gscr, s);
+  mf_lists_free(Ls, s);
+  return cuda_status(e, "mf_general_core_lists");
 }
 
 int64_t mf_offset_block_count(int32_t dim, int32_t nproto, int32_t R) {

@@ -50,6 +50,10 @@ struct AsmParams {
   double *scratch;        // per-thread scratch (generic kernel)
   int64_t scratch_stride; // doubles per thread
   int32_t *overflow;      // set when a specialised kernel cannot proceed
+  // explicit pair lists (mf_general_core_lists, generic kernel only):
+  // inner element inner[t] pairs with outer list_outer[k] for k in
+  // [list_begin[t], list_end[t]); NULL = the cell-stencil product set
+  const int64_t *list_begin, *list_end, *list_outer;
 };
 
 // aprx_min (_kernels.py:80-90): largest single-axis gap, 0 when overlapping

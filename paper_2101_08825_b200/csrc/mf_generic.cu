@@ -370,20 +370,37 @@ __global__ void __launch_bounds__(128)
     }
     for (int q = 0; q < I.nq; q++) G[q] = 0.0;
     double Gall = 0.0;  // plateau contributions common to every q1
-    int cx, cy, cz;
-    cell_coords(M.elem_cell[m], M.ncx, M.ncy, cx, cy, cz);
-    const int R = P.R;
-    const int zlo = DIM == 3 ? max(cz - R, 0) : 0;
-    const int zhi = DIM == 3 ? min(cz + R, M.ncz - 1) : 0;
     const int64_t *mdofs = M.elem_dofs + (size_t)m * M.nloc_max;
+    // pair source: the explicit list of mf_general_core_lists (every
+    // listed pair runs, as _general_core does, _kernels.py:432-438), or
+    // the cell stencil filtered by the outer mask and the box gap
+    const bool listed = P.list_begin != nullptr;
+    int cx = 0, cy = 0, cz = 0;
+    if (!listed) cell_coords(M.elem_cell[m], M.ncx, M.ncy, cx, cy, cz);
+    const int R = listed ? 0 : P.R;
+    const int zlo = DIM == 3 && !listed ? max(cz - R, 0) : 0;
+    const int zhi = DIM == 3 && !listed ? min(cz + R, M.ncz - 1) : 0;
+    const int yhi = listed ? 0 : min(cy + R, M.ncy - 1);
+    const int xhi = listed ? 0 : min(cx + R, M.ncx - 1);
     for (int z2 = zlo; z2 <= zhi; z2++)
-      for (int y2 = max(cy - R, 0); y2 <= min(cy + R, M.ncy - 1); y2++)
-        for (int x2 = max(cx - R, 0); x2 <= min(cx + R, M.ncx - 1); x2++) {
-          const int64_t c2 = ((int64_t)z2 * M.ncy + y2) * M.ncx + x2;
-          for (int64_t l = M.cell_ptr[c2]; l < M.cell_ptr[c2 + 1]; l++) {
-            if (!P.outer_mask[l]) continue;
-            if (!(elem_gap<DIM>(M.elem_lo, M.elem_hi, l, m) < P.dpe))
-              continue;
+      for (int y2 = listed ? 0 : max(cy - R, 0); y2 <= yhi; y2++)
+        for (int x2 = listed ? 0 : max(cx - R, 0); x2 <= xhi; x2++) {
+          int64_t k0, k1;
+          if (listed) {
+            k0 = P.list_begin[t];
+            k1 = P.list_end[t];
+          } else {
+            const int64_t c2 = ((int64_t)z2 * M.ncy + y2) * M.ncx + x2;
+            k0 = M.cell_ptr[c2];
+            k1 = M.cell_ptr[c2 + 1];
+          }
+          for (int64_t k = k0; k < k1; k++) {
+            const int64_t l = listed ? P.list_outer[k] : k;
+            if (!listed) {
+              if (!P.outer_mask[l]) continue;
+              if (!(elem_gap<DIM>(M.elem_lo, M.elem_hi, l, m) < P.dpe))
+                continue;
+            }
             c_pairs++;
             Outer O;
             O.kind = M.elem_kind[l];

@@ -276,8 +276,8 @@ MF_DEV void event_full(const AsmParams &P, const double *s_rt,
         for (int c = 0; c < NO; c++) nsh += shl[c];
         nsh = __reduce_add_sync(0xffffffffu, nsh);
         if (lane == 0) {
-          atomicAdd(P.counters + 6, 1ull);
-          atomicAdd(P.counters + 7, (unsigned long long)nsh);
+          atomicAdd(P.counters + 8, 1ull);
+          atomicAdd(P.counters + 9, (unsigned long long)nsh);
         }
 #endif
         double v[NO];
@@ -558,7 +558,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MF_HEX_MINB)
             }
             __syncwarp();
             if (nnext > kSplitCap) {
-              if (lane == 0) atomicExch(P.overflow, 1);
+              // cannot hold the level: flag it (the host raises) rather
+              // than return a silently incomplete matrix
+              if (lane == 0) atomicAdd(P.counters + MF_CNT_OVERFLOW, 1ull);
               nnext = 0;
             }
             uint32_t *tmp = cur;

@@ -9,6 +9,8 @@ have the same (x, y, z) parity and the same triangle proto share no DOF
 colour is one atomic-free launch.
 """
 
+import threading
+
 import numpy as np
 
 from . import _native as N
@@ -37,14 +39,34 @@ def to_device(arr, device, pinned=True):
     return t.to(dev, non_blocking=True)
 
 
+def cell_ptr_of(mesh):
+    """(flat cell id per element, CSR of elements per cell).
+
+    Our meshes provide `cell_ptr()`; the reference's Mesh does not (its
+    `_cell_ptr(mesh)` is a free function, assembly.py:135-148), so for any
+    other mesh object the same arrays are computed here from `elem_cell`
+    and `grid_ncells` (elements are cell-lex ordered, mesh.py:209-253)."""
+    if hasattr(mesh, "cell_ptr"):
+        return mesh.cell_ptr()
+    c = np.asarray(mesh.elem_cell)
+    nc = mesh.grid_ncells
+    flat = c[:, 1].astype(np.int64) * nc[0] + c[:, 0]
+    if mesh.dim == 3:
+        flat += c[:, 2].astype(np.int64) * (nc[0] * nc[1])
+    flat = flat.astype(np.int32)
+    ncells = int(np.prod(nc))
+    return flat, np.searchsorted(flat, np.arange(ncells + 1)).astype(np.int64)
+
+
 class DeviceMesh:
-    """Mesh + FE space arrays in device memory."""
+    """Mesh + FE space arrays in device memory (our host layer's objects or
+    the reference's Mesh/FESpace, which carry the same SoA arrays)."""
 
     def __init__(self, mesh, space, device=None):
         dev = _dev(device)
         self.device = dev
         self.dim = mesh.dim
-        flat, cptr = mesh.cell_ptr()
+        flat, cptr = cell_ptr_of(mesh)
         nc = mesh.grid_ncells
         host = {
             "elem_kind": np.ascontiguousarray(mesh.elem_kind, np.int8),
@@ -77,25 +99,38 @@ class DeviceMesh:
 
 
 class DeviceRules:
-    """Rule/shape tables of a `PrepTables` in device memory."""
+    """Rule/shape tables of a `PrepTables` (or of the reference's `_Prep`,
+    assembly.py:333-356) in device memory.
 
-    def __init__(self, prep, device=None):
+    The specialised box kernels sum-factorise over the 1D factors of the
+    tensor rules.  `PrepTables` carries them; for the reference's `_Prep`,
+    which does not, pass `box_1d=(outer_1d, inner_1d)` (e.g. from
+    `assembly.rule_1d(config.outer_rule)`) or leave them out, which sends
+    box meshes to the generic kernel (n1d = 0)."""
+
+    def __init__(self, prep, device=None, box_1d=None):
         dev = _dev(device)
         names = ["box_out_pts", "box_out_w", "box_in_pts", "box_in_w",
                  "tri_out_pts", "tri_out_w", "tri_in_pts", "tri_in_w"]
         host = {n: getattr(prep, n) for n in names}
         host["phi_box_in"] = prep.PHI_box_in
         host["phi_tri_in"] = prep.PHI_tri_in
-        host["box_out_x1d"], host["box_out_w1d"] = prep.box_out_1d
-        host["box_in_x1d"], host["box_in_w1d"] = prep.box_in_1d
+        if box_1d is None:
+            box_1d = (getattr(prep, "box_out_1d", None),
+                      getattr(prep, "box_in_1d", None))
+        empty = (np.zeros(1), np.zeros(1))
+        o1, i1 = (b if b is not None else empty for b in box_1d)
+        host["box_out_x1d"], host["box_out_w1d"] = o1
+        host["box_in_x1d"], host["box_in_w1d"] = i1
+        n1d_out = len(o1[0]) if box_1d[0] is not None else 0
+        n1d_in = len(i1[0]) if box_1d[1] is not None else 0
         self.t = {k: to_device(np.ascontiguousarray(v, np.float64), dev,
                                pinned=False) for k, v in host.items()}
         p = {k: v.data_ptr() for k, v in self.t.items()}
         self.struct = N.MfRules(
             nq_box_out=len(prep.box_out_w), nq_box_in=len(prep.box_in_w),
             nq_tri_out=len(prep.tri_out_w), nq_tri_in=len(prep.tri_in_w),
-            n1d_box_out=len(prep.box_out_1d[0]),
-            n1d_box_in=len(prep.box_in_1d[0]), **p)
+            n1d_box_out=n1d_out, n1d_box_in=n1d_in, **p)
 
 
 def _nproto(mesh):
@@ -186,16 +221,25 @@ class HostStager:
     CHUNK = 1 << 25          # doubles per staging chunk (256 MiB)
     NBUF = 4
     _rings = {}
+    _locks = {}
+    _guard = threading.Lock()
 
     def __init__(self, device, threads=16):
         import torch
         self.device = torch.device(device)
         key = str(self.device)
-        if key not in HostStager._rings:
-            HostStager._rings[key] = [
-                torch.empty(self.CHUNK, dtype=torch.float64, pin_memory=True)
-                for _ in range(self.NBUF)]
+        with HostStager._guard:
+            if key not in HostStager._rings:
+                HostStager._rings[key] = [
+                    torch.empty(self.CHUNK, dtype=torch.float64,
+                                pin_memory=True)
+                    for _ in range(self.NBUF)]
+                HostStager._locks[key] = threading.Lock()
         self.ring = HostStager._rings[key]
+        # one transfer at a time per device: the ring is shared by every
+        # caller in the process (two concurrent copies would interleave
+        # their chunks in the same staging buffers)
+        self.lock = HostStager._locks[key]
         self.stream = torch.cuda.Stream(device=self.device)
         self.threads = threads
 
@@ -211,7 +255,12 @@ class HostStager:
             list(pool.map(touch, range(0, n, chunk)))
 
     def run(self, src, host, ranges):
-        """Copy src[a:b] -> host[a:b] for each (event, a, b), in order."""
+        """Copy src[a:b] -> host[a:b] for each (event, a, b), in order
+        (serialised per device: the staging ring is shared)."""
+        with self.lock:
+            self._run(src, host, ranges)
+
+    def _run(self, src, host, ranges):
         import torch
         from concurrent.futures import ThreadPoolExecutor
         import os

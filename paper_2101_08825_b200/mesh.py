@@ -437,6 +437,7 @@ def _greedy_colors(elem_nodes, n_nodes, seed=0):
     src = np.concatenate(src) if src else np.zeros(0, np.int64)
     dst = np.concatenate(dst) if dst else np.zeros(0, np.int64)
     # (pairs sharing two vertices appear twice; harmless below)
+    src0, dst0 = src, dst
     rng = np.random.default_rng(seed)
     prio = rng.permutation(n)
     color = np.full(n, -1, dtype=np.int64)
@@ -458,8 +459,15 @@ def _greedy_colors(elem_nodes, n_nodes, seed=0):
         np.bitwise_or.at(used, src[cs], np.int64(1) << color[dst[cs]])
         ids = np.nonzero(pick)[0]
         u = used[ids]
+        if (u >= np.int64(1) << 61).any() or (u < 0).any():
+            # int64 masks hold 61 colours safely (1 << 62 would overflow)
+            raise RuntimeError("greedy colouring needs more than 61 colours")
         low = ~u & (u + 1)               # lowest clear bit = smallest free
         color[ids] = np.log2(low.astype(np.float64)).astype(np.int64)
+    # every colour class must be vertex-disjoint (the kernels' writes to a
+    # colour are non-atomic): no edge may join two elements of one colour
+    if (color[src0] == color[dst0]).any():
+        raise RuntimeError("colouring is not vertex-disjoint")
     return color
 
 

@@ -31,6 +31,7 @@ import time
 
 import numpy as np
 
+from . import _native as N
 from .assembly import (AssemblyConfig, AssemblyContext, SparseMatrix,
                        pattern_halfwidth)
 from .mesh import partition_geometric
@@ -163,7 +164,8 @@ def parallel_assemble(mesh, space, kernel, config=None, n_parts=1,
         A._dvals[sel] = acc
         c.t_t = time.perf_counter() - t_start
     A._dvals *= 2.0
-    counters = torch.zeros(8, dtype=torch.int64, device=A._dvals.device)
+    counters = torch.zeros(N.MF_NCOUNTERS, dtype=torch.int64,
+                           device=A._dvals.device)
     counters[0] = sum(c.events for c in contexts)
     ctx.finish(A, counters)
     from .assembly import _d2h
@@ -350,7 +352,7 @@ class SlabAssembler:
         # default plan) when the caller has the pair-count weights
         self.color_plan = ColorPlan(mesh, self.inner, self.ctx.device,
                                     work=weights)
-        self.counters = torch.zeros(8, dtype=torch.int64,
+        self.counters = torch.zeros(N.MF_NCOUNTERS, dtype=torch.int64,
                                     device=self.ctx.device)
 
     def assemble_local(self):

@@ -20,7 +20,7 @@ def test_library_exports_header_symbols():
     for n in names:
         assert hasattr(L, n), n
     assert set(names) == set(N.EXPORTED)
-    assert L.mf_abi_version() == 2
+    assert L.mf_abi_version() == N.ABI_VERSION == 3
 
 
 def test_library_is_sm100a_only():
