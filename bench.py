@@ -64,6 +64,9 @@ CONFIGS = {
                   "gauss2"),
     "R4-small": (3, ((0.0, 0.25),) * 3, 1 / 64, 0.1, 1 / 128, 2.0, "hex", 2,
                  "default"),
+    # Omega = [0, 0.5]^3 (46^3 hexes): kernel A/B timing stand-in for R4
+    "R4-half": (3, ((0.0, 0.5),) * 3, 1 / 64, 0.1, 1 / 128, 2.0, "hex", 2,
+                "default"),
     "R5": (3, ((0.0, 1.0),) * 3, 1 / 128, 4 / 128, 1 / 512, 2.0, "hex", 2,
            "default"),
     # BASELINE config #4 as written: 6-tet P1 cubes, 4-point tet rule

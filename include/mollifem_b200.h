@@ -232,6 +232,12 @@ int mf_scale(double *vals, int64_t nnz, double s, void *stream);
 /* out: device double[1]; max over rows of sum_c |A_rc - A_cr| */
 int mf_asymmetry_inf(const MfPattern *pat, const double *vals, double *out,
                      void *stream);
+/* the same over rows [row0, row1) only: vals may be a window pointer
+ * (shifted by its base) holding every row within K grid planes of the
+ * range (distributed row blocks, parallel.py) */
+int mf_asymmetry_inf_rows(const MfPattern *pat, const double *vals,
+                          int64_t row0, int64_t row1, double *out,
+                          void *stream);
 int mf_norm_inf(const MfPattern *pat, const double *vals, double *out,
                 void *stream);
 int mf_matvec(const MfPattern *pat, const double *vals, const double *x,
@@ -251,6 +257,50 @@ int mf_load_scatter(const MfMesh *mesh, const int32_t *elems,
                     const int64_t *color_ptr, int32_t ncolors,
                     const double *fval, const double *w, const double *phi,
                     int32_t nq, int32_t nloc, double *load, void *stream);
+
+/* Device solver and glue (solver.py:26-90, assembly.py:679-691,
+ * parallel.py:180-200).  Reductions are deterministic (fixed grid, block
+ * partials summed in block order); ws: device scratch of at least
+ * mf_vec_workspace_bytes() bytes; every out is a device double array.
+ *   mf_cg_matvec_dot  Ap = A p with rows where cmask != 0 zeroed;
+ *                     out[0] = p.Ap
+ *   mf_cg_update      x += alpha p; r -= alpha Ap; z = dinv r;
+ *                     out[0] = r.r, out[1] = r.z
+ *   mf_cg_direction   p = z + beta p
+ *   mf_jacobi_inverse dinv = cmask ? 0 : 1/diag; out[0] = min free diag
+ *   mf_gather_diff    out[k] = a[idx[k]] - b[idx[k]] (b may be NULL)
+ *   mf_scatter_values out[idx[k]] = v[k]
+ *   mf_sum_ordered    out = scale * (bufs[0] + bufs[1] + ...) summed in
+ *                     buffer order (bufs: HOST array of <= 64 device
+ *                     pointers)
+ *   mf_row_touched    flags[r] = row r holds a nonzero value */
+size_t mf_vec_workspace_bytes(void);
+int mf_cg_matvec_dot(const MfPattern *pat, const double *vals,
+                     const double *p, const uint8_t *cmask, double *Ap,
+                     double *out, void *ws, void *stream);
+int mf_cg_update(int64_t n, double alpha, const double *p, const double *Ap,
+                 const double *dinv, double *x, double *r, double *z,
+                 double *out, void *ws, void *stream);
+int mf_cg_direction(int64_t n, double beta, const double *z, double *p,
+                    void *stream);
+int mf_jacobi_inverse(int64_t n, const double *diag, const uint8_t *cmask,
+                      double *dinv, double *out_min_free, void *ws,
+                      void *stream);
+int mf_gather_diff(int64_t n_sel, const int64_t *idx, const double *a,
+                   const double *b, double *out, void *stream);
+int mf_scatter_values(int64_t n_sel, const int64_t *idx, const double *v,
+                      double *out, void *stream);
+int mf_sum_ordered(int32_t nbuf, const double *const *bufs, int64_t n,
+                   double scale, double *out, void *stream);
+int mf_row_touched(const MfPattern *pat, const double *vals, uint8_t *flags,
+                   void *stream);
+/* out = a x + b y (out may alias x or y) */
+int mf_axpby(int64_t n, double a, const double *x, double b,
+             const double *y, double *out, void *stream);
+/* y[r] = (A x)[r] for rows [row0, row1) only; vals may be a window
+ * pointer holding those rows (distributed row blocks) */
+int mf_matvec_rows(const MfPattern *pat, const double *vals, const double *x,
+                   int64_t row0, int64_t row1, double *y, void *stream);
 
 /* FP64 roofline probe: independent DFMA chains; out = device double[1]
  * (sink).  Time it with events to get the sustained DFMA rate. */

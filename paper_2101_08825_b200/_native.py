@@ -103,6 +103,8 @@ _SIGS = {
                                           _P, _P]),
     "mf_scale": (C.c_int, [_P, C.c_int64, C.c_double, _P]),
     "mf_asymmetry_inf": (C.c_int, [C.POINTER(MfPattern), _P, _P, _P]),
+    "mf_asymmetry_inf_rows": (C.c_int, [C.POINTER(MfPattern), _P, C.c_int64,
+                                        C.c_int64, _P, _P]),
     "mf_norm_inf": (C.c_int, [C.POINTER(MfPattern), _P, _P, _P]),
     "mf_matvec": (C.c_int, [C.POINTER(MfPattern), _P, _P, _P, _P]),
     "mf_diag": (C.c_int, [C.POINTER(MfPattern), _P, _P, _P]),
@@ -110,6 +112,22 @@ _SIGS = {
     "mf_fill_cols": (C.c_int, [C.POINTER(MfPattern), _P, _P]),
     "mf_load_scatter": (C.c_int, [C.POINTER(MfMesh), _P, _P, C.c_int32, _P,
                                   _P, _P, C.c_int32, C.c_int32, _P, _P]),
+    "mf_vec_workspace_bytes": (C.c_size_t, []),
+    "mf_cg_matvec_dot": (C.c_int, [C.POINTER(MfPattern), _P, _P, _P, _P, _P,
+                                   _P, _P]),
+    "mf_cg_update": (C.c_int, [C.c_int64, C.c_double, _P, _P, _P, _P, _P, _P,
+                               _P, _P, _P]),
+    "mf_cg_direction": (C.c_int, [C.c_int64, C.c_double, _P, _P, _P]),
+    "mf_jacobi_inverse": (C.c_int, [C.c_int64, _P, _P, _P, _P, _P, _P]),
+    "mf_gather_diff": (C.c_int, [C.c_int64, _P, _P, _P, _P, _P]),
+    "mf_scatter_values": (C.c_int, [C.c_int64, _P, _P, _P, _P]),
+    "mf_sum_ordered": (C.c_int, [C.c_int32, C.POINTER(C.c_void_p),
+                                 C.c_int64, C.c_double, _P, _P]),
+    "mf_row_touched": (C.c_int, [C.POINTER(MfPattern), _P, _P, _P]),
+    "mf_axpby": (C.c_int, [C.c_int64, C.c_double, _P, C.c_double, _P, _P,
+                           _P]),
+    "mf_matvec_rows": (C.c_int, [C.POINTER(MfPattern), _P, _P, C.c_int64,
+                                 C.c_int64, _P, _P]),
     "mf_fp64_probe": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_int32, _P]),
     "mf_fp64_probe_flops": (C.c_double, [C.c_int64, C.c_int32, C.c_int32]),
     "mf_last_error": (C.c_char_p, []),

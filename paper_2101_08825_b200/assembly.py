@@ -481,7 +481,7 @@ def candidates(mesh, reach, outer_ids, inner_mask, device=None,
     mask = to_device(np.ascontiguousarray(inner_mask, np.uint8), dev)
     n = int(outer.numel())
     R = stencil_radius(reach + stencil_pad(mesh), mesh.h)
-    st = N.stream_ptr()
+    st = N.stream_ptr(device=dev)
     counts = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
     N.check(L.mf_count_candidates(C_byref(dmesh.struct), N.ptr(outer), n,
                                   N.ptr(mask), R, float(reach), N.ptr(counts),
@@ -1014,7 +1014,7 @@ def group_load_device(mesh, space, f, element_ids, dmesh, device=None):
             C_byref(dmesh.struct), N.ptr(elems),
             cptr.ctypes.data_as(ctypes_void_p()), ncol,
             N.ptr(fvd), N.ptr(wd), N.ptr(phid), len(rule), PHI.shape[1],
-            N.ptr(load), N.stream_ptr()), "mf_load_scatter")
+            N.ptr(load), N.stream_ptr(device=dev)), "mf_load_scatter")
     return load
 
 
@@ -1024,9 +1024,16 @@ def assemble_rhs(mesh, space, kernel, f, g, A):
     gt is the nodal interpolant of g on constrained DOFs (callable, or an
     array over all DOFs / constrained DOFs), zero elsewhere."""
     import torch
+    dev = A.vals_device.device
+    with torch.cuda.device(dev):
+        return _assemble_rhs_on(mesh, space, f, g, A, dev)
+
+
+def _assemble_rhs_on(mesh, space, f, g, A, dev):
+    import torch
     from . import _native as N
     from .device import DeviceMesh, to_device
-    dmesh = DeviceMesh(mesh, space)
+    dmesh = DeviceMesh(mesh, space, dev)
     load = group_load_device(mesh, space, f, mesh.omega_element_ids(), dmesh)
     gt = np.zeros(space.n_dofs)
     if callable(g):
@@ -1035,10 +1042,15 @@ def assemble_rhs(mesh, space, kernel, f, g, A):
         gv = np.asarray(g, dtype=float)
         gt[space.constrained] = (gv[space.constrained]
                                  if gv.shape == (space.n_dofs,) else gv)
-    gtd = to_device(gt, dmesh.device)
+    gtd = to_device(gt, dev)
     y = torch.empty_like(gtd)
-    N.check(N.lib().mf_matvec(C_byref(A._pattern_struct()),
-                              N.ptr(A.vals_device), N.ptr(gtd), N.ptr(y),
-                              N.stream_ptr()), "mf_matvec")
-    free = to_device(np.asarray(space.free, dtype=np.int64), dmesh.device)
-    return (load[free] - y[free]).cpu().numpy()
+    st = N.stream_ptr(device=dev)
+    L = N.lib()
+    N.check(L.mf_matvec(C_byref(A._pattern_struct()), N.ptr(A.vals_device),
+                        N.ptr(gtd), N.ptr(y), st), "mf_matvec")
+    free = np.asarray(space.free, dtype=np.int64)
+    free_d = to_device(free, dev)
+    out = torch.empty(len(free), dtype=torch.float64, device=dev)
+    N.check(L.mf_gather_diff(len(free), N.ptr(free_d), N.ptr(load), N.ptr(y),
+                             N.ptr(out), st), "mf_gather_diff")
+    return out.cpu().numpy()

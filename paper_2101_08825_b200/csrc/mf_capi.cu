@@ -54,6 +54,8 @@ cudaError_t mf_launch_asym(const MfPattern &, const double *, double *,
                            cudaStream_t);
 cudaError_t mf_launch_norm(const MfPattern &, const double *, double *,
                            cudaStream_t);
+cudaError_t mf_launch_asym_rows(const MfPattern &, const double *, int64_t,
+                                int64_t, double *, cudaStream_t);
 cudaError_t mf_launch_matvec(const MfPattern &, const double *,
                              const double *, double *, cudaStream_t);
 cudaError_t mf_launch_symmetrize(const MfPattern &, double *, cudaStream_t);
@@ -62,6 +64,31 @@ cudaError_t mf_launch_diag(const MfPattern &, const double *, double *,
                            cudaStream_t);
 cudaError_t mf_launch_scale(double *, int64_t, double, cudaStream_t);
 cudaError_t mf_launch_probe(double *, int64_t, int, int, cudaStream_t);
+size_t mf_vec_ws_bytes();
+cudaError_t mf_launch_cg_matvec_dot(const MfPattern &, const double *,
+                                    const double *, const uint8_t *, double *,
+                                    double *, double *, cudaStream_t);
+cudaError_t mf_launch_cg_update(int64_t, double, const double *,
+                                const double *, const double *, double *,
+                                double *, double *, double *, double *,
+                                cudaStream_t);
+cudaError_t mf_launch_cg_direction(int64_t, double, const double *, double *,
+                                   cudaStream_t);
+cudaError_t mf_launch_jacobi(int64_t, const double *, const uint8_t *,
+                             double *, double *, double *, cudaStream_t);
+cudaError_t mf_launch_gather_diff(int64_t, const int64_t *, const double *,
+                                  const double *, double *, cudaStream_t);
+cudaError_t mf_launch_scatter(int64_t, const int64_t *, const double *,
+                              double *, cudaStream_t);
+cudaError_t mf_launch_sum_ordered(int, const double *const *, int64_t, double,
+                                  double *, cudaStream_t);
+cudaError_t mf_launch_row_touched(const MfPattern &, const double *,
+                                  uint8_t *, cudaStream_t);
+cudaError_t mf_launch_axpby(int64_t, double, const double *, double,
+                            const double *, double *, cudaStream_t);
+cudaError_t mf_launch_matvec_rows(const MfPattern &, const double *,
+                                  const double *, int64_t, int64_t, double *,
+                                  cudaStream_t);
 cudaError_t mf_launch_load(const MfMesh &, const int32_t *, int64_t,
                            const double *, const double *, const double *,
                            int, int, double *, cudaStream_t);
@@ -674,6 +701,19 @@ int mf_asymmetry_inf(const MfPattern *pat, const double *vals, double *out,
                      "mf_asymmetry_inf");
 }
 
+int mf_asymmetry_inf_rows(const MfPattern *pat, const double *vals,
+                          int64_t row0, int64_t row1, double *out,
+                          void *stream) {
+  if (int rc = check_pattern(pat)) return rc;
+  if (!vals || !out) return fail(MF_ERR_ARG, "NULL array");
+  if (row0 < 0 || row1 > pat->n || row0 > row1)
+    return fail(MF_ERR_ARG, "bad row range");
+  MF_CHECK_DEV(out);
+  return cuda_status(mf_launch_asym_rows(*pat, vals, row0, row1, out,
+                                         S(stream)),
+                     "mf_asymmetry_inf_rows");
+}
+
 int mf_norm_inf(const MfPattern *pat, const double *vals, double *out,
                 void *stream) {
   if (int rc = check_pattern(pat)) return rc;
@@ -738,6 +778,110 @@ int mf_load_scatter(const MfMesh *mesh, const int32_t *elems,
     if (e != cudaSuccess) return cuda_status(e, "mf_load_scatter");
   }
   return MF_OK;
+}
+
+size_t mf_vec_workspace_bytes(void) { return mf_vec_ws_bytes(); }
+
+int mf_cg_matvec_dot(const MfPattern *pat, const double *vals,
+                     const double *p, const uint8_t *cmask, double *Ap,
+                     double *out, void *ws, void *stream) {
+  if (int rc = check_pattern(pat)) return rc;
+  if (!vals || !p || !cmask || !Ap || !out || !ws)
+    return fail(MF_ERR_ARG, "NULL array");
+  MF_CHECK_DEV(vals);
+  MF_CHECK_DEV(Ap);
+  return cuda_status(
+      mf_launch_cg_matvec_dot(*pat, vals, p, cmask, Ap, out,
+                              static_cast<double *>(ws), S(stream)),
+      "mf_cg_matvec_dot");
+}
+
+int mf_cg_update(int64_t n, double alpha, const double *p, const double *Ap,
+                 const double *dinv, double *x, double *r, double *z,
+                 double *out, void *ws, void *stream) {
+  if (n < 0 || (n > 0 && (!p || !Ap || !dinv || !x || !r || !z)) || !out ||
+      !ws)
+    return fail(MF_ERR_ARG, "bad cg update arguments");
+  return cuda_status(mf_launch_cg_update(n, alpha, p, Ap, dinv, x, r, z, out,
+                                         static_cast<double *>(ws),
+                                         S(stream)),
+                     "mf_cg_update");
+}
+
+int mf_cg_direction(int64_t n, double beta, const double *z, double *p,
+                    void *stream) {
+  if (n < 0 || (n > 0 && (!z || !p)))
+    return fail(MF_ERR_ARG, "bad cg direction arguments");
+  return cuda_status(mf_launch_cg_direction(n, beta, z, p, S(stream)),
+                     "mf_cg_direction");
+}
+
+int mf_jacobi_inverse(int64_t n, const double *diag, const uint8_t *cmask,
+                      double *dinv, double *out_min_free, void *ws,
+                      void *stream) {
+  if (n < 0 || (n > 0 && (!diag || !cmask || !dinv)) || !out_min_free || !ws)
+    return fail(MF_ERR_ARG, "bad jacobi arguments");
+  return cuda_status(mf_launch_jacobi(n, diag, cmask, dinv, out_min_free,
+                                      static_cast<double *>(ws), S(stream)),
+                     "mf_jacobi_inverse");
+}
+
+int mf_gather_diff(int64_t n_sel, const int64_t *idx, const double *a,
+                   const double *b, double *out, void *stream) {
+  if (n_sel < 0 || (n_sel > 0 && (!idx || !a || !out)))
+    return fail(MF_ERR_ARG, "bad gather arguments");
+  return cuda_status(mf_launch_gather_diff(n_sel, idx, a, b, out, S(stream)),
+                     "mf_gather_diff");
+}
+
+int mf_scatter_values(int64_t n_sel, const int64_t *idx, const double *v,
+                      double *out, void *stream) {
+  if (n_sel < 0 || (n_sel > 0 && (!idx || !v || !out)))
+    return fail(MF_ERR_ARG, "bad scatter arguments");
+  return cuda_status(mf_launch_scatter(n_sel, idx, v, out, S(stream)),
+                     "mf_scatter_values");
+}
+
+int mf_sum_ordered(int32_t nbuf, const double *const *bufs, int64_t n,
+                   double scale, double *out, void *stream) {
+  if (nbuf < 1 || nbuf > 64 || !bufs || n < 0 || (n > 0 && !out))
+    return fail(MF_ERR_ARG, "bad buffer-sum arguments");
+  for (int k = 0; k < nbuf; k++)
+    if (n > 0 && !bufs[k]) return fail(MF_ERR_ARG, "NULL buffer");
+  return cuda_status(mf_launch_sum_ordered(nbuf, bufs, n, scale, out,
+                                           S(stream)),
+                     "mf_sum_ordered");
+}
+
+int mf_row_touched(const MfPattern *pat, const double *vals, uint8_t *flags,
+                   void *stream) {
+  if (int rc = check_pattern(pat)) return rc;
+  if (!vals || !flags) return fail(MF_ERR_ARG, "NULL array");
+  MF_CHECK_DEV(vals);
+  MF_CHECK_DEV(flags);
+  return cuda_status(mf_launch_row_touched(*pat, vals, flags, S(stream)),
+                     "mf_row_touched");
+}
+
+int mf_axpby(int64_t n, double a, const double *x, double b,
+             const double *y, double *out, void *stream) {
+  if (n < 0 || (n > 0 && (!x || !y || !out)))
+    return fail(MF_ERR_ARG, "bad axpby arguments");
+  return cuda_status(mf_launch_axpby(n, a, x, b, y, out, S(stream)),
+                     "mf_axpby");
+}
+
+int mf_matvec_rows(const MfPattern *pat, const double *vals, const double *x,
+                   int64_t row0, int64_t row1, double *y, void *stream) {
+  if (int rc = check_pattern(pat)) return rc;
+  if (!vals || !x || !y) return fail(MF_ERR_ARG, "NULL array");
+  if (row0 < 0 || row1 > pat->n || row0 > row1)
+    return fail(MF_ERR_ARG, "bad row range");
+  MF_CHECK_DEV(x);
+  MF_CHECK_DEV(y);
+  return cuda_status(mf_launch_matvec_rows(*pat, vals, x, row0, row1, y,
+                                           S(stream)),
+                     "mf_matvec_rows");
 }
 
 int mf_fp64_probe(double *out, int64_t iters, int32_t blocks,

@@ -41,6 +41,9 @@ constexpr int kSplitCap = 64;  // split nodes per level (L_max <= 4)
 #ifndef MF_HEX_GROUP
 #define MF_HEX_GROUP 3
 #endif
+#ifndef MF_HEX_SHELLQ
+#define MF_HEX_SHELLQ 0
+#endif
 
 struct Box {
   double lo[3], hi[3];
@@ -315,14 +318,130 @@ MF_DEV void event_full(const AsmParams &P, const double *s_rt,
   __syncwarp();
 }
 
+#if MF_HEX_SHELLQ
+// Full event with the shell mollifier evaluated on a warp-compacted queue
+// (eps > 0).  Per outer x node a: every lane classifies its NO^2 point
+// pairs (plateau / shell / beyond) by the high word of the exact d2; the
+// lanes' shell d2 values are appended to a per-warp shared-memory queue at
+// warp-prefix-sum offsets; the warp evaluates the queue 32 entries per
+// round (all lanes busy, instead of NO polynomials per (a, b) line whenever
+// one lane of 27 needs one); each lane reads its shell values back in its
+// own order and contracts as event_full does.
+template <int NO>
+MF_DEV void event_full_q(const AsmParams &P, const double *s_rt,
+                         const double *s_rw, WarpCtx<NO> &C, int slot,
+                         const double y[3], int lane, double V[8],
+                         double *q) {
+  event_axes<NO>(P, s_rt, s_rw, C, slot, lane);
+  double sq1[NO], sq2[NO];
+#pragma unroll
+  for (int b = 0; b < NO; b++) {
+    const double d1 = xsub(C.X[1][b], y[1]);
+    const double d2 = xsub(C.X[2][b], y[2]);
+    sq1[b] = xmul(d1, d1);
+    sq2[b] = xmul(d2, d2);
+  }
+#pragma unroll 1
+  for (int a = 0; a < NO; a++) {
+    const double d0 = xsub(C.X[0][a], y[0]);
+    const double sq0 = xmul(d0, d0);
+    double d2v[NO * NO];
+    unsigned plm = 0, shm = 0;
+#pragma unroll
+    for (int b = 0; b < NO; b++) {
+      const double sxy = xadd(sq0, sq1[b]);
+#pragma unroll
+      for (int c = 0; c < NO; c++) {
+        const double d2 = xadd(sxy, sq2[c]);
+        d2v[b * NO + c] = d2;
+        const int hi = __double2hiint(d2);
+        const bool pl = hi < P.hi_dm2;
+        const bool sh = !pl && hi <= P.hi_dp2;
+        plm |= (unsigned)pl << (b * NO + c);
+        shm |= (unsigned)sh << (b * NO + c);
+      }
+    }
+    // warp prefix sum of the shell counts -> this lane's queue offset
+    const int n = __popc(shm);
+    int incl = n;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += t;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    const int base = incl - n;
+    if (total > 0) {
+      int k = base;
+#pragma unroll
+      for (int p = 0; p < NO * NO; p++)
+        if ((shm >> p) & 1u) q[k++] = d2v[p];
+      __syncwarp();
+      // evaluate the queue, two entries per lane at a time (independent
+      // DP chains interleave); entries past `total` are computed on stale
+      // data and never stored
+      const int rounds = (total + 31) >> 5;
+      int r = 0;
+      for (; r + 1 < rounds; r += 2) {
+        const int g0 = (r << 5) + lane, g1 = g0 + 32;
+        double d2[2] = {q[g0], q[g1 < total ? g1 : g0]};
+        double v[2];
+        xi256_unclamped_n<2>(P, d2, v);
+        q[g0] = v[0];
+        if (g1 < total) q[g1] = v[1];
+      }
+      if (r < rounds) {
+        const int g0 = (r << 5) + lane;
+        if (g0 < total) q[g0] = xi256_unclamped(P, q[g0]);
+      }
+      __syncwarp();
+    }
+    double W[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // [jy][jz]
+    int k = base;
+#pragma unroll
+    for (int b = 0; b < NO; b++) {
+      double u0 = 0.0, u1 = 0.0;  // z contraction
+#pragma unroll
+      for (int c = 0; c < NO; c++) {
+        const int p = b * NO + c;
+        double mu = ((plm >> p) & 1u) ? 256.0 : 0.0;
+        if ((shm >> p) & 1u) mu = q[k++];
+        u0 = fma(mu, C.sh[2][0][c], u0);
+        u1 = fma(mu, C.sh[2][1][c], u1);
+      }
+#pragma unroll
+      for (int jy = 0; jy < 2; jy++) {
+        const double wy = C.sh[1][jy][b];
+        W[jy][0] = fma(u0, wy, W[jy][0]);
+        W[jy][1] = fma(u1, wy, W[jy][1]);
+      }
+    }
+    const double x0 = C.sh[0][0][a], x1 = C.sh[0][1][a];
+#pragma unroll
+    for (int jz = 0; jz < 2; jz++)
+#pragma unroll
+      for (int jy = 0; jy < 2; jy++) {
+        V[2 * jy + 4 * jz] = fma(x0, W[jy][jz], V[2 * jy + 4 * jz]);
+        V[1 + 2 * jy + 4 * jz] = fma(x1, W[jy][jz], V[1 + 2 * jy + 4 * jz]);
+      }
+    __syncwarp();  // the next node reuses the queue
+  }
+}
+#endif
+
 template <int NO>
 MF_DEV void run_full(const AsmParams &P, const double *s_rt,
                      const double *s_rw, WarpCtx<NO> &C, int slot,
-                     const double y[3], int lane, bool active, double V[8]) {
+                     const double y[3], int lane, bool active, double V[8],
+                     double *q) {
   if (P.eps == 0.0)
     event_full<NO, true>(P, s_rt, s_rw, C, slot, y, lane, V);
   else
+#if MF_HEX_SHELLQ
+    event_full_q<NO>(P, s_rt, s_rw, C, slot, y, lane, V, q);
+#else
     event_full<NO, false>(P, s_rt, s_rw, C, slot, y, lane, V);
+#endif
 }
 
 template <int NO, int NI>
@@ -335,6 +454,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MF_HEX_MINB)
   __shared__ WarpCtx<NO> s_ctx[kWarpsPerBlock];
   __shared__ double s_buf[kWarpsPerBlock][NQ1][9];
   __shared__ uint32_t s_split[kWarpsPerBlock][2][kSplitCap];
+#if MF_HEX_SHELLQ
+  __shared__ double s_q[kWarpsPerBlock][NO * NO * 32];
+  double *q = s_q[threadIdx.x >> 5];
+#else
+  double *q = nullptr;
+#endif
 
   const MfMesh &M = P.mesh;
   const MfRules &Rr = P.rules;
@@ -495,7 +620,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MF_HEX_MINB)
           ev++;
           live = true;
           (act == ACT_FULL ? c_full : c_up)++;
-          run_full<NO>(P, s_rt, s_rw, C, 32, y, lane, active, V);
+          run_full<NO>(P, s_rt, s_rw, C, 32, y, lane, active, V, q);
         } else if (act == ACT_DEAD) {
           ev++;
           c_dead++;
@@ -554,7 +679,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MF_HEX_MINB)
                 event_plateau<NO>(P, s_rt, s_rw, C, __ffs(mm) - 1, lane, V);
               for (unsigned mm = mfull; mm; mm &= mm - 1)
                 run_full<NO>(P, s_rt, s_rw, C, __ffs(mm) - 1, y, lane,
-                             active, V);
+                             active, V, q);
             }
             __syncwarp();
             if (nnext > kSplitCap) {

@@ -73,6 +73,26 @@ __global__ void k_asym(MfPattern P, const double *vals, double *out) {
 }
 }
 
+// rows [row0, row1) only (distributed row blocks: vals may be a window
+// holding the rows within K planes of the range)
+__global__ void k_asym_rows(MfPattern P, const double *vals, int64_t row0,
+                            int64_t row1, double *out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = row0 + w0; r < row1; r += nw) {
+    const RowBox b = row_box(P, r);
+    const int ne = (int)(P.rowptr[r + 1] - b.p0);
+    double s = 0.0;
+    for (int e = lane; e < ne; e += 32) {
+      int64_t c = entry_col(P, b, e);
+      s += fabs(vals[b.p0 + e] - vals[pat_index(P, c, r)]);
+    }
+    s = warp_sum(s);
+    if (lane == 0) atomic_max_nonneg(out, s);
+  }
+}
+
 __global__ void k_norm(MfPattern P, const double *vals, double *out) {
   WARP_ROWS_BEGIN
   double s = 0.0;
@@ -190,6 +210,16 @@ cudaError_t mf_launch_asym(const MfPattern &P, const double *vals,
   cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), s);
   if (e != cudaSuccess) return e;
   k_asym<<<rows_grid(P.n), 256, 0, s>>>(P, vals, out);
+  return cudaGetLastError();
+}
+cudaError_t mf_launch_asym_rows(const MfPattern &P, const double *vals,
+                                int64_t row0, int64_t row1, double *out,
+                                cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), s);
+  if (e != cudaSuccess) return e;
+  if (row1 > row0)
+    k_asym_rows<<<rows_grid(row1 - row0), 256, 0, s>>>(P, vals, row0, row1,
+                                                         out);
   return cudaGetLastError();
 }
 cudaError_t mf_launch_norm(const MfPattern &P, const double *vals,

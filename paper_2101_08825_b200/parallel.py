@@ -27,6 +27,7 @@ The communication code is device-agnostic (NCCL tensors on GPUs, gloo on
 CPU for the world_size-2 tests).
 """
 
+import os
 import time
 
 import numpy as np
@@ -140,30 +141,42 @@ def parallel_assemble(mesh, space, kernel, config=None, n_parts=1,
         c.events = int(cnt[0].item())
         c.t_a = time.perf_counter() - t0
         buffers.append(B._dvals)
-    # ownership audit: a buffer only holds rows of its own elements' DOFs
+    # ownership audit (parallel.py:180-188): a buffer may only hold nonzeros
+    # in rows of DOFs carried by its partition's own elements -- per-row
+    # flags from the device (n_dofs bytes, no nnz-sized index)
+    import ctypes
+    from .assembly import C_byref
+    L = N.lib()
     A = ctx.new_matrix()
-    rowptr = A.rowptr
-    entry_owner = torch.from_numpy(
-        np.repeat(row_owner, np.diff(rowptr))).to(A._dvals.device)
+    dev = A._dvals.device
+    st = N.stream_ptr(device=dev)
+    pat = A._pattern_struct()
+    flags = torch.empty(max(space.n_dofs, 1), dtype=torch.uint8, device=dev)
     for c in contexts:
+        N.check(L.mf_row_touched(C_byref(pat), N.ptr(buffers[c.part]),
+                                 N.ptr(flags), st), "mf_row_touched")
+        touched = np.nonzero(flags[:space.n_dofs].cpu().numpy())[0]
         own = np.unique(space.element_dofs[c.owned])
-        rows_mask = np.zeros(space.n_dofs, bool)
-        rows_mask[own[own >= 0]] = True
-        touched = torch.nonzero(buffers[c.part] != 0).flatten().cpu().numpy()
-        if touched.size:
-            rows = np.searchsorted(rowptr, touched, side="right") - 1
-            if not rows_mask[rows].all():
-                raise AssertionError("partition wrote a row outside its "
-                                     "elements")
-    # merge: one pass per row owner, buffers summed in partition order
+        own = own[own >= 0]
+        if not np.isin(touched, own).all():
+            raise AssertionError("partition wrote a row outside its "
+                                 "elements")
+    # merge (parallel.py:190-200): every entry is the sum of the partition
+    # buffers in partition order (the reference sums per row owner, which
+    # gives the same per-entry order); _finish's x2 folded in
+    nnz = A.nnz
+    done = 0
+    while done < n_parts:
+        k = min(64 - (1 if done else 0), n_parts - done)
+        ptrs = ([A._dvals.data_ptr()] if done else []) + [
+            b.data_ptr() for b in buffers[done:done + k]]
+        arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
+        last = done + k == n_parts
+        N.check(L.mf_sum_ordered(len(ptrs), arr, nnz, 2.0 if last else 1.0,
+                                 N.ptr(A._dvals), st), "mf_sum_ordered")
+        done += k
     for c in contexts:
-        sel = entry_owner == c.part
-        acc = buffers[0][sel].clone()
-        for jp in range(1, n_parts):
-            acc += buffers[jp][sel]
-        A._dvals[sel] = acc
         c.t_t = time.perf_counter() - t_start
-    A._dvals *= 2.0
     counters = torch.zeros(N.MF_NCOUNTERS, dtype=torch.int64,
                            device=A._dvals.device)
     counters[0] = sum(c.events for c in contexts)
@@ -335,6 +348,11 @@ class SlabAssembler:
         from .device import ColorPlan
         self.rank, self.world = rank, world
         self.ctx = AssemblyContext(mesh, space, kernel, config, device)
+        if isinstance(weights, str) and weights == "pairs":
+            # per-element candidate-pair counts (the GPU count pass): slabs
+            # balanced by pair work, not by layer count
+            weights = pair_counts(mesh, kernel, self.ctx.dmesh)
+        self.weights = weights
         self.layers = layers or slab_layers(mesh, world, weights)
         K, oe = pattern_halfwidth(mesh, kernel, config, space.degree)
         self.A = SparseMatrix(space, K, allocate=False)
@@ -372,6 +390,122 @@ class SlabAssembler:
         return gather_rows(self.local, self.plan, self.plans, self.A.nnz,
                            group, dst)
 
+    # -- host result without a rank-0 funnel ------------------------------
+    def owned_view(self):
+        """(device tensor of this rank's owned values, their offset)."""
+        base = self.plan.vals_touch[0]
+        a, b = self.plan.vals_own
+        return self.local[a - base:b - base], a
+
+    def copy_owned_to_host(self, host, event=None):
+        """D2H of the owned row block straight into host[vals_own] (one
+        slice of a node-shared array): pinned staging ring, thread-pool
+        copies (device.HostStager)."""
+        import torch
+        from .device import HostStager
+        src, a = self.owned_view()
+        if src.numel() == 0:
+            return
+        if event is None:
+            event = torch.cuda.Event()
+            event.record(torch.cuda.current_stream(self.ctx.device))
+        HostStager(self.ctx.device).run(src, host[a:a + src.numel()],
+                                        [(event, 0, src.numel())])
+
+    def asymmetry(self, group=None):
+        """presym_asymmetry of the distributed matrix: every rank takes the
+        max over its owned rows of sum_c |A_rc - A_cr| from a halo window
+        (its rows plus K grid planes either side, from the owners over
+        P2P), then one all-reduce MAX."""
+        import torch
+        import torch.distributed as dist
+        from .assembly import C_byref
+        win, wa = halo_window(self.local, self.plan, self.plans, self.A,
+                              group)
+        out = torch.zeros(1, dtype=torch.float64, device=self.ctx.device)
+        r0, r1 = self.plan.rows_own
+        import ctypes
+        N.check(N.lib().mf_asymmetry_inf_rows(
+            C_byref(self.A._pattern_struct()),
+            ctypes.c_void_p(win.data_ptr() - 8 * wa), r0, r1, N.ptr(out),
+            N.stream_ptr(device=self.ctx.device)), "mf_asymmetry_inf_rows")
+        if self.world > 1:
+            dist.all_reduce(out, op=dist.ReduceOp.MAX, group=group)
+        return float(out.item())
+
+
+def window_range(plan, plans, A):
+    """Value range [wa, wb) of the rows within K grid planes of a rank's
+    owned rows (what the transposed lookups of its rows touch)."""
+    K = A.K
+    nplanes = A.NZ if A.NZ > 1 else A.NY
+    lo_p = max(plan.own_planes[0] - K, 0)
+    hi_p = min(plan.own_planes[1] + K, nplanes)
+    return int(A.rowptr[lo_p * plan.plane]), int(A.rowptr[hi_p * plan.plane])
+
+
+def halo_window(local, plan, plans, A, group=None):
+    """This rank's owned values plus the owned values of the other ranks
+    within its window_range, as one tensor (and its offset).  Every rank
+    sends the part of its owned block each other rank's window needs and
+    receives its own window's parts, in one batched P2P round."""
+    import torch.distributed as dist
+    base = plan.vals_touch[0]
+    wa, wb = window_range(plan, plans, A)
+    win = local.new_empty(wb - wa)
+    oa, ob = plan.vals_own
+    win[oa - wa:ob - wa] = local[oa - base:ob - base]
+    ops = []
+    for q in plans:
+        if q.rank == plan.rank:
+            continue
+        a, b = max(q.vals_own[0], wa), min(q.vals_own[1], wb)
+        if a < b:
+            ops.append(dist.P2POp(dist.irecv, win[a - wa:b - wa], q.rank,
+                                  group))
+        qa, qb = window_range(q, plans, A)
+        a, b = max(oa, qa), min(ob, qb)
+        if a < b:
+            ops.append(dist.P2POp(dist.isend,
+                                  local[a - base:b - base].contiguous(),
+                                  q.rank, group))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+    return win, wa
+
+
+class SharedHostArray:
+    """float64[n] backed by one file mapped by every rank of the node
+    (/dev/shm when it has room, else the temp directory): each rank writes
+    its own slice, rank `dst` keeps the whole array as its result."""
+
+    def __init__(self, n, group=None, dst=0):
+        import tempfile
+        import torch.distributed as dist
+        rank = dist.get_rank(group)
+        src = dst if group is None else dist.get_global_rank(group, dst)
+        name = [None]
+        if rank == dst:
+            d = "/dev/shm"
+            try:
+                st = os.statvfs(d)
+                if st.f_bavail * st.f_frsize < 8 * n * 1.05:
+                    d = None
+            except OSError:
+                d = None
+            fd, path = tempfile.mkstemp(prefix="mf_vals_", dir=d)
+            os.ftruncate(fd, max(8 * n, 8))
+            os.close(fd)
+            name = [path]
+        dist.broadcast_object_list(name, src=src, group=group)
+        self.path = name[0]
+        self.array = np.memmap(self.path, dtype=np.float64, mode="r+",
+                               shape=(max(n, 1),))[:n]
+        dist.barrier(group)
+        if rank == dst:
+            os.unlink(self.path)     # the mappings stay valid
+
 
 def emulate_slabs(mesh, space, kernel, config, world, device=None):
     """Run every rank's slab on ONE device, one after another, and merge
@@ -400,6 +534,60 @@ def emulate_slabs(mesh, space, kernel, config, world, device=None):
     return full, events
 
 
+def emulate_distributed(mesh, space, kernel, config, world, device=None):
+    """The host-gather path of assemble_distributed for `world` ranks, run
+    rank after rank on ONE device (ranks never wait on one another): each
+    rank's slab assembly, the interface additions, each rank's D2H of its
+    owned block into its slice of one host array, and each rank's halo
+    asymmetry over its owned rows.  Returns (host values, events,
+    presym_asymmetry, per-rank timings in seconds)."""
+    import ctypes
+
+    import torch
+
+    from .assembly import C_byref
+    ranks = [SlabAssembler(mesh, space, kernel, config, r, world, device,
+                           weights="pairs") for r in range(world)]
+    dev = ranks[0].ctx.device
+    host = np.empty(ranks[0].A.nnz, dtype=np.float64)
+    timing = []
+    events = 0
+    for s in ranks:
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        events += int(s.assemble_local()[0].item())
+        torch.cuda.synchronize(dev)
+        timing.append({"rank": s.rank, "assemble_s": time.perf_counter() - t0,
+                       "layers": list(s.plan.layers)})
+    for r in range(world - 1):           # rank r's shared top plane -> r+1
+        src, dst = ranks[r], ranks[r + 1]
+        a, b = src.plan.send_range
+        dst.local[a - dst.plan.vals_touch[0]:b - dst.plan.vals_touch[0]] += \
+            src.local[a - src.plan.vals_touch[0]:b - src.plan.vals_touch[0]]
+    for s, t in zip(ranks, timing):
+        t0 = time.perf_counter()
+        s.copy_owned_to_host(host)
+        t["d2h_s"] = time.perf_counter() - t0
+        t["d2h_bytes"] = 8 * (s.plan.vals_own[1] - s.plan.vals_own[0])
+    # halo windows from the merged owned blocks (what the P2P round gives)
+    full = torch.empty(ranks[0].A.nnz, dtype=torch.float64, device=dev)
+    for s in ranks:
+        v, a = s.owned_view()
+        full[a:a + v.numel()] = v
+    asym = 0.0
+    out = torch.zeros(1, dtype=torch.float64, device=dev)
+    for s in ranks:
+        wa, wb = window_range(s.plan, s.plans, s.A)
+        win = full[wa:wb].clone()
+        r0, r1 = s.plan.rows_own
+        N.check(N.lib().mf_asymmetry_inf_rows(
+            C_byref(s.A._pattern_struct()),
+            ctypes.c_void_p(win.data_ptr() - 8 * wa), r0, r1, N.ptr(out),
+            N.stream_ptr(device=dev)), "mf_asymmetry_inf_rows")
+        asym = max(asym, float(out.item()))
+    return host, events, asym, timing
+
+
 def pair_counts(mesh, params, dmesh):
     """Candidate-pair count per element (the count pass of the GPU
     neighbour search, mf_count_candidates) -- the slab balancing weight."""
@@ -419,33 +607,126 @@ def pair_counts(mesh, params, dmesh):
         ctypes.byref(dmesh.struct), N.ptr(outer), n, N.ptr(mask),
         stencil_radius(reach + stencil_pad(mesh), mesh.h), float(reach),
         N.ptr(counts),
-        N.stream_ptr()), "mf_count_candidates")
+        N.stream_ptr(device=dev)), "mf_count_candidates")
     return counts.cpu().numpy()
 
 
 def assemble_distributed(mesh, space, kernel, config=None, group=None,
-                         dst=0, weights=None):
+                         dst=0, weights="pairs", gather="host",
+                         return_slab=False):
     """Multi-GPU `assemble`: every rank of the process group calls it with
     the same host inputs; rank `dst` returns the full SparseMatrix (host
-    values, events, presym_asymmetry), the others return None."""
+    values, events, presym_asymmetry), the others return None.
+
+    weights="pairs" balances the slabs by candidate-pair counts.
+    gather="host": each rank copies its owned row block straight into its
+    slice of one node-shared host array (no rank-0 funnel; the copies of
+    all ranks run in parallel), the asymmetry comes from per-rank halo
+    windows.  gather="nccl" (also used for symmetrize=True): NCCL row-block
+    gather to rank dst, then the single-device finish and D2H.
+    return_slab=True also returns this rank's SlabAssembler (for
+    assemble_rhs_distributed)."""
     import torch
     import torch.distributed as dist
 
-    from .assembly import _d2h
+    from .assembly import _d2h, check_counters
     config = config or AssemblyConfig()
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
     dev = torch.device("cuda", torch.cuda.current_device())
     s = SlabAssembler(mesh, space, kernel, config, rank, world, dev,
                       weights=weights)
+    if gather == "nccl" or config.symmetrize:
+        cnt = s.assemble_local().clone()
+        s.exchange(group)
+        full = s.gather(group, dst)
+        dist.all_reduce(cnt, group=group)
+        A = None
+        if rank == dst:
+            A = s.A
+            A._dvals = full      # the slab kernels already fold _finish's x2
+            s.ctx.finish(A, cnt)
+            A._vals = _d2h(A._dvals)
+        return (A, s) if return_slab else A
+    shm = SharedHostArray(s.A.nnz, group, dst)
     cnt = s.assemble_local().clone()
     s.exchange(group)
-    full = s.gather(group, dst)
+    s.copy_owned_to_host(shm.array)
+    asym = s.asymmetry(group)
     dist.all_reduce(cnt, group=group)
+    dist.barrier(group)          # every slice is in the shared array
+    A = None
+    if rank == dst:
+        A = s.A
+        c = cnt.cpu().numpy()
+        check_counters(c)
+        A.counters = c
+        A.events = int(c[N.CNT_EVENTS])
+        A.presym_asymmetry = asym
+        A._vals = shm.array
+    return (A, s) if return_slab else A
+
+
+def assemble_rhs_distributed(mesh, space, kernel, f, g, slab, group=None,
+                             dst=0):
+    """`assemble_rhs` (assembly.py:679-691) over the slab decomposition:
+    each rank integrates the load of its own slab elements and the matvec
+    A g of its owned rows; the partial vectors (n_dofs each) are gathered
+    on rank `dst` and summed there in rank order (deterministic).  Rank
+    dst returns rhs[free], the others None."""
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    from .assembly import C_byref, group_load_device
+    from .device import to_device
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    dev = slab.ctx.device
+    L = N.lib()
+    st = N.stream_ptr(device=dev)
+    n = space.n_dofs
+    omega = np.zeros(mesh.n_elements, dtype=bool)
+    omega[mesh.omega_element_ids()] = True
+    own = slab.inner[omega[slab.inner]]
+    part = group_load_device(mesh, space, f, own, slab.ctx.dmesh)
+    gt = np.zeros(n)
+    if callable(g):
+        gt[space.constrained] = g(space.dof_coords[space.constrained])
+    else:
+        gv = np.asarray(g, dtype=float)
+        gt[space.constrained] = (gv[space.constrained]
+                                 if gv.shape == (n,) else gv)
+    gtd = to_device(gt, dev)
+    y = torch.zeros(n, dtype=torch.float64, device=dev)
+    r0, r1 = slab.plan.rows_own
+    base = slab.plan.vals_touch[0]
+    N.check(L.mf_matvec_rows(
+        C_byref(slab.A._pattern_struct()),
+        ctypes.c_void_p(slab.local.data_ptr() - 8 * base), N.ptr(gtd), r0,
+        r1, N.ptr(y), st), "mf_matvec_rows")
+    # partial = load part - (A g) on owned rows
+    N.check(L.mf_axpby(n, 1.0, N.ptr(part), -1.0, N.ptr(y), N.ptr(part), st),
+            "mf_axpby")
     if rank != dst:
+        dist.send(part, dst, group)
         return None
-    A = s.A
-    A._dvals = full          # the slab kernels already fold _finish's x2
-    s.ctx.finish(A, cnt)
-    A._vals = _d2h(A._dvals)
-    return A
+    parts = []
+    for q in range(world):
+        if q == rank:
+            parts.append(part)
+        else:
+            t = torch.empty_like(part)
+            dist.recv(t, q, group)
+            parts.append(t)
+    tot = torch.empty_like(part)
+    arr = (ctypes.c_void_p * world)(*[t.data_ptr() for t in parts])
+    N.check(L.mf_sum_ordered(world, arr, n, 1.0, N.ptr(tot), st),
+            "mf_sum_ordered")
+    free = np.asarray(space.free, dtype=np.int64)
+    fd = to_device(free, dev)
+    out = torch.empty(len(free), dtype=torch.float64, device=dev)
+    N.check(L.mf_gather_diff(len(free), N.ptr(fd), N.ptr(tot), None,
+                             N.ptr(out), st), "mf_gather_diff")
+    return out.cpu().numpy()

@@ -116,3 +116,67 @@ def test_assemble_distributed_scaling_contract():
     assert "full * 2" not in src
     src2 = inspect.getsource(parallel.SlabAssembler.assemble_local)
     assert "scale" not in src2 or "scale=2" in src2
+
+
+def _host_worker(rank, world, port, name, out_q):
+    """The host-gather path of assemble_distributed: interface exchange,
+    owned slices written into one node-shared array, halo windows."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        from paper_2101_08825_b200.assembly import HostPattern
+        from paper_2101_08825_b200.parallel import (
+            SharedHostArray, SlabPlan, exchange_interfaces, halo_window,
+            slab_layers, window_range)
+        g = _golden(name)
+        mesh, space, kp, cfg = g.build()
+        layers = slab_layers(mesh, world)
+        A = HostPattern.for_space(mesh, space, kp, cfg)
+        plans = [SlabPlan(mesh, space, A.rowptr, layers, r)
+                 for r in range(world)]
+        plan = plans[rank]
+        mask = np.zeros(mesh.n_elements, np.uint8)
+        mask[plan.inner_ids(mesh)] = 1
+        oracle.run_general(mesh, space, kp, cfg, A, inner_mask=mask)
+        a, b = plan.vals_touch
+        local = torch.from_numpy(A.vals[a:b] * 2.0)
+        exchange_interfaces(local, plan)
+        shm = SharedHostArray(A.nnz)
+        oa, ob = plan.vals_own
+        shm.array[oa:ob] = local[oa - a:ob - a].numpy()
+        win, wa = halo_window(local, plan, plans, A)
+        assert (wa, wa + win.numel()) == window_range(plan, plans, A)
+        dist.barrier()
+        # every rank's window equals the merged matrix over that range
+        full = np.array(shm.array)
+        ok = bool(np.array_equal(win.numpy(), full[wa:wa + win.numel()]))
+        flag = torch.tensor([int(ok)])
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if rank == 0:
+            out_q.put((full, int(flag.item())))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,world", [("hex_q1_gl3", 2),
+                                        ("hex_q1_gl3", 3),
+                                        ("tri_p1_lmax3", 2)])
+def test_host_gather_and_halo_windows_gloo(name, world, oracle_lib):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_host_worker,
+                         args=(r, world, port, name, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    vals, ok = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    g = _golden(name)
+    assert ok == 1
+    assert rel_frob(vals, g["vals"]) <= 1e-14
