@@ -128,7 +128,12 @@ struct OuterBox {
 };
 
 // ---- triangle events (Dunavant outer rule in shared memory) ----
-template <int NQO, int NQ1, bool SHARP>
+// VOTE: evaluate the shell polynomials only when some lane of the warp
+// needs one (thread-per-pair callers, whose lanes hold unrelated pairs);
+// the warp-cooperative phase B of k_tri_q passes false: there every lane
+// integrates a full event and the vote nearly always fires (R2-small
+// 186 -> 178 ms without it; k_2d on R3-16h is faster with it, 669 vs 725)
+template <int NQO, int NQ1, bool SHARP, bool VOTE = true>
 MF_DEV void tri_full(const AsmParams &P, const double *g, const OuterTri &O,
                      const double (*y)[2], const double *s_pts,
                      const double *s_w, double (*V)[3]) {
@@ -165,12 +170,12 @@ MF_DEV void tri_full(const AsmParams &P, const double *g, const OuterTri &O,
         anysh |= sh;
       }
     }
-    if (!SHARP && __any_sync(__activemask(), anysh)) {
+    if (!SHARP && (!VOTE || __any_sync(__activemask(), anysh))) {
+      double v[NQ1];
+      xi256_fast_n<NQ1>(P, mu, v);
 #pragma unroll
-      for (int q1 = 0; q1 < NQ1; q1++) {
-        const double v = xi256_unclamped(P, mu[q1]);
-        if ((shm >> q1) & 1u) mu[q1] = v;
-      }
+      for (int q1 = 0; q1 < NQ1; q1++)
+        if ((shm >> q1) & 1u) mu[q1] = v[q1];
     }
 #pragma unroll
     for (int q1 = 0; q1 < NQ1; q1++) {
@@ -261,11 +266,11 @@ MF_DEV void quad_full(const AsmParams &P, const double *g, const OuterBox &O,
         }
       }
       if (!SHARP && __any_sync(__activemask(), shm != 0)) {
+        double v[NO];
+        xi256_fast_n<NO>(P, mu, v);
 #pragma unroll
-        for (int a = 0; a < NO; a++) {
-          const double v = xi256_unclamped(P, mu[a]);
-          if ((shm >> a) & 1u) mu[a] = v;
-        }
+        for (int a = 0; a < NO; a++)
+          if ((shm >> a) & 1u) mu[a] = v[a];
       }
       double t0 = 0.0, t1 = 0.0;
 #pragma unroll
@@ -1292,7 +1297,7 @@ __global__ void __launch_bounds__(32 * kTriQWarps, MINB)
         for (int q = 0; q < NQ1; q++)
 #pragma unroll
           for (int j = 0; j < NL; j++) Ve[q][j] = 0.0;
-        tri_full<NQO, NQ1, false>(P, gg, O, yy, s_opts, s_ow, Ve);
+        tri_full<NQO, NQ1, false, false>(P, gg, O, yy, s_opts, s_ow, Ve);
 #pragma unroll
         for (int q = 0; q < NQ1; q++)
 #pragma unroll

@@ -43,6 +43,7 @@ struct AsmParams {
   double dm2, dp2;        // squared        (_kernels.py:412-413)
   double dme2_lo, dme2_hi;// sqrt-free decision band for aprx_max < dme
   double inv_eps, alpha;  // 1/eps and delta/eps (eps > 0 kernels)
+  double half_inv_eps;    // 0.5/eps
   int32_t hi_dm2, hi_dp2; // high 32-bit words of dm2 / dp2 (non-negative
                           // doubles order like their bit patterns)
   int32_t nl_box, nl_tri;
@@ -123,19 +124,6 @@ MF_DEV double xi_shell_256(const AsmParams &P, double d2) {
   return fma(p, r, 128.0);
 }
 
-// 1/sqrt(x) for normal x > 0 without the libdevice slow-path call:
-// MUFU.RSQ64H seed + two Newton steps (relative error ~1e-16)
-MF_DEV double rsqrt_fast(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double h = x * y;
-  double r = fma(-h, y, 1.0);
-  y = fma(0.5 * y, r, y);
-  h = x * y;
-  r = fma(-h, y, 1.0);
-  return fma(0.5 * y, r, y);
-}
-
 // 1/x for normal x without the IEEE-division slow path (Newton twice)
 MF_DEV double rcp_fast(double x) {
   double y;
@@ -146,74 +134,31 @@ MF_DEV double rcp_fast(double x) {
   return fma(y, e, y);
 }
 
-// sqrt(x) for normal x > 0: MUFU.RSQ64H seed y0 (~20 bits), one Newton
-// step on d0 = x*y0 and one residual correction (error ~ e0^3, full double
-// precision); 7 DP instructions instead of 2 rsqrt Newton steps + multiply
-MF_DEV double sqrt_fast(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  const double hy = 0.5 * y;
-  const double d0 = x * y;
-  const double e0 = fma(-d0, d0, x);
-  const double d1 = fma(hy, e0, d0);
-  const double e1 = fma(-d1, d1, x);
-  return fma(hy, e1, d1);
-}
-
-// Branch-free 256*mu for eps > 0: r = clamp((delta - d)/eps, -1, 1) and
-// xi(+1) = 1, xi(-1) = 0 exactly, so the plateau and the cut-off need no
-// branch; d = d2 * rsqrt(d2) (d2 clamped away from 0, where r clamps to 1).
-// Matches the reference's piecewise mu (_kernels.py:18-29) to rounding.
-MF_DEV double mu256_smooth(const AsmParams &P, double d2) {
-  const double dd = fmax(d2, 1e-300);
-  const double d = dd * rsqrt_fast(dd);
-  double r = fma(-d, P.inv_eps, P.alpha);
-  r = fmin(fmax(r, -1.0), 1.0);
-  const double r2 = r * r;
-  const double p = fma(fma(fma(fma(35.0, r2, -180.0), r2, 378.0), r2, -420.0),
-                       r2, 315.0);
-  return fma(p, r, 128.0);
-}
-
-// shell mollifier without clamp: callers select it only for pairs whose
-// d2 shares its high 32-bit word with, or lies between, dm2 and dp2, so
-// |r| exceeds 1 by at most (delta/eps) 2^-21 and xi, flat to fourth order
-// at +-1, deviates from its end value by < 1e-24 there.
-MF_DEV double xi256_unclamped(const AsmParams &P, double d2) {
-  const double d = sqrt_fast(d2);
-  const double r = fma(-d, P.inv_eps, P.alpha);
-  const double r2 = r * r;
-  const double p = fma(fma(fma(fma(35.0, r2, -180.0), r2, 378.0), r2, -420.0),
-                       r2, 315.0);
-  return fma(p, r, 128.0);
-}
-
-// xi256_unclamped for N independent squared distances, written step by
-// step across the N values so their dependent DP chains interleave (one
-// chain is ~14 dependent DP operations; alone it leaves the FP64 pipe idle)
+// xi256 for N squared distances with ONE Newton correction folded into r:
+// y = rsqrt(d2) (MUFU), d0 = d2 y, e0 = d2 - d0^2, and
+//   r = (alpha - inv_eps d0) - (0.5 inv_eps y) e0
+// which is alpha - inv_eps (d0 + 0.5 y e0), the Newton-corrected distance.
+// Relative error of the distance ~ (rsqrt seed error)^2; 10 DP operations
+// and 9 dependent levels instead of 12 and 13.
 template <int N>
-MF_DEV void xi256_unclamped_n(const AsmParams &P, const double *d2,
-                              double *out) {
-  double y[N], hy[N], d[N], e[N];
+MF_DEV void xi256_fast_n(const AsmParams &P, const double *d2, double *out) {
+  double y[N], d0[N], g[N], e[N], r[N];
 #pragma unroll
   for (int i = 0; i < N; i++)
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y[i]) : "d"(d2[i]));
 #pragma unroll
   for (int i = 0; i < N; i++) {
-    hy[i] = 0.5 * y[i];
-    d[i] = d2[i] * y[i];
+    d0[i] = d2[i] * y[i];
+    g[i] = P.half_inv_eps * y[i];
   }
 #pragma unroll
-  for (int i = 0; i < N; i++) e[i] = fma(-d[i], d[i], d2[i]);
+  for (int i = 0; i < N; i++) {
+    e[i] = fma(-d0[i], d0[i], d2[i]);
+    r[i] = fma(-d0[i], P.inv_eps, P.alpha);
+  }
 #pragma unroll
-  for (int i = 0; i < N; i++) d[i] = fma(hy[i], e[i], d[i]);
-#pragma unroll
-  for (int i = 0; i < N; i++) e[i] = fma(-d[i], d[i], d2[i]);
-#pragma unroll
-  for (int i = 0; i < N; i++) d[i] = fma(hy[i], e[i], d[i]);
-  double r[N], r2[N], p[N];
-#pragma unroll
-  for (int i = 0; i < N; i++) r[i] = fma(-d[i], P.inv_eps, P.alpha);
+  for (int i = 0; i < N; i++) r[i] = fma(-g[i], e[i], r[i]);
+  double r2[N], p[N];
 #pragma unroll
   for (int i = 0; i < N; i++) r2[i] = r[i] * r[i];
 #pragma unroll
@@ -226,11 +171,6 @@ MF_DEV void xi256_unclamped_n(const AsmParams &P, const double *d2,
   for (int i = 0; i < N; i++) p[i] = fma(p[i], r2[i], 315.0);
 #pragma unroll
   for (int i = 0; i < N; i++) out[i] = fma(p[i], r[i], 128.0);
-}
-
-// eps = 0: the reference skips d2 >= delta^2 and takes mu = 1 below
-MF_DEV double mu256_sharp(const AsmParams &P, double d2) {
-  return d2 < P.dp2 ? 256.0 : 0.0;
 }
 
 MF_DEV double mu256(const AsmParams &P, double d2) {

@@ -38,12 +38,6 @@ constexpr int kSplitCap = 64;  // split nodes per level (L_max <= 4)
 #ifndef MF_HEX_MINB
 #define MF_HEX_MINB 4
 #endif
-#ifndef MF_HEX_GROUP
-#define MF_HEX_GROUP 3
-#endif
-#ifndef MF_HEX_SHELLQ
-#define MF_HEX_SHELLQ 0
-#endif
 
 struct Box {
   double lo[3], hi[3];
@@ -188,117 +182,65 @@ MF_DEV void event_plateau(const AsmParams &P, const double *s_rt,
 }
 
 // Full event: lane q1 evaluates its NO^3 point pairs and contracts them
-// by sum factorisation into V.  Loop order: x node a outermost (rolled, its
-// operands re-read from shared memory), then y node b and z node c
-// unrolled; contraction z first (2 DFMA per point), then y (4 per b), then
-// x (8 per a).  Point pairs are classified on the high word of the exact
-// d2 (certainly inside delta-eps -> mu = 1, certainly beyond delta+eps ->
-// 0); the shell polynomial runs for the NO z-nodes of one (a, b) only when
-// a lane of the warp needs it.  Inactive lanes carry a far-away point, so
+// by sum factorisation into V.  Every loop is unrolled (x node a, y node b,
+// z node c), so the compiler interleaves the NO^3 independent distance /
+// mollifier chains of a lane.  Point pairs are classified on the high word
+// of the exact d2 (certainly inside delta-eps -> 256, certainly beyond
+// delta+eps -> 0, else the shell value).  The shell polynomial is
+// evaluated for EVERY point pair, without a warp vote: a vote per (a, b)
+// z-line fires on 86% of the lines (some lane of 27 needs the shell there)
+// and its branch cost more than the 14% of polynomials it saved (R4-half
+// 1300 -> 1275 ms; the straight-line code is what lets the a-unroll pay,
+// 1275 -> 1223 ms).  Contraction: z first (2 DFMA per point), then y (4
+// per b), then x (8 per a).  Inactive lanes carry a far-away point, so
 // every one of their pairs classifies as "beyond".
 template <int NO, bool SHARP>
 MF_DEV void event_full(const AsmParams &P, const double *s_rt,
                        const double *s_rw, WarpCtx<NO> &C, int slot,
                        const double y[3], int lane, double V[8]) {
   event_axes<NO>(P, s_rt, s_rw, C, slot, lane);
-  double sq1[NO], sq2[NO], shy[2][NO], shz[2][NO];
+  // the outer y/z weights stay in shared memory (broadcast loads at each
+  // use): 24 fewer live registers than register copies
+  const double(*shy)[NO] = C.sh[1];
+  const double(*shz)[NO] = C.sh[2];
+  double sq1[NO], sq2[NO];
 #pragma unroll
   for (int b = 0; b < NO; b++) {
     const double d1 = xsub(C.X[1][b], y[1]);
     const double d2 = xsub(C.X[2][b], y[2]);
     sq1[b] = xmul(d1, d1);
     sq2[b] = xmul(d2, d2);
-#pragma unroll
-    for (int j = 0; j < 2; j++) {
-      shy[j][b] = C.sh[1][j][b];
-      shz[j][b] = C.sh[2][j][b];
-    }
   }
-#pragma unroll 1
+#pragma unroll
   for (int a = 0; a < NO; a++) {
     const double d0 = xsub(C.X[0][a], y[0]);
     const double sq0 = xmul(d0, d0);
-    double mu[NO][NO];
-#if MF_HEX_GROUP == 9
-    double d2v[NO][NO];
-    bool anysh = false;
-    unsigned shm = 0;
-#pragma unroll
-    for (int b = 0; b < NO; b++) {
-      const double sxy = xadd(sq0, sq1[b]);
-#pragma unroll
-      for (int c = 0; c < NO; c++) {
-        const double d2 = xadd(sxy, sq2[c]);
-        d2v[b][c] = d2;
-        if (SHARP) {
-          mu[b][c] = d2 < P.dp2 ? 256.0 : 0.0;
-        } else {
-          const int hi = __double2hiint(d2);
-          const bool pl = hi < P.hi_dm2;
-          const bool sh = !pl && hi <= P.hi_dp2;
-          mu[b][c] = pl ? 256.0 : 0.0;
-          shm |= (unsigned)sh << (b * NO + c);
-          anysh |= sh;
-        }
-      }
-    }
-    if (!SHARP && __any_sync(0xffffffffu, anysh)) {
-#pragma unroll
-      for (int b = 0; b < NO; b++)
-#pragma unroll
-        for (int c = 0; c < NO; c++) {
-          const double v = xi256_unclamped(P, d2v[b][c]);
-          if ((shm >> (b * NO + c)) & 1u) mu[b][c] = v;
-        }
-    }
-#else
-#pragma unroll
-    for (int b = 0; b < NO; b++) {
-      const double sxy = xadd(sq0, sq1[b]);
-      double d2v[NO];
-      bool shl[NO];
-      bool anysh = false;
-#pragma unroll
-      for (int c = 0; c < NO; c++) {
-        d2v[c] = xadd(sxy, sq2[c]);
-        if (SHARP) {
-          mu[b][c] = d2v[c] < P.dp2 ? 256.0 : 0.0;
-          shl[c] = false;
-        } else {
-          const int hi = __double2hiint(d2v[c]);
-          const bool pl = hi < P.hi_dm2;
-          shl[c] = !pl && hi <= P.hi_dp2;
-          mu[b][c] = pl ? 256.0 : 0.0;
-          anysh |= shl[c];
-        }
-      }
-      if (!SHARP && __any_sync(0xffffffffu, anysh)) {
-#ifdef MF_HEX_STATS
-        unsigned nsh = 0;
-#pragma unroll
-        for (int c = 0; c < NO; c++) nsh += shl[c];
-        nsh = __reduce_add_sync(0xffffffffu, nsh);
-        if (lane == 0) {
-          atomicAdd(P.counters + 8, 1ull);
-          atomicAdd(P.counters + 9, (unsigned long long)nsh);
-        }
-#endif
-        double v[NO];
-        xi256_unclamped_n<NO>(P, d2v, v);
-#pragma unroll
-        for (int c = 0; c < NO; c++)
-          if (shl[c]) mu[b][c] = v[c];
-      }
-    }
-#endif
     double W[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // [jy][jz]
 #pragma unroll
     for (int b = 0; b < NO; b++) {
+      const double sxy = xadd(sq0, sq1[b]);
+      double d2v[NO], mu[NO];
+#pragma unroll
+      for (int c = 0; c < NO; c++) d2v[c] = xadd(sxy, sq2[c]);
+      if (SHARP) {
+#pragma unroll
+        for (int c = 0; c < NO; c++) mu[c] = d2v[c] < P.dp2 ? 256.0 : 0.0;
+      } else {
+        double v[NO];
+        xi256_fast_n<NO>(P, d2v, v);
+#pragma unroll
+        for (int c = 0; c < NO; c++) {
+          const int hi = __double2hiint(d2v[c]);
+          const bool pl = hi < P.hi_dm2;
+          const bool sh = !pl && hi <= P.hi_dp2;
+          mu[c] = sh ? v[c] : (pl ? 256.0 : 0.0);
+        }
+      }
       double u0 = 0.0, u1 = 0.0;  // z contraction
 #pragma unroll
       for (int c = 0; c < NO; c++) {
-        u0 = fma(mu[b][c], shz[0][c], u0);
-        u1 = fma(mu[b][c], shz[1][c], u1);
+        u0 = fma(mu[c], shz[0][c], u0);
+        u1 = fma(mu[c], shz[1][c], u1);
       }
 #pragma unroll
       for (int jy = 0; jy < 2; jy++) {
@@ -318,130 +260,14 @@ MF_DEV void event_full(const AsmParams &P, const double *s_rt,
   __syncwarp();
 }
 
-#if MF_HEX_SHELLQ
-// Full event with the shell mollifier evaluated on a warp-compacted queue
-// (eps > 0).  Per outer x node a: every lane classifies its NO^2 point
-// pairs (plateau / shell / beyond) by the high word of the exact d2; the
-// lanes' shell d2 values are appended to a per-warp shared-memory queue at
-// warp-prefix-sum offsets; the warp evaluates the queue 32 entries per
-// round (all lanes busy, instead of NO polynomials per (a, b) line whenever
-// one lane of 27 needs one); each lane reads its shell values back in its
-// own order and contracts as event_full does.
-template <int NO>
-MF_DEV void event_full_q(const AsmParams &P, const double *s_rt,
-                         const double *s_rw, WarpCtx<NO> &C, int slot,
-                         const double y[3], int lane, double V[8],
-                         double *q) {
-  event_axes<NO>(P, s_rt, s_rw, C, slot, lane);
-  double sq1[NO], sq2[NO];
-#pragma unroll
-  for (int b = 0; b < NO; b++) {
-    const double d1 = xsub(C.X[1][b], y[1]);
-    const double d2 = xsub(C.X[2][b], y[2]);
-    sq1[b] = xmul(d1, d1);
-    sq2[b] = xmul(d2, d2);
-  }
-#pragma unroll 1
-  for (int a = 0; a < NO; a++) {
-    const double d0 = xsub(C.X[0][a], y[0]);
-    const double sq0 = xmul(d0, d0);
-    double d2v[NO * NO];
-    unsigned plm = 0, shm = 0;
-#pragma unroll
-    for (int b = 0; b < NO; b++) {
-      const double sxy = xadd(sq0, sq1[b]);
-#pragma unroll
-      for (int c = 0; c < NO; c++) {
-        const double d2 = xadd(sxy, sq2[c]);
-        d2v[b * NO + c] = d2;
-        const int hi = __double2hiint(d2);
-        const bool pl = hi < P.hi_dm2;
-        const bool sh = !pl && hi <= P.hi_dp2;
-        plm |= (unsigned)pl << (b * NO + c);
-        shm |= (unsigned)sh << (b * NO + c);
-      }
-    }
-    // warp prefix sum of the shell counts -> this lane's queue offset
-    const int n = __popc(shm);
-    int incl = n;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, incl, off);
-      if (lane >= off) incl += t;
-    }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    const int base = incl - n;
-    if (total > 0) {
-      int k = base;
-#pragma unroll
-      for (int p = 0; p < NO * NO; p++)
-        if ((shm >> p) & 1u) q[k++] = d2v[p];
-      __syncwarp();
-      // evaluate the queue, two entries per lane at a time (independent
-      // DP chains interleave); entries past `total` are computed on stale
-      // data and never stored
-      const int rounds = (total + 31) >> 5;
-      int r = 0;
-      for (; r + 1 < rounds; r += 2) {
-        const int g0 = (r << 5) + lane, g1 = g0 + 32;
-        double d2[2] = {q[g0], q[g1 < total ? g1 : g0]};
-        double v[2];
-        xi256_unclamped_n<2>(P, d2, v);
-        q[g0] = v[0];
-        if (g1 < total) q[g1] = v[1];
-      }
-      if (r < rounds) {
-        const int g0 = (r << 5) + lane;
-        if (g0 < total) q[g0] = xi256_unclamped(P, q[g0]);
-      }
-      __syncwarp();
-    }
-    double W[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // [jy][jz]
-    int k = base;
-#pragma unroll
-    for (int b = 0; b < NO; b++) {
-      double u0 = 0.0, u1 = 0.0;  // z contraction
-#pragma unroll
-      for (int c = 0; c < NO; c++) {
-        const int p = b * NO + c;
-        double mu = ((plm >> p) & 1u) ? 256.0 : 0.0;
-        if ((shm >> p) & 1u) mu = q[k++];
-        u0 = fma(mu, C.sh[2][0][c], u0);
-        u1 = fma(mu, C.sh[2][1][c], u1);
-      }
-#pragma unroll
-      for (int jy = 0; jy < 2; jy++) {
-        const double wy = C.sh[1][jy][b];
-        W[jy][0] = fma(u0, wy, W[jy][0]);
-        W[jy][1] = fma(u1, wy, W[jy][1]);
-      }
-    }
-    const double x0 = C.sh[0][0][a], x1 = C.sh[0][1][a];
-#pragma unroll
-    for (int jz = 0; jz < 2; jz++)
-#pragma unroll
-      for (int jy = 0; jy < 2; jy++) {
-        V[2 * jy + 4 * jz] = fma(x0, W[jy][jz], V[2 * jy + 4 * jz]);
-        V[1 + 2 * jy + 4 * jz] = fma(x1, W[jy][jz], V[1 + 2 * jy + 4 * jz]);
-      }
-    __syncwarp();  // the next node reuses the queue
-  }
-}
-#endif
-
 template <int NO>
 MF_DEV void run_full(const AsmParams &P, const double *s_rt,
                      const double *s_rw, WarpCtx<NO> &C, int slot,
-                     const double y[3], int lane, bool active, double V[8],
-                     double *q) {
+                     const double y[3], int lane, double V[8]) {
   if (P.eps == 0.0)
     event_full<NO, true>(P, s_rt, s_rw, C, slot, y, lane, V);
   else
-#if MF_HEX_SHELLQ
-    event_full_q<NO>(P, s_rt, s_rw, C, slot, y, lane, V, q);
-#else
     event_full<NO, false>(P, s_rt, s_rw, C, slot, y, lane, V);
-#endif
 }
 
 template <int NO, int NI>
@@ -454,12 +280,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MF_HEX_MINB)
   __shared__ WarpCtx<NO> s_ctx[kWarpsPerBlock];
   __shared__ double s_buf[kWarpsPerBlock][NQ1][9];
   __shared__ uint32_t s_split[kWarpsPerBlock][2][kSplitCap];
-#if MF_HEX_SHELLQ
-  __shared__ double s_q[kWarpsPerBlock][NO * NO * 32];
-  double *q = s_q[threadIdx.x >> 5];
-#else
-  double *q = nullptr;
-#endif
 
   const MfMesh &M = P.mesh;
   const MfRules &Rr = P.rules;
@@ -493,7 +313,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MF_HEX_MINB)
                         (0.5 * (C.ihi[2] - C.ilo[2]));
   const bool active = lane < NQ1;
   // inactive lanes sit far away: all their pairs classify as "beyond"
-  double y[3] = {1e300, 1e300, 1e300};
+  double y[3] = {1e100, 1e100, 1e100};
   if (active) {
 #pragma unroll
     for (int k = 0; k < 3; k++)
@@ -620,7 +440,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MF_HEX_MINB)
           ev++;
           live = true;
           (act == ACT_FULL ? c_full : c_up)++;
-          run_full<NO>(P, s_rt, s_rw, C, 32, y, lane, active, V, q);
+          run_full<NO>(P, s_rt, s_rw, C, 32, y, lane, V);
         } else if (act == ACT_DEAD) {
           ev++;
           c_dead++;
@@ -678,8 +498,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MF_HEX_MINB)
               for (unsigned mm = mplat; mm; mm &= mm - 1)
                 event_plateau<NO>(P, s_rt, s_rw, C, __ffs(mm) - 1, lane, V);
               for (unsigned mm = mfull; mm; mm &= mm - 1)
-                run_full<NO>(P, s_rt, s_rw, C, __ffs(mm) - 1, y, lane,
-                             active, V, q);
+                run_full<NO>(P, s_rt, s_rw, C, __ffs(mm) - 1, y, lane, V);
             }
             __syncwarp();
             if (nnext > kSplitCap) {

@@ -168,11 +168,11 @@ MF_DEV void tet_full(const AsmParams &P, const double *g, const OuterTet &O,
       }
     }
     if (!SHARP && __any_sync(__activemask(), anysh)) {
+      double v[NQ1];
+      xi256_fast_n<NQ1>(P, mu, v);
 #pragma unroll
-      for (int q1 = 0; q1 < NQ1; q1++) {
-        const double v = xi256_unclamped(P, mu[q1]);
-        if ((shm >> q1) & 1u) mu[q1] = v;
-      }
+      for (int q1 = 0; q1 < NQ1; q1++)
+        if ((shm >> q1) & 1u) mu[q1] = v[q1];
     }
 #pragma unroll
     for (int q1 = 0; q1 < NQ1; q1++) {
