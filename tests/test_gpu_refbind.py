@@ -165,3 +165,42 @@ def test_general_core_lists_rejects_bad_ids():
     with pytest.raises(RuntimeError, match="out of range"):
         call(np.array([0, 1, 2, n], np.int64), ids)
     assert float(np.abs(A.vals).max()) == 0.0
+
+
+@pytest.mark.parametrize("name", ["hex_q1_gl3", "tri_p1_lmax3"])
+def test_unmodified_reference_package_bound_to_b200(name, monkeypatch):
+    """The reference package itself (installed under baseline/_ref) with
+    its hooks bound to the B200 library, as INTEGRATION.md section 2 shows:
+    its own assemble() and parallel_assemble() then match its golden
+    outputs."""
+    import bench
+    mf = bench.ref_import()
+    if mf is None:
+        pytest.skip("reference not installed under baseline/_ref")
+    from mollifem import _kernels as RK
+    from mollifem import assembly as RA
+    from mollifem import parallel as RP
+    from paper_2101_08825_b200 import refbind
+    g = Golden(name)
+    m = g.meta
+    mesh = mf.build_mesh(m["dim"], m["omega"], m["h"], m["delta"] + m["eps"],
+                         m["kind"])
+    space = mf.FESpace(mesh, m["degree"])
+    kp = mf.KernelParams(m["dim"], m["delta"], m["eps"], m["kappa"])
+    cfg = mf.AssemblyConfig(L_min=m["L_min"], L_max=m["L_max"],
+                            outer_rule=m["outer_rule"],
+                            inner_rule=m["inner_rule"], strategy="general")
+    monkeypatch.setattr(RA, "_run_general", refbind.run_general)
+    monkeypatch.setattr(RP, "_run_general", refbind.run_general)
+    A = mf.assemble(mesh, space, kp, cfg)
+    assert A.events == int(g["events"])
+    assert rel_frob(A.vals, g["vals"]) <= 1e-10
+    B, ctxs = mf.parallel_assemble(mesh, space, kp, cfg, n_parts=3)
+    assert B.events == int(g["events"])
+    assert rel_frob(B.vals, g["vals"]) <= 1e-10
+    # one level lower: the array-level core
+    monkeypatch.undo()
+    monkeypatch.setattr(RK, "_general_core", refbind.general_core)
+    C = mf.assemble(mesh, space, kp, cfg)
+    assert C.events == int(g["events"])
+    assert rel_frob(C.vals, g["vals"]) <= 1e-10
