@@ -338,7 +338,16 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MF_HEX_MINB)
   }
   __syncwarp();
   double G = 0.0;
-  unsigned c_ev = 0, c_pairs = 0, c_up = 0, c_pl = 0, c_dead = 0, c_full = 0;
+  // warp-uniform event counters live in shared memory (lane 0 updates
+  // them): 6 fewer registers per lane.  Events = up + plateau + dead + full.
+  __shared__ unsigned s_cnt[kWarpsPerBlock][5];
+  unsigned *cnt = s_cnt[wib];
+  if (lane < 5) cnt[lane] = 0;
+  __syncwarp();
+#define MF_CNT(k, v)            \
+  do {                          \
+    if (lane == 0) cnt[k] += (v); \
+  } while (0)
   int cx, cy, cz;
   cell_coords(M.elem_cell[m], M.ncx, M.ncy, cx, cy, cz);
   const int Rs = P.R;
@@ -406,7 +415,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MF_HEX_MINB)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(P.vals + slot0));
         asm volatile("prefetch.global.L2 [%0];" ::"l"(P.vals + slot1));
       }
-      c_pairs++;
+      MF_CNT(0, 1u);
       if (lane < 3) {
         const double lo = M.elem_lo[l * 3 + lane];
         const double hi = M.elem_hi[l * 3 + lane];
@@ -420,7 +429,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MF_HEX_MINB)
       double V[8];
 #pragma unroll
       for (int j = 0; j < 8; j++) V[j] = 0.0;
-      unsigned ev = 0;
       bool live = false;  // warp-uniform: some plateau/full event
       {
         Box root;
@@ -432,18 +440,15 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MF_HEX_MINB)
         const int act = classify(P, root, 1, C.ilo, C.ihi, C.pilo, C.pihi,
                                  tmin, tmax);
         if (act == ACT_UPPER || act == ACT_PLAT) {
-          ev++;
           live = true;
-          (act == ACT_UPPER ? c_up : c_pl)++;
+          MF_CNT(act == ACT_UPPER ? 1 : 2, 1u);
           event_plateau<NO>(P, s_rt, s_rw, C, 32, lane, V);
         } else if (act == ACT_FULL || act == ACT_UPPER_FULL) {
-          ev++;
           live = true;
-          (act == ACT_FULL ? c_full : c_up)++;
+          MF_CNT(act == ACT_FULL ? 4 : 1, 1u);
           run_full<NO>(P, s_rt, s_rw, C, 32, y, lane, V);
         } else if (act == ACT_DEAD) {
-          ev++;
-          c_dead++;
+          MF_CNT(3, 1u);
         } else if (act == ACT_SPLIT) {
           uint32_t *cur = s_split[wib][0], *nxt = s_split[wib][1];
           int nsplit = 1;
@@ -488,12 +493,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MF_HEX_MINB)
               const unsigned mdead = __ballot_sync(0xffffffffu, a == ACT_DEAD);
               const unsigned mup = __ballot_sync(
                   0xffffffffu, a == ACT_UPPER || a == ACT_UPPER_FULL);
-              ev += __popc(mplat) + __popc(mfull) + __popc(mdead);
               live |= (mplat | mfull) != 0u;
-              c_dead += __popc(mdead);
-              c_up += __popc(mup);
-              c_pl += __popc(mplat & ~mup);
-              c_full += __popc(mfull & ~mup);
+              if (lane == 0) {
+                cnt[3] += __popc(mdead);
+                cnt[1] += __popc(mup);
+                cnt[2] += __popc(mplat & ~mup);
+                cnt[4] += __popc(mfull & ~mup);
+              }
               __syncwarp();
               for (unsigned mm = mplat; mm; mm &= mm - 1)
                 event_plateau<NO>(P, s_rt, s_rw, C, __ffs(mm) - 1, lane, V);
@@ -514,7 +520,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MF_HEX_MINB)
           }
         }
       }
-      c_ev += ev;
       // dead-only pairs have an exactly zero block: skip its contraction
       // and read-modify-write (adding zeros changes no value)
       if (live) {
@@ -564,12 +569,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MF_HEX_MINB)
   P.vals[pat_index(P.pat, mdofs[oi + 4], col)] += sc * b1;
   if (lane == 0) {
     unsigned long long *Cn = P.counters;
-    counter_add(Cn + MF_CNT_EVENTS, c_ev);
-    counter_add(Cn + MF_CNT_PAIRS, c_pairs);
-    counter_add(Cn + MF_CNT_EV_UPPER, c_up);
-    counter_add(Cn + MF_CNT_EV_PLATEAU, c_pl);
-    counter_add(Cn + MF_CNT_EV_DEAD, c_dead);
-    counter_add(Cn + MF_CNT_EV_FULL, c_full);
+    counter_add(Cn + MF_CNT_EVENTS, (unsigned long long)cnt[1] + cnt[2] +
+                                        cnt[3] + cnt[4]);
+    counter_add(Cn + MF_CNT_PAIRS, cnt[0]);
+    counter_add(Cn + MF_CNT_EV_UPPER, cnt[1]);
+    counter_add(Cn + MF_CNT_EV_PLATEAU, cnt[2]);
+    counter_add(Cn + MF_CNT_EV_DEAD, cnt[3]);
+    counter_add(Cn + MF_CNT_EV_FULL, cnt[4]);
+#undef MF_CNT
   }
 }
 
