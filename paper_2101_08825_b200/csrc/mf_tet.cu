@@ -42,9 +42,9 @@ constexpr int kTetLevels = 6;
 // size, conflict-free): outer root vertices, the outer inverse map and the
 // inner box -- read rarely, so they need not occupy registers
 constexpr int kTetThreads = 128;
-// (ST_N sets the dynamic shared memory per block, 36 KB at 128 threads:
-// it is an occupancy limit -- 54 doubles per thread measured R4-tet 17.5
-// -> 22.8 s)
+// (ST_N sets the dynamic shared memory per block, 36 KB at 128 threads,
+// and with it the occupancy: 54 doubles per thread measured R4-tet 17.5 ->
+// 22.8 s)
 enum : int { ST_ROOT = 0, ST_V0 = 12, ST_INV = 15, ST_ILO = 24, ST_IHI = 27,
              ST_PILO = 30, ST_PIHI = 33, ST_N = 36 };
 
@@ -385,7 +385,166 @@ __global__ void __launch_bounds__(32 * kTetWarps, MF_TET_MINB(NQ1))
           {
 #pragma unroll
             for (int u = 0; u < 12; u++) st[(ST_ROOT + u) * kTetThreads] = g[u];
+            double e[3][3];
+            const double det = tet_edges(g, e);
+            const double idet = rcp_fast(det);
+            // rows (e2 x e3), (e3 x e1), (e1 x e2) over det (oracle tet_inv)
+#pragma unroll
+            for (int r = 0; r < 3; r++) {
+              const double *u = e[(r + 1) % 3], *v = e[(r + 2) % 3];
+              st[(ST_INV + 3 * r + 0) * kTetThreads] =
+                  (u[1] * v[2] - u[2] * v[1]) * idet;
+              st[(ST_INV + 3 * r + 1) * kTetThreads] =
+                  (u[2] * v[0] - u[0] * v[2]) * idet;
+              st[(ST_INV + 3 * r + 2) * kTetThreads] =
+                  (u[0] * v[1] - u[1] * v[0]) * idet;
+            }
+#pragma unroll
+            for (int k = 0; k < 3; k++) st[(ST_V0 + k) * kTetThreads] = g[k];
+          }
+          double V[NQ1][4];
+#pragma unroll
+          for (int q = 0; q < NQ1; q++)
+#pragma unroll
+            for (int j = 0; j < 4; j++) V[q][j] = 0.0;
+          double SP[4] = {0.0, 0.0, 0.0, 0.0};
+          unsigned ev = 0;
+          bool live = false;  // some plateau/full event: nonzero block
+          // Algorithm 1, depth first over a path code (3 bits per level
+          // below the root); the node is recomputed from the root
+          uint32_t code = 0;
+          int L = 1;
+          for (;;) {
+            double slo[3], shi[3], ilo[3], ihi[3];
+            tet_bbox(g, slo, shi);
+#pragma unroll
+            for (int k = 0; k < 3; k++) {
+              ilo[k] = st[(ST_ILO + k) * kTetThreads];
+              ihi[k] = st[(ST_IHI + k) * kTetThreads];
+            }
+            int act = ACT_NONE;
+            if (L < P.L_min) {
+              act = ACT_SPLIT;
+            } else if (L == P.L_max) {
+              if (aprx_min_d<3>(slo, shi, ilo, ihi) < P.dpe) {
+                if (!P.shortcuts) {
+                  act = ACT_FULL;
+                } else {
+                  // dead / plateau proofs on the point-set boxes (see
+                  // mf_hex.cu classify): every point pair certainly beyond
+                  // delta+eps, or certainly inside delta-eps
+                  double qlo[3], qhi[3], plo[3], phi[3];
+#pragma unroll
+                  for (int k = 0; k < 3; k++) {
+                    const double c =
+                        0.25 * ((g[k] + g[3 + k]) + (g[6 + k] + g[9 + k]));
+                    const double mg = 1e-9 * (shi[k] - slo[k]);
+                    qlo[k] = c + fo * (slo[k] - c) - mg;
+                    qhi[k] = c + fo * (shi[k] - c) + mg;
+                    plo[k] = st[(ST_PILO + k) * kTetThreads];
+                    phi[k] = st[(ST_PIHI + k) * kTetThreads];
+                  }
+                  if (box_dead<3>(P, qlo, qhi, plo, phi))
+                    act = ACT_DEAD;
+                  else if (aprx_max_sq<3>(qlo, qhi, plo, phi) <
+                           P.dm2 * (1.0 - 4e-9))
+                    act = ACT_PLAT;
+                  else
+                    act = ACT_FULL;
+                }
+              }
+            } else if (aprx_max_lt_dme(P,
+                                       aprx_max_sq<3>(slo, shi, ilo, ihi))) {
+              act = ACT_UPPER;
+            } else if (aprx_min_d<3>(slo, shi, ilo, ihi) < P.dpe) {
+              act = ACT_SPLIT;
+            }
+            if (act >= ACT_UPPER) {
+              ev++;
+              if (act == ACT_UPPER) c_up++;
+              if (act == ACT_DEAD) c_dead++;
+              if (act == ACT_PLAT) c_pl++;
+              if (act == ACT_FULL) c_full++;
+              const bool plateau =
+                  act == ACT_PLAT || (act == ACT_UPPER && P.shortcuts);
+              const bool full =
+                  act == ACT_FULL || (act == ACT_UPPER && !P.shortcuts);
+              live |= plateau || full;
+              if (plateau)
+                tet_plateau<NQO>(P, g, O, s_opts, s_ow, SP);
+              else if (full && P.eps > 0.0)
+                tet_full<NQO, NQ1, false>(P, g, O, y, lane, s_opts, s_ow, V);
+              else if (full)
+                tet_full<NQO, NQ1, true>(P, g, O, y, lane, s_opts, s_ow, V);
+            }
+            if (act == ACT_SPLIT) {
+              ++L;  // first child: code bits of level L stay 0
+              double c[12];
+              tet_child(g, 0, c);
+#pragma unroll
+              for (int u = 0; u < 12; u++) g[u] = c[u];
+              continue;
+            }
+            // next sibling, climbing while the current level is exhausted
+            while (L > 1 && ((code >> (3 * (L - 2))) & 7) == 7) {
+              code &= ~(7u << (3 * (L - 2)));
+              --L;
+            }
+            if (L == 1) break;
+            code += 1u << (3 * (L - 2));
+            tet_path(st, code, L, g);
+          }
+          c_ev += ev;
+          // dead-only pairs have an exactly zero block: adding it would
+          // change no value, so the 16 read-modify-writes are skipped
+          if (live) {
+            double spsum = (SP[0] + SP[1]) + (SP[2] + SP[3]);
+            const double sc = -P.scale * scale_in;
+#if MF_TET_LOADS_FIRST
+            // the 16 old values are loaded together before any store, so
+            // their latencies overlap (the compiler cannot hoist them past
+            // the stores itself: it cannot prove the slots distinct)
+            double old[4][4];
+            if constexpr (NQ1 <= MF_TET_LOADS_FIRST_MAXNQ) {
+#pragma unroll
+              for (int j = 0; j < 4; j++) {
+                const int v = c_tet_corner[tout][j];
+                const int gx = x2 + (v & 1), gy = y2 + ((v >> 1) & 1),
+                          gzo = (v >> 2) & 1;
+#pragma unroll
+                for (int i = 0; i < 4; i++)
+                  old[i][j] = P.vals[rowz[i] +
+                                     ((int64_t)gzo * rwy[i] + (gy - rylo[i])) *
+                                         rwx[i] +
+                                     (gx - rxlo[i])];
+              }
+            }
+#endif
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+              double mi = 0.0;
+#pragma unroll
+              for (int q = 0; q < NQ1; q++) mi += s_phiw[q][i];
+#pragma unroll
+              for (int j = 0; j < 4; j++) {
+                double b = mi * SP[j];
+#pragma unroll
+                for (int q = 0; q < NQ1; q++) b = fma(s_phiw[q][i], V[q][j], b);
+                const int v = c_tet_corner[tout][j];
+                const int gx = x2 + (v & 1), gy = y2 + ((v >> 1) & 1),
+                          gzo = (v >> 2) & 1;
+                const int64_t slot =
+                    rowz[i] +
+                    ((int64_t)gzo * rwy[i] + (gy - rylo[i])) * rwx[i] +
+                    (gx - rxlo[i]);
+#if MF_TET_LOADS_FIRST
+                if constexpr (NQ1 <= MF_TET_LOADS_FIRST_MAXNQ)
+                  P.vals[slot] = old[i][j] + sc * b;
+                else
+                  P.vals[slot] += sc * b;
+#else
                 P.vals[slot] += sc * b;
+#endif
               }
             }
 #pragma unroll
