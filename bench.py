@@ -23,9 +23,15 @@ one interface-plane send/recv per slab boundary (parallel.py).  e2e at N>1
 is `assemble_distributed` (upload, slab assembly, exchange, NCCL row-block
 gather to rank 0, D2H on rank 0).
 
-The CPU leg (cpu_baseline / --impl reference) times the oracle
-(oracle/mf_oracle.c, the C restatement of the reference numba cores) on a
-seeded sample of outer elements with all host threads.
+The CPU leg (cpu_baseline / --impl reference) times the UNMODIFIED
+reference (numba, installed under baseline/_ref) on a seeded sample of
+outer elements with all host threads -- its general path, the comparison
+path of the GPU design -- and, once, its default assemble() (strategy
+"auto" -> offset-blocked) in full on a smaller workload
+(cpu_baseline.default_path).  Workloads the reference cannot build (tets,
+Delaunay) fall back to the oracle port (oracle/mf_oracle.c, within 10-20%
+of numba per thread, tools/ref_vs_port.py).  On structured meshes the GPU
+line also reports e2e_default_path: our assemble(strategy="auto").
 """
 
 import argparse
@@ -789,6 +795,31 @@ def run_ours(args):
     }
     if e2e:
         line["e2e"] = e2e
+    if (world == 1 and not args.no_e2e and args.strategy == "general"
+            and mesh.kind in ("tri", "quad", "hex")
+            and not getattr(mesh, "unstructured", False)):
+        # the reference's DEFAULT path on structured meshes is the
+        # offset-blocked strategy (assemble(strategy="auto"),
+        # assembly.py:448-473): the like-for-like end-to-end comparison
+        # with the reference arm's cpu_baseline.default_path
+        from paper_2101_08825_b200 import AssemblyConfig
+        auto = AssemblyConfig(L_max=cfg.L_max, outer_rule=cfg.outer_rule,
+                              inner_rule=cfg.inner_rule, strategy="auto")
+        B = assemble(mesh, space, kp, auto, device=dev)
+        del B
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(2):
+            t = time.perf_counter()
+            B = assemble(mesh, space, kp, auto, device=dev)
+            _ = B.vals[-1]
+            ts.append(time.perf_counter() - t)
+            del B
+        line["e2e_default_path"] = {
+            "value": pairs_all / min(ts), "unit": "pairs/s",
+            "seconds_per_assembly": min(ts),
+            "path": "assemble(strategy='auto') -> GPU offset-blocked "
+                    "(mf_offset_blocks + gather), host in, host out"}
     if world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_sample(name, mesh, space, kp, cfg,
                                           budget_s=args.cpu_budget)
