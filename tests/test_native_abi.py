@@ -40,3 +40,17 @@ def test_compute_calls_fail_loudly_without_gpu():
     from paper_2101_08825_b200 import _native as N
     with pytest.raises(RuntimeError, match="CUDA device"):
         N.lib()
+
+
+def test_overflow_counter_raises():
+    """A kernel that reports dropped work (MF_CNT_OVERFLOW) makes finish()
+    raise instead of returning an incomplete matrix."""
+    import numpy as np
+    import pytest
+    from paper_2101_08825_b200 import _native as N
+    from paper_2101_08825_b200.assembly import check_counters
+    c = np.zeros(N.MF_NCOUNTERS, np.int64)
+    check_counters(c)
+    c[N.CNT_OVERFLOW] = 1
+    with pytest.raises(RuntimeError, match="overflow"):
+        check_counters(c)
