@@ -38,9 +38,6 @@ constexpr int kSplitCap = 64;  // split nodes per level (L_max <= 4)
 #ifndef MF_HEX_MINB
 #define MF_HEX_MINB 4
 #endif
-#ifndef MF_HEX_BATCHAXES
-#define MF_HEX_BATCHAXES 0
-#endif
 
 struct Box {
   double lo[3], hi[3];
@@ -112,25 +109,14 @@ MF_DEV int classify(const AsmParams &P, const Box &g, int L,
 
 // Per-warp uniform state kept in shared memory (not registers) so the
 // event code has the register file to itself.
-// the per-round axes need 33 slots of shared memory per warp: static
-// shared memory stays under 48 KB only up to 3 outer points per axis
-template <int NO>
-constexpr bool batch_axes() {
-  return MF_HEX_BATCHAXES && NO <= 3;
-}
-
 template <int NO>
 struct WarpCtx {
   double ilo[3], ihi[3];           // inner element box
   double pilo[3], pihi[3];         // bounding box of its quadrature points
   double olo[3], ohi[3], oinv[3];  // current outer element box
   double blo[33][3], bhi[33][3];   // event boxes of the round (32 = root)
-  // per event slot of the round (32 = root) when the axes are computed
-  // per round (batch_axes<NO>), else one event at a time: outer 1D
-  // coordinates and weighted pullback shapes
-  static constexpr int kSlots = batch_axes<NO>() ? 33 : 1;
-  double X[kSlots][3][NO];
-  double sh[kSlots][3][2][NO];
+  double X[3][NO];                 // event: outer 1D coordinates
+  double sh[3][2][NO];             // event: weighted pullback shapes
 };
 
 // Phase 0 of an event: lanes (k, a) compute the outer 1D coordinate
@@ -138,11 +124,11 @@ struct WarpCtx {
 // pullback shapes (1-s, s) * w_a on axis k; the x axis also carries
 // cde * |sub-cell| / 8 / 256.
 template <int NO>
-MF_DEV void axes_task(const AsmParams &P, const double *s_rt,
-                      const double *s_rw, WarpCtx<NO> &C, int slot, int task,
-                      double (*X)[NO], double (*sh)[2][NO]) {
-  {
-    const int k = task / NO, a = task - (task / NO) * NO;
+MF_DEV void event_axes_to(const AsmParams &P, const double *s_rt,
+                          const double *s_rw, WarpCtx<NO> &C, int slot,
+                          int lane, double (*X)[NO], double (*sh)[2][NO]) {
+  if (lane < 3 * NO) {
+    const int k = lane / NO, a = lane - (lane / NO) * NO;
     const double lo = C.blo[slot][k], hi = C.bhi[slot][k];
     double wa = s_rw[a];
     if (k == 0) {
@@ -160,34 +146,10 @@ MF_DEV void axes_task(const AsmParams &P, const double *s_rt,
 }
 
 template <int NO>
-MF_DEV double (*ev_X(WarpCtx<NO> &C, int slot))[NO] {
-  return C.X[batch_axes<NO>() ? slot : 0];
-}
-template <int NO>
-MF_DEV double (*ev_sh(WarpCtx<NO> &C, int slot))[2][NO] {
-  return C.sh[batch_axes<NO>() ? slot : 0];
-}
-// the axes of every event of a round (mask of slots), 32 tasks per pass
-template <int NO>
-MF_DEV void round_axes(const AsmParams &P, const double *s_rt,
-                       const double *s_rw, WarpCtx<NO> &C, unsigned mev,
-                       int lane) {
-  const int ntask = 3 * NO * __popc(mev);
-  for (int t = lane; t < ntask; t += 32) {
-    const int e = t / (3 * NO);
-    const int slot = (int)__fns(mev, 0, e + 1);
-    axes_task<NO>(P, s_rt, s_rw, C, slot, t - e * 3 * NO, ev_X(C, slot),
-                  ev_sh(C, slot));
-  }
-  __syncwarp();
-}
-template <int NO>
 MF_DEV void event_axes(const AsmParams &P, const double *s_rt,
                        const double *s_rw, WarpCtx<NO> &C, int slot,
                        int lane) {
-  if (batch_axes<NO>()) return;  // computed per round (round_axes)
-  if (lane < 3 * NO)
-    axes_task<NO>(P, s_rt, s_rw, C, slot, lane, C.X[0], C.sh[0]);
+  event_axes_to<NO>(P, s_rt, s_rw, C, slot, lane, C.X, C.sh);
   __syncwarp();
 }
 
@@ -197,7 +159,6 @@ MF_DEV void event_plateau(const AsmParams &P, const double *s_rt,
                           const double *s_rw, WarpCtx<NO> &C, int slot,
                           int lane, double V[8]) {
   event_axes<NO>(P, s_rt, s_rw, C, slot, lane);
-  double(*SH)[2][NO] = ev_sh(C, slot);
   double S[3][2];
 #pragma unroll
   for (int k = 0; k < 3; k++)
@@ -205,10 +166,10 @@ MF_DEV void event_plateau(const AsmParams &P, const double *s_rt,
     for (int j = 0; j < 2; j++) {
       double s = 0.0;
 #pragma unroll
-      for (int a = 0; a < NO; a++) s += SH[k][j][a];
+      for (int a = 0; a < NO; a++) s += C.sh[k][j][a];
       S[k][j] = s;
     }
-  if (!batch_axes<NO>()) __syncwarp();
+  __syncwarp();
 #pragma unroll
   for (int jz = 0; jz < 2; jz++)
 #pragma unroll
@@ -238,23 +199,21 @@ MF_DEV void event_full(const AsmParams &P, const double *s_rt,
                        const double *s_rw, WarpCtx<NO> &C, int slot,
                        const double y[3], int lane, double V[8]) {
   event_axes<NO>(P, s_rt, s_rw, C, slot, lane);
-  const double(*EX)[NO] = ev_X(C, slot);
-  const double(*SH)[2][NO] = ev_sh(C, slot);
   // the outer y/z weights stay in shared memory (broadcast loads at each
   // use): 24 fewer live registers than register copies
-  const double(*shy)[NO] = SH[1];
-  const double(*shz)[NO] = SH[2];
+  const double(*shy)[NO] = C.sh[1];
+  const double(*shz)[NO] = C.sh[2];
   double sq1[NO], sq2[NO];
 #pragma unroll
   for (int b = 0; b < NO; b++) {
-    const double d1 = xsub(EX[1][b], y[1]);
-    const double d2 = xsub(EX[2][b], y[2]);
+    const double d1 = xsub(C.X[1][b], y[1]);
+    const double d2 = xsub(C.X[2][b], y[2]);
     sq1[b] = xmul(d1, d1);
     sq2[b] = xmul(d2, d2);
   }
 #pragma unroll
   for (int a = 0; a < NO; a++) {
-    const double d0 = xsub(EX[0][a], y[0]);
+    const double d0 = xsub(C.X[0][a], y[0]);
     const double sq0 = xmul(d0, d0);
     double W[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // [jy][jz]
 #pragma unroll
@@ -289,7 +248,7 @@ MF_DEV void event_full(const AsmParams &P, const double *s_rt,
         W[jy][1] = fma(u1, shy[jy][b], W[jy][1]);
       }
     }
-    const double x0 = SH[0][0][a], x1 = SH[0][1][a];
+    const double x0 = C.sh[0][0][a], x1 = C.sh[0][1][a];
 #pragma unroll
     for (int jz = 0; jz < 2; jz++)
 #pragma unroll
@@ -298,7 +257,7 @@ MF_DEV void event_full(const AsmParams &P, const double *s_rt,
         V[1 + 2 * jy + 4 * jz] = fma(x1, W[jy][jz], V[1 + 2 * jy + 4 * jz]);
       }
   }
-  if (!batch_axes<NO>()) __syncwarp();
+  __syncwarp();
 }
 
 template <int NO>
@@ -480,13 +439,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MF_HEX_MINB)
         }
         const int act = classify(P, root, 1, C.ilo, C.ihi, C.pilo, C.pihi,
                                  tmin, tmax);
-        if (batch_axes<NO>() && act != ACT_SPLIT && act != ACT_NONE &&
-            act != ACT_DEAD) {
-          if (lane < 3 * NO)
-            axes_task<NO>(P, s_rt, s_rw, C, 32, lane, ev_X(C, 32),
-                          ev_sh(C, 32));
-          __syncwarp();
-        }
         if (act == ACT_UPPER || act == ACT_PLAT) {
           live = true;
           MF_CNT(act == ACT_UPPER ? 1 : 2, 1u);
@@ -549,8 +501,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MF_HEX_MINB)
                 cnt[4] += __popc(mfull & ~mup);
               }
               __syncwarp();
-              if (batch_axes<NO>() && (mplat | mfull))
-                round_axes<NO>(P, s_rt, s_rw, C, mplat | mfull, lane);
               for (unsigned mm = mplat; mm; mm &= mm - 1)
                 event_plateau<NO>(P, s_rt, s_rw, C, __ffs(mm) - 1, lane, V);
               for (unsigned mm = mfull; mm; mm &= mm - 1)
