@@ -143,6 +143,9 @@ int mf_exclusive_scan(const int64_t *counts, int64_t n, int64_t *ptr,
 #define MF_FLAG_ELEMENT_THREADS 4 /* small structured P1 triangle meshes:
                                      keep the thread-per-element kernel
                                      instead of the row-split one */
+#define MF_FLAG_HEX_LEVELS 8      /* hex Q1 meshes with L_max == 2: keep the
+                                     level-synchronous kernel (k_hex) instead
+                                     of the separable one (k_hex2) */
 size_t mf_general_workspace_bytes(const MfMesh *mesh, const MfRules *rules,
                                   int64_t n_inner);
 int mf_general_core(const MfMesh *mesh, const MfRules *rules,

@@ -19,6 +19,7 @@ ABI_VERSION = 3
 FLAG_FORCE_GENERIC = 1
 FLAG_NO_SHORTCUTS = 2
 FLAG_ELEMENT_THREADS = 4
+FLAG_HEX_LEVELS = 8
 
 
 class MfMesh(C.Structure):

@@ -43,6 +43,8 @@ cudaError_t mf_launch_blocked_scatter(const AsmParams &, int, int, int,
 cudaError_t mf_launch_hex(const AsmParams &, cudaStream_t);
 cudaError_t mf_launch_2d(const AsmParams &, cudaStream_t);
 bool mf_hex_supported(const AsmParams &);
+cudaError_t mf_launch_hex2(const AsmParams &, cudaStream_t);
+bool mf_hex2_supported(const AsmParams &);
 bool mf_2d_supported(const AsmParams &);
 cudaError_t mf_launch_tet(const AsmParams &, double *, cudaStream_t);
 size_t mf_tet_scratch_doubles(const AsmParams &, int64_t);
@@ -223,6 +225,14 @@ AsmParams make_params(const MfMesh *mesh, const MfRules *rules,
     P.hi_dm2 = (int32_t)(b >> 32);
     memcpy(&b, &P.dp2, 8);
     P.hi_dp2 = (int32_t)(b >> 32);
+    // scaled shell edges: r = alpha - sqrt(q) leaves [-1, 1] by at most
+    // 2^-20 relative there, where xi is flat to fourth order
+    double ql = (P.alpha - 1.0) * (P.alpha - 1.0);
+    double qh = (P.alpha + 1.0) * (P.alpha + 1.0);
+    memcpy(&b, &ql, 8);
+    P.hq_lo = (int32_t)(b >> 32) - 1;
+    memcpy(&b, &qh, 8);
+    P.hq_hi = (int32_t)(b >> 32) + 1;
   }
   P.nl_box = mesh->dim == 3 ? (mesh->degree + 1) * (mesh->degree + 1) *
                                   (mesh->degree + 1)
@@ -382,6 +392,7 @@ int mf_general_core(const MfMesh *mesh, const MfRules *rules,
     return cuda_status(ef, "mf_general_core scratch");
   }
   bool use_hex = !force_generic && mf_hex_supported(P);
+  bool use_hex2 = use_hex && mf_hex2_supported(P);
   bool use_2d = !force_generic && !use_hex && mf_2d_supported(P);
   for (int c = 0; c < ncolors; c++) {
     int64_t n = color_ptr[c + 1] - color_ptr[c];
@@ -389,7 +400,9 @@ int mf_general_core(const MfMesh *mesh, const MfRules *rules,
     P.inner = inner_sorted + color_ptr[c];
     P.n_inner = n;
     cudaError_t e;
-    if (use_hex) {
+    if (use_hex2) {
+      e = mf_launch_hex2(P, s);
+    } else if (use_hex) {
       e = mf_launch_hex(P, s);
     } else if (use_2d) {
       e = mf_launch_2d(P, s);

@@ -46,6 +46,8 @@ struct AsmParams {
   double half_inv_eps;    // 0.5/eps
   int32_t hi_dm2, hi_dp2; // high 32-bit words of dm2 / dp2 (non-negative
                           // doubles order like their bit patterns)
+  int32_t hq_lo, hq_hi;   // high words of the shell edges (alpha -/+ 1)^2
+                          // of q = d^2/eps^2, widened by one unit
   int32_t nl_box, nl_tri;
   int32_t shortcuts;      // plateau/dead event shortcuts enabled
   double *scratch;        // per-thread scratch (generic kernel)

@@ -1,0 +1,497 @@
+// mf_hex2.cu -- hex Q1 assembly kernel for L_max == 2 with eps > 0 and
+// the shortcuts on (the BASELINE #4/#5 stand-ins R4/R5).
+//
+// Same work decomposition and results as k_hex (mf_hex.cu: one warp per
+// inner element, lane = inner quadrature point, colour-scheduled
+// scatter), restructured around what L_max == 2 makes separable:
+//
+// * The root sub-cell and its 8 children are axis-aligned boxes built
+//   from 3 intervals per axis (lower half, upper half, whole).  Every
+//   Algorithm-1 quantity is a max or an ordered sum of per-axis terms
+//   (_aprx_min / _aprx_max, _kernels.py:80-102), so 9 lanes compute the
+//   per-(axis, interval) terms once per pair with the reference's exact
+//   arithmetic, and 9 lanes (8 children + root) combine three of them
+//   each: one classification pass per pair instead of a root pass, a
+//   child pass and a path-box recomputation.
+// * The outer quadrature coordinates and weighted pullback shapes of an
+//   event are per-axis too: the same 9 lanes compute them once per pair
+//   for all 8 children (k_hex: once per event).
+// * Plateau events (mu == 1 at every point pair) add the same rank-1
+//   term to every inner point, so they are folded into the pair's block
+//   through sum_q1 phiw[q1][i] instead of through V.
+// * Full events evaluate the mollifier on coordinates scaled by 1/eps:
+//   q = |x - y|^2 / eps^2 has its high word clamped to the shell
+//   [(alpha-1)^2, (alpha+1)^2] with integer min/max (xi(+-1) = 256 / 0 and
+//   four vanishing derivatives there make the 2^-20 slack invisible,
+//   < 1e-21), one MUFU rsqrt seed y, and the Newton step folded into
+//     r = alpha - u0 (1.5 - 0.5 y u0),  u0 = q y
+//   (3 DP operations; same 1.5 e^2 error as k_hex's 5-operation form),
+//   then the degree-9 xi: 9 DP operations per point pair, no selects.
+// * The candidate boxes of a 32-cell batch are staged in shared memory by
+//   the lanes that found them, so a pair starts without a global load.
+//
+// Events are counted exactly as the reference does (same aprx_min /
+// aprx_max decisions, bit for bit); dead / plateau / full only choose the
+// form of the arithmetic.
+#include "mf_common.cuh"
+
+namespace {
+
+constexpr int kWarps2 = 4;
+#ifndef MF_HEX2_MINB
+#define MF_HEX2_MINB 4
+#endif
+
+enum : int { A_NONE = 0, A_SPLIT = 1, A_UPPER = 2, A_PLAT = 3, A_DEAD = 4,
+             A_FULL = 5 };
+
+template <int NO>
+struct Ctx2 {
+  double ilo[3], ihi[3];    // inner element box
+  double pilo[3], pihi[3];  // bounding box of its quadrature points
+  double box[32][6];        // candidate boxes of the batch (lo[3], hi[3])
+  double met[9][4];         // (axis, interval): gap, max-sep^2, point-set
+                            // gap^2, point-set max-sep^2
+  double X[9][NO];          // (axis, interval): outer coordinates / eps
+  double sh[9][2][NO];      // weighted pullback shapes (jacobian folded in)
+  double S[9][2];           // their sums over the rule
+};
+
+// 256 xi((delta - d)/eps) from the scaled squared distance q = d^2/eps^2
+MF_DEV double xi256_scaled(const AsmParams &P, double q) {
+  int hi = __double2hiint(q);
+  hi = min(max(hi, P.hq_lo), P.hq_hi);
+  const double qc = __hiloint2double(hi, __double2loint(q));
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(qc));
+  const double hy = __hiloint2double(__double2hiint(y) - 0x00100000, 0);
+  const double u0 = qc * y;
+  const double t = fma(-hy, u0, 1.5);
+  const double r = fma(-u0, t, P.alpha);
+  const double r2 = r * r;
+  double p = fma(35.0, r2, -180.0);
+  p = fma(p, r2, 378.0);
+  p = fma(p, r2, -420.0);
+  p = fma(p, r2, 315.0);
+  return fma(p, r, 128.0);
+}
+
+// Full event of child (hx, hy, hz): lane q1 evaluates its NO^3 point pairs
+// and contracts them by sum factorisation (z, then y, then x) into V.
+template <int NO>
+MF_DEV void event_full2(const AsmParams &P, const Ctx2<NO> &C, int ix, int iy,
+                        int iz, const double ys[3], double V[8]) {
+  const double *Xx = C.X[ix], *Xy = C.X[iy], *Xz = C.X[iz];
+  const double(*shx)[NO] = C.sh[ix];
+  const double(*shy)[NO] = C.sh[iy];
+  const double(*shz)[NO] = C.sh[iz];
+  double sq1[NO], sq2[NO];
+#pragma unroll
+  for (int b = 0; b < NO; b++) {
+    const double d1 = Xy[b] - ys[1];
+    const double d2 = Xz[b] - ys[2];
+    sq1[b] = d1 * d1;
+    sq2[b] = d2 * d2;
+  }
+#pragma unroll
+  for (int a = 0; a < NO; a++) {
+    const double d0 = Xx[a] - ys[0];
+    double W[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // [jy][jz]
+#pragma unroll
+    for (int b = 0; b < NO; b++) {
+      const double sxy = fma(d0, d0, sq1[b]);
+      double mu[NO];
+#pragma unroll
+      for (int c = 0; c < NO; c++) mu[c] = xi256_scaled(P, sxy + sq2[c]);
+      double u0 = 0.0, u1 = 0.0;  // z contraction
+#pragma unroll
+      for (int c = 0; c < NO; c++) {
+        u0 = fma(mu[c], shz[0][c], u0);
+        u1 = fma(mu[c], shz[1][c], u1);
+      }
+#pragma unroll
+      for (int jy = 0; jy < 2; jy++) {
+        W[jy][0] = fma(u0, shy[jy][b], W[jy][0]);
+        W[jy][1] = fma(u1, shy[jy][b], W[jy][1]);
+      }
+    }
+    const double x0 = shx[0][a], x1 = shx[1][a];
+#pragma unroll
+    for (int jz = 0; jz < 2; jz++)
+#pragma unroll
+      for (int jy = 0; jy < 2; jy++) {
+        V[2 * jy + 4 * jz] = fma(x0, W[jy][jz], V[2 * jy + 4 * jz]);
+        V[1 + 2 * jy + 4 * jz] = fma(x1, W[jy][jz], V[1 + 2 * jy + 4 * jz]);
+      }
+  }
+}
+
+template <int NO, int NI>
+__global__ void __launch_bounds__(kWarps2 * 32, MF_HEX2_MINB)
+    k_hex2(AsmParams P) {
+  constexpr int NQ1 = NI * NI * NI;
+  __shared__ double2 s_phiw2[NQ1][4];  // w_ref[q1] * PHI1[q1][i], [i + 4]
+  __shared__ double s_phi[NQ1][8];     // PHI1[q1][i]
+  __shared__ double s_pw[8];           // sum_q1 w_ref[q1] PHI1[q1][i]
+  __shared__ double s_rt[NO], s_rw[NO];
+  __shared__ Ctx2<NO> s_ctx[kWarps2];
+  __shared__ double s_buf[kWarps2][NQ1][9];
+  __shared__ unsigned s_cnt[kWarps2][5];
+
+  const MfMesh &M = P.mesh;
+  const MfRules &Rr = P.rules;
+  for (int i = threadIdx.x; i < NQ1 * 8; i += blockDim.x) {
+    const int q = i / 8, j = i % 8;
+    const double ph = Rr.phi_box_in[q * 8 + j];
+    s_phi[q][j] = ph;
+    const double pw = Rr.box_in_w[q] * ph;
+    if (j < 4)
+      s_phiw2[q][j].x = pw;
+    else
+      s_phiw2[q][j - 4].y = pw;
+  }
+  if (threadIdx.x < NO) {
+    s_rt[threadIdx.x] = xmul(xadd(Rr.box_out_x1d[threadIdx.x], 1.0), 0.5);
+    s_rw[threadIdx.x] = Rr.box_out_w1d[threadIdx.x];
+  }
+  if (threadIdx.x >= 32 && threadIdx.x < 40) {
+    const int j = threadIdx.x - 32;
+    double s = 0.0;
+    for (int q = 0; q < NQ1; q++)
+      s += Rr.box_in_w[q] * Rr.phi_box_in[q * 8 + j];
+    s_pw[j] = s;
+  }
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t t = (int64_t)blockIdx.x * kWarps2 + wib;
+  if (t >= P.n_inner) return;
+  Ctx2<NO> &C = s_ctx[wib];
+  double(*buf)[9] = s_buf[wib];
+  unsigned *cnt = s_cnt[wib];
+
+  const int64_t m = P.inner[t];
+  if (lane < 3) {
+    C.ilo[lane] = M.elem_lo[m * 3 + lane];
+    C.ihi[lane] = M.elem_hi[m * 3 + lane];
+  }
+  if (lane < 5) cnt[lane] = 0;
+  __syncwarp();
+  const double jac_in = (0.5 * (C.ihi[0] - C.ilo[0])) *
+                        (0.5 * (C.ihi[1] - C.ilo[1])) *
+                        (0.5 * (C.ihi[2] - C.ilo[2]));
+  const bool active = lane < NQ1;
+  // this lane's inner point, scaled by 1/eps; inactive lanes sit far away
+  // (their q clamps to the outer shell edge: mu = 0)
+  double ys[3] = {1e100, 1e100, 1e100};
+  if (active) {
+#pragma unroll
+    for (int k = 0; k < 3; k++)
+      ys[k] = P.inv_eps *
+              xadd(C.ilo[k],
+                   xmul(xmul(xadd(Rr.box_in_pts[lane * 3 + k], 1.0), 0.5),
+                        xsub(C.ihi[k], C.ilo[k])));
+  }
+  // point-set bounding boxes (outer rule nodes are sorted ascending)
+  const double tmin = s_rt[0], tmax = s_rt[NO - 1];
+  if (lane < 3) {
+    const double w = C.ihi[lane] - C.ilo[lane];
+    double pmn = 1e300, pmx = -1e300;
+    for (int q = 0; q < NI; q++) {
+      const double tq = xmul(xadd(Rr.box_in_x1d[q], 1.0), 0.5);
+      pmn = fmin(pmn, C.ilo[lane] + tq * w);
+      pmx = fmax(pmx, C.ilo[lane] + tq * w);
+    }
+    // widened by a relative 1e-12 of the cell: rounding of the points'
+    // exact coordinates can never leave the box
+    C.pilo[lane] = pmn - 1e-12 * w;
+    C.pihi[lane] = pmx + 1e-12 * w;
+  }
+  __syncwarp();
+  double G = 0.0;
+  int cx, cy, cz;
+  cell_coords(M.elem_cell[m], M.ncx, M.ncy, cx, cy, cz);
+  const int Rs = P.R;
+  const int xlo = max(cx - Rs, 0), xhi = min(cx + Rs, M.ncx - 1);
+  const int ylo = max(cy - Rs, 0), yhi = min(cy + Rs, M.ncy - 1);
+  const int zlo = max(cz - Rs, 0), zhi = min(cz + Rs, M.ncz - 1);
+  const int nx = xhi - xlo + 1, ny = yhi - ylo + 1;
+  const int ncell = nx * ny * (zhi - zlo + 1);
+  // this lane's two A21 rows: local DOFs oi and oi + 4 of m (same x/y
+  // corner, z and z+1); row box of the implicit pattern per row
+  const int oj = lane & 7, oi = lane >> 3;
+  int rx0, ry0, rz0, rz1, rwx, rwy;
+  int64_t rb0, rb1;
+  {
+    const int gx = cx + (oi & 1), gy = cy + ((oi >> 1) & 1);
+    const int K = P.pat.K;
+    rx0 = max(gx - K, 0);
+    rwx = min(gx + K, P.pat.NX - 1) - rx0 + 1;
+    ry0 = max(gy - K, 0);
+    rwy = min(gy + K, P.pat.NY - 1) - ry0 + 1;
+    rz0 = max(cz - K, 0);
+    rz1 = max(cz + 1 - K, 0);
+    const int64_t *md = M.elem_dofs + m * M.nloc_max;
+    rb0 = P.pat.rowptr[md[oi]];
+    rb1 = P.pat.rowptr[md[oi + 4]];
+  }
+  const double pw0 = s_pw[oi], pw1 = s_pw[oi + 4];
+  const double dead2 = P.dp2 * (1.0 + 1e-9), plat2 = P.dm2 * (1.0 - 4e-9);
+
+  for (int base = 0; base < ncell; base += 32) {
+    const int ci = base + lane;
+    bool found = false;
+    int cpos = 0;  // candidate cell, packed x | y << 10 | z << 20
+    if (ci < ncell) {
+      const int x2 = xlo + ci % nx;
+      const int tt = ci / nx;
+      const int y2 = ylo + tt % ny;
+      const int z2 = zlo + tt / ny;
+      const int64_t c2 = ((int64_t)z2 * M.ncy + y2) * M.ncx + x2;
+      const int64_t l = M.cell_ptr[c2];
+      if (l < M.cell_ptr[c2 + 1] && P.outer_mask[l]) {
+        // candidate test of _count_candidates (_kernels.py:1225-1233)
+        double gap = 0.0, lo[3], hi[3];
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+          lo[k] = M.elem_lo[l * 3 + k];
+          hi[k] = M.elem_hi[l * 3 + k];
+          const double d1 = xsub(lo[k], C.ihi[k]);
+          const double d2 = xsub(C.ilo[k], hi[k]);
+          if (d1 > gap) gap = d1;
+          if (d2 > gap) gap = d2;
+        }
+        if (gap < P.dpe) {
+          found = true;
+          cpos = x2 | (y2 << 10) | (z2 << 20);
+#pragma unroll
+          for (int k = 0; k < 3; k++) {
+            C.box[lane][k] = lo[k];
+            C.box[lane][3 + k] = hi[k];
+          }
+        }
+      }
+    }
+    unsigned mask = __ballot_sync(0xffffffffu, found);
+    if (lane == 0) cnt[0] += __popc(mask);
+    __syncwarp();
+    while (mask) {
+      const int src = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const int lpos = __shfl_sync(0xffffffffu, cpos, src);
+      // this lane's two value slots of the pair's A21 block: column DOF oj
+      // of l sits at cell(l) + corner offset (hex Q1 DOF grid = vertex
+      // grid, fe_space.py:68-80); prefetched into L2 now, written at the
+      // end of the pair
+      int64_t slot0, slot1;
+      {
+        const int gx = (lpos & 1023) + (oj & 1);
+        const int gy = ((lpos >> 10) & 1023) + ((oj >> 1) & 1);
+        const int gz = (lpos >> 20) + (oj >> 2);
+        slot0 = rb0 + ((int64_t)(gz - rz0) * rwy + (gy - ry0)) * rwx +
+                (gx - rx0);
+        slot1 = rb1 + ((int64_t)(gz - rz1) * rwy + (gy - ry0)) * rwx +
+                (gx - rx0);
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(P.vals + slot0));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(P.vals + slot1));
+      }
+      // ---- phase 0: per-(axis, interval) terms, lanes 0..8 ----
+      if (lane < 9) {
+        const int k = lane / 3, h = lane - 3 * (lane / 3);
+        const double olo = C.box[src][k], ohi = C.box[src][3 + k];
+        const double mid = xmul(0.5, xadd(olo, ohi));  // _kernels.py:262
+        const double lo = (h == 1) ? mid : olo;
+        const double hi = (h == 0) ? mid : ohi;
+        // cell boxes: _aprx_min / _aprx_max terms, exact
+        const double d1 = xsub(lo, C.ihi[k]);
+        const double d2 = xsub(C.ilo[k], hi);
+        double g = 0.0;
+        if (d1 > g) g = d1;
+        if (d2 > g) g = d2;
+        const double a = xmul(d1, d1), b = xmul(d2, d2);
+        C.met[lane][0] = g;
+        C.met[lane][1] = (a > b) ? a : b;
+        // point-set boxes: dead / plateau proofs (1e-9 margins)
+        const double w = hi - lo;
+        const double qlo = lo + tmin * w, qhi = lo + tmax * w;
+        const double e1 = qlo - C.pihi[k], e2 = C.pilo[k] - qhi;
+        const double gd = fmax(fmax(e1, e2), 0.0);
+        C.met[lane][2] = gd * gd;
+        C.met[lane][3] = fmax(e1 * e1, e2 * e2);
+        // outer points and weighted pullback shapes of this interval
+        const double oinv = rcp_fast(ohi - olo);
+        double hw = 0.5 * w;
+        if (k == 0) hw *= P.cde * (1.0 / 256.0);
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int q = 0; q < NO; q++) {
+          const double x = xadd(lo, xmul(s_rt[q], xsub(hi, lo)));
+          const double sx = (x - olo) * oinv;
+          const double wa = s_rw[q] * hw;
+          const double f0 = (1.0 - sx) * wa, f1 = sx * wa;
+          C.X[lane][q] = x * P.inv_eps;
+          C.sh[lane][0][q] = f0;
+          C.sh[lane][1][q] = f1;
+          s0 += f0;
+          s1 += f1;
+        }
+        C.S[lane][0] = s0;
+        C.S[lane][1] = s1;
+      }
+      __syncwarp();
+      // ---- classification: lanes 0..7 = children, lane 8 = root ----
+      int act = A_NONE;
+      const int ix = (lane < 8) ? (lane & 1) : 2;
+      const int iy = 3 + ((lane < 8) ? ((lane >> 1) & 1) : 2);
+      const int iz = 6 + ((lane < 8) ? ((lane >> 2) & 1) : 2);
+      if (lane < 9) {
+        const double amin =
+            fmax(fmax(C.met[ix][0], C.met[iy][0]), C.met[iz][0]);
+        if (lane == 8) {
+          if (P.L_min > 1) {
+            act = A_SPLIT;
+          } else {
+            const double s =
+                xadd(xadd(C.met[ix][1], C.met[iy][1]), C.met[iz][1]);
+            if (aprx_max_lt_dme(P, s))
+              act = A_UPPER;
+            else if (amin < P.dpe)
+              act = A_SPLIT;
+          }
+        } else if (amin < P.dpe) {
+          const double sd = C.met[ix][2] + C.met[iy][2] + C.met[iz][2];
+          const double sp = C.met[ix][3] + C.met[iy][3] + C.met[iz][3];
+          act = (sd >= dead2) ? A_DEAD : (sp < plat2) ? A_PLAT : A_FULL;
+        }
+      }
+      const int ract = __shfl_sync(0xffffffffu, act, 8);
+      unsigned mfull = 0u, mplat = 0u;
+      if (ract == A_UPPER) {
+        mplat = 1u << 8;
+        if (lane == 0) cnt[1] += 1u;
+      } else if (ract == A_SPLIT) {
+        const unsigned kids = 0xffu;
+        mfull = __ballot_sync(0xffffffffu, act == A_FULL) & kids;
+        mplat = __ballot_sync(0xffffffffu, act == A_PLAT) & kids;
+        const unsigned mdead = __ballot_sync(0xffffffffu, act == A_DEAD) & kids;
+        if (lane == 0) {
+          cnt[2] += __popc(mplat);
+          cnt[3] += __popc(mdead);
+          cnt[4] += __popc(mfull);
+        }
+      }
+      if (mfull | mplat) {
+        // plateau events: V[q1][j] += 256 Sx[jx] Sy[jy] Sz[jz] for every
+        // q1; lane (oi, oj) keeps component oj and the sum over j
+        double vp = 0.0, gp = 0.0;
+        for (unsigned mm = mplat; mm; mm &= mm - 1) {
+          const int c = __ffs(mm) - 1;
+          const int jx = (c < 8) ? (c & 1) : 2;
+          const int jy = 3 + ((c < 8) ? ((c >> 1) & 1) : 2);
+          const int jz = 6 + ((c < 8) ? ((c >> 2) & 1) : 2);
+          vp = fma(C.S[jx][oj & 1] * C.S[jy][(oj >> 1) & 1],
+                   C.S[jz][oj >> 2], vp);
+          gp = fma((C.S[jx][0] + C.S[jx][1]) * (C.S[jy][0] + C.S[jy][1]),
+                   C.S[jz][0] + C.S[jz][1], gp);
+        }
+        vp *= 256.0;
+        gp *= 256.0;
+        double b0 = pw0 * vp, b1 = pw1 * vp;
+        G += gp;
+        if (mfull) {
+          double V[8];
+#pragma unroll
+          for (int j = 0; j < 8; j++) V[j] = 0.0;
+          for (unsigned mm = mfull; mm; mm &= mm - 1) {
+            const int c = __ffs(mm) - 1;
+            event_full2<NO>(P, C, c & 1, 3 + ((c >> 1) & 1),
+                            6 + ((c >> 2) & 1), ys, V);
+          }
+          // b21[i][j] = -jac_in * sum_q1 phiw[q1][i] V[q1][j]
+          if (active) {
+#pragma unroll
+            for (int j = 0; j < 8; j++) buf[lane][j] = V[j];
+          }
+          double gs = 0.0;
+#pragma unroll
+          for (int j = 0; j < 8; j++) gs += V[j];
+          G += gs;
+          __syncwarp();
+#pragma unroll
+          for (int q = 0; q < NQ1; q++) {
+            const double v = buf[q][oj];
+            const double2 pw = s_phiw2[q][oi];
+            b0 = fma(pw.x, v, b0);
+            b1 = fma(pw.y, v, b1);
+          }
+        }
+        const double sc = -P.scale * jac_in;
+        // both old values loaded before either store (distinct rows; the
+        // compiler cannot prove it and would serialise the two RMWs)
+        const double o0 = P.vals[slot0], o1 = P.vals[slot1];
+        P.vals[slot0] = o0 + sc * b0;
+        P.vals[slot1] = o1 + sc * b1;
+      }
+      __syncwarp();
+    }
+  }
+  // A22 for the whole element: jac_in * sum_q1 G[q1] phiw[q1][i] phi[q1][j]
+  if (active) buf[lane][8] = G;
+  __syncwarp();
+  double b0 = 0.0, b1 = 0.0;
+#pragma unroll
+  for (int q = 0; q < NQ1; q++) {
+    const double gq = buf[q][8] * s_phi[q][oj];
+    const double2 pw = s_phiw2[q][oi];
+    b0 = fma(pw.x, gq, b0);
+    b1 = fma(pw.y, gq, b1);
+  }
+  const int64_t *mdofs = M.elem_dofs + m * M.nloc_max;
+  const int64_t col = mdofs[oj];
+  const double sc = P.scale * jac_in;
+  P.vals[pat_index(P.pat, mdofs[oi], col)] += sc * b0;
+  P.vals[pat_index(P.pat, mdofs[oi + 4], col)] += sc * b1;
+  if (lane == 0) {
+    unsigned long long *Cn = P.counters;
+    counter_add(Cn + MF_CNT_EVENTS,
+                (unsigned long long)cnt[1] + cnt[2] + cnt[3] + cnt[4]);
+    counter_add(Cn + MF_CNT_PAIRS, cnt[0]);
+    counter_add(Cn + MF_CNT_EV_UPPER, cnt[1]);
+    counter_add(Cn + MF_CNT_EV_PLATEAU, cnt[2]);
+    counter_add(Cn + MF_CNT_EV_DEAD, cnt[3]);
+    counter_add(Cn + MF_CNT_EV_FULL, cnt[4]);
+  }
+}
+
+template <int NO, int NI>
+cudaError_t launch2(const AsmParams &P, cudaStream_t s) {
+  const int64_t grid = (P.n_inner + kWarps2 - 1) / kWarps2;
+  k_hex2<NO, NI><<<(unsigned)grid, kWarps2 * 32, 0, s>>>(P);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// L_max == 2 fast path of mf_hex_supported() meshes
+bool mf_hex2_supported(const AsmParams &P) {
+#ifdef MF_NO_HEX2  // A/B builds only
+  return false;
+#endif
+  return P.L_max == 2 && P.shortcuts && P.eps > 0.0 &&
+         !(P.flags & MF_FLAG_HEX_LEVELS);
+}
+
+cudaError_t mf_launch_hex2(const AsmParams &P, cudaStream_t s) {
+  const int no = P.rules.n1d_box_out, ni = P.rules.n1d_box_in;
+  if (ni == 3) {
+    if (no == 2) return launch2<2, 3>(P, s);
+    if (no == 3) return launch2<3, 3>(P, s);
+    if (no == 4) return launch2<4, 3>(P, s);
+  } else if (ni == 2) {
+    if (no == 2) return launch2<2, 2>(P, s);
+    if (no == 3) return launch2<3, 2>(P, s);
+    if (no == 4) return launch2<4, 2>(P, s);
+  }
+  return cudaErrorNotSupported;
+}
