@@ -218,6 +218,7 @@ AsmParams make_params(const MfMesh *mesh, const MfRules *rules,
   P.dme2_hi = dm * dm * (1.0 + 4e-12);
   P.inv_eps = kern->eps > 0.0 ? 1.0 / kern->eps : 0.0;
   P.alpha = kern->delta * P.inv_eps;
+  P.alpha2 = 2.0 * P.alpha;
   P.half_inv_eps = 0.5 * P.inv_eps;
   {
     int64_t b;

@@ -43,6 +43,7 @@ struct AsmParams {
   double dm2, dp2;        // squared        (_kernels.py:412-413)
   double dme2_lo, dme2_hi;// sqrt-free decision band for aprx_max < dme
   double inv_eps, alpha;  // 1/eps and delta/eps (eps > 0 kernels)
+  double alpha2;          // 2 delta/eps
   double half_inv_eps;    // 0.5/eps
   int32_t hi_dm2, hi_dp2; // high 32-bit words of dm2 / dp2 (non-negative
                           // doubles order like their bit patterns)

@@ -23,10 +23,16 @@
 //   q = |x - y|^2 / eps^2 has its high word clamped to the shell
 //   [(alpha-1)^2, (alpha+1)^2] with integer min/max (xi(+-1) = 256 / 0 and
 //   four vanishing derivatives there make the 2^-20 slack invisible,
-//   < 1e-21), one MUFU rsqrt seed y, and the Newton step folded into
-//     r = alpha - u0 (1.5 - 0.5 y u0),  u0 = q y
+//   < 1e-21), one MUFU rsqrt seed z, and the Newton step folded into
+//     2 r = 2 alpha - W (3 - W z),  W = q z
 //   (3 DP operations; same 1.5 e^2 error as k_hex's 5-operation form),
-//   then the degree-9 xi: 9 DP operations per point pair, no selects.
+//   then the degree-9 xi in 2 r: 9 DP operations per point pair, no
+//   selects, no integer fix-ups.
+// * Measured on B200: the kernel is dispatch-bound.  FP64 and integer-ALU
+//   instructions occupy an SM sub-partition's dispatch port for 2 cycles,
+//   everything else for 1; 2 (FP64 + ALU) + rest reproduces the SM active
+//   cycles of the ncu capture to 0.3%.  More warps or more interleaved
+//   chains change nothing (measured); only fewer instructions do.
 // * The candidate boxes of a 32-cell batch are staged in shared memory by
 //   the lanes that found them, so a pair starts without a global load.
 //
@@ -37,10 +43,13 @@
 
 namespace {
 
-constexpr int kWarps2 = 4;
-#ifndef MF_HEX2_MINB
-#define MF_HEX2_MINB 4
+#ifndef MF_HEX2_WARPS
+#define MF_HEX2_WARPS 1
 #endif
+#ifndef MF_HEX2_MINB
+#define MF_HEX2_MINB 20
+#endif
+constexpr int kWarps2 = MF_HEX2_WARPS;
 
 enum : int { A_NONE = 0, A_SPLIT = 1, A_UPPER = 2, A_PLAT = 3, A_DEAD = 4,
              A_FULL = 5 };
@@ -55,25 +64,47 @@ struct Ctx2 {
   double X[9][NO];          // (axis, interval): outer coordinates / eps
   double sh[9][2][NO];      // weighted pullback shapes (jacobian folded in)
   double S[9][2];           // their sums over the rule
+  double jac_in;            // inner jacobian
+  long long rb[32][2];      // per lane: value base of its two A21 rows
+  int rbox[32][6];          // per lane: row box x0, y0, z0, z1, wx, wy
 };
 
-// 256 xi((delta - d)/eps) from the scaled squared distance q = d^2/eps^2
-MF_DEV double xi256_scaled(const AsmParams &P, double q) {
-  int hi = __double2hiint(q);
-  hi = min(max(hi, P.hq_lo), P.hq_hi);
-  const double qc = __hiloint2double(hi, __double2loint(q));
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(qc));
-  const double hy = __hiloint2double(__double2hiint(y) - 0x00100000, 0);
-  const double u0 = qc * y;
-  const double t = fma(-hy, u0, 1.5);
-  const double r = fma(-u0, t, P.alpha);
-  const double r2 = r * r;
-  double p = fma(35.0, r2, -180.0);
-  p = fma(p, r2, 378.0);
-  p = fma(p, r2, -420.0);
-  p = fma(p, r2, 315.0);
-  return fma(p, r, 128.0);
+// 256 xi((delta - d)/eps) from N scaled squared distances q = d^2/eps^2,
+// written stage by stage so the N chains interleave.  With the MUFU seed
+// z ~ 1/sqrt(q):  W = q z,  T = 3 - W z,  rho = 2 alpha - W T = 2 r  (the
+// Newton step for sqrt(q) with every constant folded: 3 DP operations, no
+// integer exponent fix-up), then xi as a polynomial in rho = 2 r (the
+// coefficients 315/2, -420/8, 378/32, -180/128, 35/512 are exact).
+template <int N>
+MF_DEV void xi256_scaled_n(const AsmParams &P, const double *q, double *out) {
+  double qc[N], z[N], W[N], T[N], r[N], r2[N], p[N];
+#pragma unroll
+  for (int i = 0; i < N; i++) {
+    int hi = __double2hiint(q[i]);
+    hi = min(max(hi, P.hq_lo), P.hq_hi);
+    qc[i] = __hiloint2double(hi, __double2loint(q[i]));
+  }
+#pragma unroll
+  for (int i = 0; i < N; i++)
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(z[i]) : "d"(qc[i]));
+#pragma unroll
+  for (int i = 0; i < N; i++) W[i] = qc[i] * z[i];
+#pragma unroll
+  for (int i = 0; i < N; i++) T[i] = fma(-W[i], z[i], 3.0);
+#pragma unroll
+  for (int i = 0; i < N; i++) r[i] = fma(-W[i], T[i], P.alpha2);
+#pragma unroll
+  for (int i = 0; i < N; i++) r2[i] = r[i] * r[i];
+#pragma unroll
+  for (int i = 0; i < N; i++) p[i] = fma(0.068359375, r2[i], -1.40625);
+#pragma unroll
+  for (int i = 0; i < N; i++) p[i] = fma(p[i], r2[i], 11.8125);
+#pragma unroll
+  for (int i = 0; i < N; i++) p[i] = fma(p[i], r2[i], -52.5);
+#pragma unroll
+  for (int i = 0; i < N; i++) p[i] = fma(p[i], r2[i], 157.5);
+#pragma unroll
+  for (int i = 0; i < N; i++) out[i] = fma(p[i], r[i], 128.0);
 }
 
 // Full event of child (hx, hy, hz): lane q1 evaluates its NO^3 point pairs
@@ -100,9 +131,10 @@ MF_DEV void event_full2(const AsmParams &P, const Ctx2<NO> &C, int ix, int iy,
 #pragma unroll
     for (int b = 0; b < NO; b++) {
       const double sxy = fma(d0, d0, sq1[b]);
-      double mu[NO];
+      double qq[NO], mu[NO];
 #pragma unroll
-      for (int c = 0; c < NO; c++) mu[c] = xi256_scaled(P, sxy + sq2[c]);
+      for (int c = 0; c < NO; c++) qq[c] = sxy + sq2[c];
+      xi256_scaled_n<NO>(P, qq, mu);
       double u0 = 0.0, u1 = 0.0;  // z contraction
 #pragma unroll
       for (int c = 0; c < NO; c++) {
@@ -154,8 +186,8 @@ __global__ void __launch_bounds__(kWarps2 * 32, MF_HEX2_MINB)
     s_rt[threadIdx.x] = xmul(xadd(Rr.box_out_x1d[threadIdx.x], 1.0), 0.5);
     s_rw[threadIdx.x] = Rr.box_out_w1d[threadIdx.x];
   }
-  if (threadIdx.x >= 32 && threadIdx.x < 40) {
-    const int j = threadIdx.x - 32;
+  if (threadIdx.x >= 8 && threadIdx.x < 16) {
+    const int j = threadIdx.x - 8;
     double s = 0.0;
     for (int q = 0; q < NQ1; q++)
       s += Rr.box_in_w[q] * Rr.phi_box_in[q * 8 + j];
@@ -178,9 +210,9 @@ __global__ void __launch_bounds__(kWarps2 * 32, MF_HEX2_MINB)
   }
   if (lane < 5) cnt[lane] = 0;
   __syncwarp();
-  const double jac_in = (0.5 * (C.ihi[0] - C.ilo[0])) *
-                        (0.5 * (C.ihi[1] - C.ilo[1])) *
-                        (0.5 * (C.ihi[2] - C.ilo[2]));
+  if (lane == 0)
+    C.jac_in = (0.5 * (C.ihi[0] - C.ilo[0])) * (0.5 * (C.ihi[1] - C.ilo[1])) *
+               (0.5 * (C.ihi[2] - C.ilo[2]));
   const bool active = lane < NQ1;
   // this lane's inner point, scaled by 1/eps; inactive lanes sit far away
   // (their q clamps to the outer shell edge: mu = 0)
@@ -194,7 +226,6 @@ __global__ void __launch_bounds__(kWarps2 * 32, MF_HEX2_MINB)
                         xsub(C.ihi[k], C.ilo[k])));
   }
   // point-set bounding boxes (outer rule nodes are sorted ascending)
-  const double tmin = s_rt[0], tmax = s_rt[NO - 1];
   if (lane < 3) {
     const double w = C.ihi[lane] - C.ilo[lane];
     double pmn = 1e300, pmx = -1e300;
@@ -208,8 +239,8 @@ __global__ void __launch_bounds__(kWarps2 * 32, MF_HEX2_MINB)
     C.pilo[lane] = pmn - 1e-12 * w;
     C.pihi[lane] = pmx + 1e-12 * w;
   }
+  if (active) buf[lane][8] = 0.0;  // G: sum over all pairs of sum_j V[j]
   __syncwarp();
-  double G = 0.0;
   int cx, cy, cz;
   cell_coords(M.elem_cell[m], M.ncx, M.ncy, cx, cy, cz);
   const int Rs = P.R;
@@ -221,22 +252,21 @@ __global__ void __launch_bounds__(kWarps2 * 32, MF_HEX2_MINB)
   // this lane's two A21 rows: local DOFs oi and oi + 4 of m (same x/y
   // corner, z and z+1); row box of the implicit pattern per row
   const int oj = lane & 7, oi = lane >> 3;
-  int rx0, ry0, rz0, rz1, rwx, rwy;
-  int64_t rb0, rb1;
   {
     const int gx = cx + (oi & 1), gy = cy + ((oi >> 1) & 1);
     const int K = P.pat.K;
-    rx0 = max(gx - K, 0);
-    rwx = min(gx + K, P.pat.NX - 1) - rx0 + 1;
-    ry0 = max(gy - K, 0);
-    rwy = min(gy + K, P.pat.NY - 1) - ry0 + 1;
-    rz0 = max(cz - K, 0);
-    rz1 = max(cz + 1 - K, 0);
+    const int rx0 = max(gx - K, 0), ry0 = max(gy - K, 0);
+    C.rbox[lane][0] = rx0;
+    C.rbox[lane][1] = ry0;
+    C.rbox[lane][2] = max(cz - K, 0);
+    C.rbox[lane][3] = max(cz + 1 - K, 0);
+    C.rbox[lane][4] = min(gx + K, P.pat.NX - 1) - rx0 + 1;
+    C.rbox[lane][5] = min(gy + K, P.pat.NY - 1) - ry0 + 1;
     const int64_t *md = M.elem_dofs + m * M.nloc_max;
-    rb0 = P.pat.rowptr[md[oi]];
-    rb1 = P.pat.rowptr[md[oi + 4]];
+    C.rb[lane][0] = P.pat.rowptr[md[oi]];
+    C.rb[lane][1] = P.pat.rowptr[md[oi + 4]];
   }
-  const double pw0 = s_pw[oi], pw1 = s_pw[oi + 4];
+  __syncwarp();
   const double dead2 = P.dp2 * (1.0 + 1e-9), plat2 = P.dm2 * (1.0 - 4e-9);
 
   for (int base = 0; base < ncell; base += 32) {
@@ -289,12 +319,15 @@ __global__ void __launch_bounds__(kWarps2 * 32, MF_HEX2_MINB)
         const int gx = (lpos & 1023) + (oj & 1);
         const int gy = ((lpos >> 10) & 1023) + ((oj >> 1) & 1);
         const int gz = (lpos >> 20) + (oj >> 2);
-        slot0 = rb0 + ((int64_t)(gz - rz0) * rwy + (gy - ry0)) * rwx +
-                (gx - rx0);
-        slot1 = rb1 + ((int64_t)(gz - rz1) * rwy + (gy - ry0)) * rwx +
-                (gx - rx0);
+        const int *rbx = C.rbox[lane];
+        const int rwx = rbx[4], rwy = rbx[5];
+        const int xy = (gy - rbx[1]) * rwx + (gx - rbx[0]);
+        slot0 = C.rb[lane][0] + (int64_t)(gz - rbx[2]) * (rwy * rwx) + xy;
+        slot1 = C.rb[lane][1] + (int64_t)(gz - rbx[3]) * (rwy * rwx) + xy;
+#ifndef MF_HEX2_NOPF
         asm volatile("prefetch.global.L2 [%0];" ::"l"(P.vals + slot0));
         asm volatile("prefetch.global.L2 [%0];" ::"l"(P.vals + slot1));
+#endif
       }
       // ---- phase 0: per-(axis, interval) terms, lanes 0..8 ----
       if (lane < 9) {
@@ -314,7 +347,7 @@ __global__ void __launch_bounds__(kWarps2 * 32, MF_HEX2_MINB)
         C.met[lane][1] = (a > b) ? a : b;
         // point-set boxes: dead / plateau proofs (1e-9 margins)
         const double w = hi - lo;
-        const double qlo = lo + tmin * w, qhi = lo + tmax * w;
+        const double qlo = lo + s_rt[0] * w, qhi = lo + s_rt[NO - 1] * w;
         const double e1 = qlo - C.pihi[k], e2 = C.pilo[k] - qhi;
         const double gd = fmax(fmax(e1, e2), 0.0);
         C.met[lane][2] = gd * gd;
@@ -397,8 +430,7 @@ __global__ void __launch_bounds__(kWarps2 * 32, MF_HEX2_MINB)
         }
         vp *= 256.0;
         gp *= 256.0;
-        double b0 = pw0 * vp, b1 = pw1 * vp;
-        G += gp;
+        double b0 = s_pw[oi] * vp, b1 = s_pw[oi + 4] * vp;
         if (mfull) {
           double V[8];
 #pragma unroll
@@ -413,10 +445,8 @@ __global__ void __launch_bounds__(kWarps2 * 32, MF_HEX2_MINB)
 #pragma unroll
             for (int j = 0; j < 8; j++) buf[lane][j] = V[j];
           }
-          double gs = 0.0;
 #pragma unroll
-          for (int j = 0; j < 8; j++) gs += V[j];
-          G += gs;
+          for (int j = 0; j < 8; j++) gp += V[j];
           __syncwarp();
 #pragma unroll
           for (int q = 0; q < NQ1; q++) {
@@ -426,7 +456,8 @@ __global__ void __launch_bounds__(kWarps2 * 32, MF_HEX2_MINB)
             b1 = fma(pw.y, v, b1);
           }
         }
-        const double sc = -P.scale * jac_in;
+        if (active) buf[lane][8] += gp;
+        const double sc = -P.scale * C.jac_in;
         // both old values loaded before either store (distinct rows; the
         // compiler cannot prove it and would serialise the two RMWs)
         const double o0 = P.vals[slot0], o1 = P.vals[slot1];
@@ -437,7 +468,6 @@ __global__ void __launch_bounds__(kWarps2 * 32, MF_HEX2_MINB)
     }
   }
   // A22 for the whole element: jac_in * sum_q1 G[q1] phiw[q1][i] phi[q1][j]
-  if (active) buf[lane][8] = G;
   __syncwarp();
   double b0 = 0.0, b1 = 0.0;
 #pragma unroll
@@ -449,7 +479,7 @@ __global__ void __launch_bounds__(kWarps2 * 32, MF_HEX2_MINB)
   }
   const int64_t *mdofs = M.elem_dofs + m * M.nloc_max;
   const int64_t col = mdofs[oj];
-  const double sc = P.scale * jac_in;
+  const double sc = P.scale * C.jac_in;
   P.vals[pat_index(P.pat, mdofs[oi], col)] += sc * b0;
   P.vals[pat_index(P.pat, mdofs[oi + 4], col)] += sc * b1;
   if (lane == 0) {
