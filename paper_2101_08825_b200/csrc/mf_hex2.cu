@@ -51,16 +51,11 @@ namespace {
 #endif
 constexpr int kWarps2 = MF_HEX2_WARPS;
 
-enum : int { A_NONE = 0, A_SPLIT = 1, A_UPPER = 2, A_PLAT = 3, A_DEAD = 4,
-             A_FULL = 5 };
-
 template <int NO>
 struct Ctx2 {
   double ilo[3], ihi[3];    // inner element box
   double pilo[3], pihi[3];  // bounding box of its quadrature points
   double box[32][6];        // candidate boxes of the batch (lo[3], hi[3])
-  double met[9][4];         // (axis, interval): gap, max-sep^2, point-set
-                            // gap^2, point-set max-sep^2
   double X[9][NO];          // (axis, interval): outer coordinates / eps
   double sh[9][2][NO];      // weighted pullback shapes (jacobian folded in)
   double S[9][2];           // their sums over the rule
@@ -270,9 +265,14 @@ __global__ void __launch_bounds__(kWarps2 * 32, MF_HEX2_MINB)
   const double dead2 = P.dp2 * (1.0 + 1e-9), plat2 = P.dm2 * (1.0 - 4e-9);
 
   for (int base = 0; base < ncell; base += 32) {
+    // ---- scan: every lane looks at one stencil cell, and classifies the
+    // pair it finds there all by itself (root + 8 children) ----
     const int ci = base + lane;
-    bool found = false;
-    int cpos = 0;  // candidate cell, packed x | y << 10 | z << 20
+    bool cand = false;
+    int cpos = 0;       // candidate cell, packed x | y << 10 | z << 20
+    unsigned cls = 0u;  // bits 0-7 full children, 8-15 plateau children,
+                        // 16 root plateau (UPPER)
+    unsigned ndead = 0u;
     if (ci < ncell) {
       const int x2 = xlo + ci % nx;
       const int tt = ci / nx;
@@ -281,35 +281,94 @@ __global__ void __launch_bounds__(kWarps2 * 32, MF_HEX2_MINB)
       const int64_t c2 = ((int64_t)z2 * M.ncy + y2) * M.ncx + x2;
       const int64_t l = M.cell_ptr[c2];
       if (l < M.cell_ptr[c2 + 1] && P.outer_mask[l]) {
-        // candidate test of _count_candidates (_kernels.py:1225-1233)
-        double gap = 0.0, lo[3], hi[3];
+        // per axis: root gap (the candidate test of _count_candidates,
+        // _kernels.py:1225-1233, is the root's _aprx_min), root max
+        // separation, and for the two halves the gap test and the
+        // point-set terms of the dead / plateau proofs
+        double gap = 0.0, smx[3], pd[3][2], pp[3][2];
+        unsigned alive = 0u;  // bit 2k + h: half h of axis k within reach
 #pragma unroll
         for (int k = 0; k < 3; k++) {
-          lo[k] = M.elem_lo[l * 3 + k];
-          hi[k] = M.elem_hi[l * 3 + k];
-          const double d1 = xsub(lo[k], C.ihi[k]);
-          const double d2 = xsub(C.ilo[k], hi[k]);
-          if (d1 > gap) gap = d1;
-          if (d2 > gap) gap = d2;
+          const double olo = M.elem_lo[l * 3 + k], ohi = M.elem_hi[l * 3 + k];
+          C.box[lane][k] = olo;
+          C.box[lane][3 + k] = ohi;
+          const double ilo = C.ilo[k], ihi = C.ihi[k];
+          const double r1 = xsub(olo, ihi), r2 = xsub(ilo, ohi);
+          if (r1 > gap) gap = r1;
+          if (r2 > gap) gap = r2;
+          const double ra = xmul(r1, r1), rb = xmul(r2, r2);
+          smx[k] = (ra > rb) ? ra : rb;
+          const double mid = xmul(0.5, xadd(olo, ohi));  // _kernels.py:262
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const double lo = h ? mid : olo, hi = h ? ohi : mid;
+            const double d1 = xsub(lo, ihi), d2 = xsub(ilo, hi);
+            // _aprx_min term max(0, d1, d2) < dpe
+            if (d1 < P.dpe && d2 < P.dpe) alive |= 1u << (2 * k + h);
+            const double w = hi - lo;
+            const double qlo = lo + s_rt[0] * w, qhi = lo + s_rt[NO - 1] * w;
+            const double e1 = qlo - C.pihi[k], e2 = C.pilo[k] - qhi;
+            const double gd = fmax(fmax(e1, e2), 0.0);
+            pd[k][h] = gd * gd;
+            pp[k][h] = fmax(e1 * e1, e2 * e2);
+          }
         }
         if (gap < P.dpe) {
-          found = true;
+          cand = true;
           cpos = x2 | (y2 << 10) | (z2 << 20);
+          bool split = true;
+          if (P.L_min <= 1) {
+            const double sm = xadd(xadd(smx[0], smx[1]), smx[2]);
+            if (aprx_max_lt_dme(P, sm)) {  // root inside delta - eps
+              split = false;
+              cls = 1u << 16;
+            }
+          }
+          if (split) {
 #pragma unroll
-          for (int k = 0; k < 3; k++) {
-            C.box[lane][k] = lo[k];
-            C.box[lane][3 + k] = hi[k];
+            for (int c = 0; c < 8; c++) {
+              const int hx = c & 1, hy = (c >> 1) & 1, hz = c >> 2;
+              const unsigned need =
+                  (1u << hx) | (4u << hy) | (16u << hz);
+              if ((alive & need) == need) {
+                const double sd = pd[0][hx] + pd[1][hy] + pd[2][hz];
+                const double sp = pp[0][hx] + pp[1][hy] + pp[2][hz];
+                if (sd >= dead2)
+                  ndead++;
+                else if (sp < plat2)
+                  cls |= 0x100u << c;
+                else
+                  cls |= 1u << c;
+              }
+            }
           }
         }
       }
     }
-    unsigned mask = __ballot_sync(0xffffffffu, found);
-    if (lane == 0) cnt[0] += __popc(mask);
+    // live pairs only enter the pair loop; the counters take everything
+    unsigned mask = __ballot_sync(0xffffffffu, cls != 0u);
+    {
+      const unsigned mc = __ballot_sync(0xffffffffu, cand);
+      const unsigned mu = __ballot_sync(0xffffffffu, (cls >> 16) != 0u);
+      const unsigned packed = ndead | (__popc(cls & 0xffu) << 10) |
+                              (__popc(cls & 0xff00u) << 20);
+      const unsigned tot = __reduce_add_sync(0xffffffffu, packed);
+      if (lane == 0) {
+        cnt[0] += __popc(mc);
+        cnt[1] += __popc(mu);
+        cnt[2] += tot >> 20;
+        cnt[3] += tot & 1023u;
+        cnt[4] += (tot >> 10) & 1023u;
+      }
+    }
     __syncwarp();
     while (mask) {
       const int src = __ffs(mask) - 1;
       mask &= mask - 1;
       const int lpos = __shfl_sync(0xffffffffu, cpos, src);
+      const unsigned pcls = __shfl_sync(0xffffffffu, cls, src);
+      const unsigned mfull = pcls & 0xffu;
+      const unsigned mplat = (pcls >> 8) & 0x1ffu;  // bit 8 = the root
       // this lane's two value slots of the pair's A21 block: column DOF oj
       // of l sits at cell(l) + corner offset (hex Q1 DOF grid = vertex
       // grid, fe_space.py:68-80); prefetched into L2 now, written at the
@@ -329,32 +388,15 @@ __global__ void __launch_bounds__(kWarps2 * 32, MF_HEX2_MINB)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(P.vals + slot1));
 #endif
       }
-      // ---- phase 0: per-(axis, interval) terms, lanes 0..8 ----
+      // ---- event axes of the pair: lanes (axis k, interval h) ----
       if (lane < 9) {
         const int k = lane / 3, h = lane - 3 * (lane / 3);
         const double olo = C.box[src][k], ohi = C.box[src][3 + k];
-        const double mid = xmul(0.5, xadd(olo, ohi));  // _kernels.py:262
+        const double mid = xmul(0.5, xadd(olo, ohi));
         const double lo = (h == 1) ? mid : olo;
         const double hi = (h == 0) ? mid : ohi;
-        // cell boxes: _aprx_min / _aprx_max terms, exact
-        const double d1 = xsub(lo, C.ihi[k]);
-        const double d2 = xsub(C.ilo[k], hi);
-        double g = 0.0;
-        if (d1 > g) g = d1;
-        if (d2 > g) g = d2;
-        const double a = xmul(d1, d1), b = xmul(d2, d2);
-        C.met[lane][0] = g;
-        C.met[lane][1] = (a > b) ? a : b;
-        // point-set boxes: dead / plateau proofs (1e-9 margins)
-        const double w = hi - lo;
-        const double qlo = lo + s_rt[0] * w, qhi = lo + s_rt[NO - 1] * w;
-        const double e1 = qlo - C.pihi[k], e2 = C.pilo[k] - qhi;
-        const double gd = fmax(fmax(e1, e2), 0.0);
-        C.met[lane][2] = gd * gd;
-        C.met[lane][3] = fmax(e1 * e1, e2 * e2);
-        // outer points and weighted pullback shapes of this interval
         const double oinv = rcp_fast(ohi - olo);
-        double hw = 0.5 * w;
+        double hw = 0.5 * (hi - lo);
         if (k == 0) hw *= P.cde * (1.0 / 256.0);
         double s0 = 0.0, s1 = 0.0;
 #pragma unroll
@@ -373,47 +415,6 @@ __global__ void __launch_bounds__(kWarps2 * 32, MF_HEX2_MINB)
         C.S[lane][1] = s1;
       }
       __syncwarp();
-      // ---- classification: lanes 0..7 = children, lane 8 = root ----
-      int act = A_NONE;
-      const int ix = (lane < 8) ? (lane & 1) : 2;
-      const int iy = 3 + ((lane < 8) ? ((lane >> 1) & 1) : 2);
-      const int iz = 6 + ((lane < 8) ? ((lane >> 2) & 1) : 2);
-      if (lane < 9) {
-        const double amin =
-            fmax(fmax(C.met[ix][0], C.met[iy][0]), C.met[iz][0]);
-        if (lane == 8) {
-          if (P.L_min > 1) {
-            act = A_SPLIT;
-          } else {
-            const double s =
-                xadd(xadd(C.met[ix][1], C.met[iy][1]), C.met[iz][1]);
-            if (aprx_max_lt_dme(P, s))
-              act = A_UPPER;
-            else if (amin < P.dpe)
-              act = A_SPLIT;
-          }
-        } else if (amin < P.dpe) {
-          const double sd = C.met[ix][2] + C.met[iy][2] + C.met[iz][2];
-          const double sp = C.met[ix][3] + C.met[iy][3] + C.met[iz][3];
-          act = (sd >= dead2) ? A_DEAD : (sp < plat2) ? A_PLAT : A_FULL;
-        }
-      }
-      const int ract = __shfl_sync(0xffffffffu, act, 8);
-      unsigned mfull = 0u, mplat = 0u;
-      if (ract == A_UPPER) {
-        mplat = 1u << 8;
-        if (lane == 0) cnt[1] += 1u;
-      } else if (ract == A_SPLIT) {
-        const unsigned kids = 0xffu;
-        mfull = __ballot_sync(0xffffffffu, act == A_FULL) & kids;
-        mplat = __ballot_sync(0xffffffffu, act == A_PLAT) & kids;
-        const unsigned mdead = __ballot_sync(0xffffffffu, act == A_DEAD) & kids;
-        if (lane == 0) {
-          cnt[2] += __popc(mplat);
-          cnt[3] += __popc(mdead);
-          cnt[4] += __popc(mfull);
-        }
-      }
       if (mfull | mplat) {
         // plateau events: V[q1][j] += 256 Sx[jx] Sy[jy] Sz[jz] for every
         // q1; lane (oi, oj) keeps component oj and the sum over j
