@@ -152,30 +152,23 @@ MF_DEV void tri_full(const AsmParams &P, const double *g, const OuterTri &O,
     const double ry = O.inv[2] * dx0 + O.inv[3] * dx1;
     const double p1 = rx * w2, p2 = ry * w2, p0 = w2 - p1 - p2;
     double mu[NQ1];
-    bool anysh = false;
-    unsigned shm = 0;
+    if (SHARP) {
 #pragma unroll
-    for (int q1 = 0; q1 < NQ1; q1++) {
-      const double dx = xsub(x0, y[q1][0]), dy = xsub(x1, y[q1][1]);
-      const double d2 = xadd(xmul(dx, dx), xmul(dy, dy));
-      if (SHARP) {
+      for (int q1 = 0; q1 < NQ1; q1++) {
+        const double dx = xsub(x0, y[q1][0]), dy = xsub(x1, y[q1][1]);
+        const double d2 = xadd(xmul(dx, dx), xmul(dy, dy));
         mu[q1] = d2 < P.dp2 ? 256.0 : 0.0;
-      } else {
-        // high-word classification + warp-voted shell (see mf_hex.cu)
-        const int hi = __double2hiint(d2);
-        const bool pl = hi < P.hi_dm2, sk = hi > P.hi_dp2;
-        const bool sh = !(pl || sk);
-        mu[q1] = sh ? d2 : (pl ? 256.0 : 0.0);
-        shm |= (unsigned)sh << q1;
-        anysh |= sh;
       }
-    }
-    if (!SHARP && (!VOTE || __any_sync(__activemask(), anysh))) {
-      double v[NQ1];
-      xi256_fast_n<NQ1>(P, mu, v);
+    } else {
+      // eps > 0: mu is continuous, so the distances may use fused
+      // arithmetic and the clamped mollifier needs no classification
+      double d2[NQ1];
 #pragma unroll
-      for (int q1 = 0; q1 < NQ1; q1++)
-        if ((shm >> q1) & 1u) mu[q1] = v[q1];
+      for (int q1 = 0; q1 < NQ1; q1++) {
+        const double dx = x0 - y[q1][0], dy = x1 - y[q1][1];
+        d2[q1] = fma(dy, dy, dx * dx);
+      }
+      xi256_clamped_n<NQ1>(P, d2, mu);
     }
 #pragma unroll
     for (int q1 = 0; q1 < NQ1; q1++) {
@@ -251,26 +244,15 @@ MF_DEV void quad_full(const AsmParams &P, const double *g, const OuterBox &O,
 #pragma unroll
     for (int b = 0; b < NO; b++) {
       double mu[NO];
-      unsigned shm = 0;
-#pragma unroll
-      for (int a = 0; a < NO; a++) {
-        const double d2 = xadd(sqx[a], sqy[b]);
-        if (SHARP) {
-          mu[a] = d2 < P.dp2 ? 256.0 : 0.0;
-        } else {
-          const int hi = __double2hiint(d2);
-          const bool pl = hi < P.hi_dm2, sk = hi > P.hi_dp2;
-          const bool shl = !(pl || sk);
-          mu[a] = shl ? d2 : (pl ? 256.0 : 0.0);
-          shm |= (unsigned)shl << a;
-        }
-      }
-      if (!SHARP && __any_sync(__activemask(), shm != 0)) {
-        double v[NO];
-        xi256_fast_n<NO>(P, mu, v);
+      if (SHARP) {
 #pragma unroll
         for (int a = 0; a < NO; a++)
-          if ((shm >> a) & 1u) mu[a] = v[a];
+          mu[a] = xadd(sqx[a], sqy[b]) < P.dp2 ? 256.0 : 0.0;
+      } else {
+        double d2[NO];
+#pragma unroll
+        for (int a = 0; a < NO; a++) d2[a] = sqx[a] + sqy[b];
+        xi256_clamped_n<NO>(P, d2, mu);
       }
       double t0 = 0.0, t1 = 0.0;
 #pragma unroll

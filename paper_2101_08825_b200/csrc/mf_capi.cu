@@ -226,6 +226,8 @@ AsmParams make_params(const MfMesh *mesh, const MfRules *rules,
     P.hi_dm2 = (int32_t)(b >> 32);
     memcpy(&b, &P.dp2, 8);
     P.hi_dp2 = (int32_t)(b >> 32);
+    P.hd_lo = P.hi_dm2 - 1;
+    P.hd_hi = P.hi_dp2 + 1;
     // scaled shell edges: r = alpha - sqrt(q) leaves [-1, 1] by at most
     // 2^-20 relative there, where xi is flat to fourth order
     double ql = (P.alpha - 1.0) * (P.alpha - 1.0);

@@ -49,6 +49,7 @@ struct AsmParams {
                           // doubles order like their bit patterns)
   int32_t hq_lo, hq_hi;   // high words of the shell edges (alpha -/+ 1)^2
                           // of q = d^2/eps^2, widened by one unit
+  int32_t hd_lo, hd_hi;   // the same for d^2 itself: hi_dm2 - 1, hi_dp2 + 1
   int32_t nl_box, nl_tri;
   int32_t shortcuts;      // plateau/dead event shortcuts enabled
   double *scratch;        // per-thread scratch (generic kernel)
@@ -172,6 +173,52 @@ MF_DEV void xi256_fast_n(const AsmParams &P, const double *d2, double *out) {
   for (int i = 0; i < N; i++) p[i] = fma(p[i], r2[i], -420.0);
 #pragma unroll
   for (int i = 0; i < N; i++) p[i] = fma(p[i], r2[i], 315.0);
+#pragma unroll
+  for (int i = 0; i < N; i++) out[i] = fma(p[i], r[i], 128.0);
+}
+
+// 256 mu(d) for N squared distances, eps > 0, with no classification:
+// the high word of d2 is clamped to the shell [(delta-eps)^2,
+// (delta+eps)^2] (widened by one unit) with integer min/max -- xi(+-1) =
+// 256 / 0 with four vanishing derivatives, so the 2^-20 slack changes
+// nothing above 1e-21 -- then one MUFU rsqrt seed z and the Newton step
+// with its constants folded:  W = d2 z,  T = 3 - W z,  2 r = 2 alpha -
+// (W T) / eps,  and xi as a polynomial in 2 r (coefficients 315/2, -420/8,
+// 378/32, -180/128, 35/512, all exact).  10 DP operations, 2 integer, no
+// selects, no vote.  (B200: FP64 and integer-ALU instructions hold the
+// dispatch port for 2 cycles, so the selects of a classified form cost as
+// much as the polynomial they avoid.)
+template <int N>
+MF_DEV void xi256_clamped_n(const AsmParams &P, const double *d2,
+                            double *out) {
+  double dc[N], z[N], W[N], T[N], r[N], r2[N], p[N];
+#pragma unroll
+  for (int i = 0; i < N; i++) {
+    int hi = __double2hiint(d2[i]);
+    hi = min(max(hi, P.hd_lo), P.hd_hi);
+    dc[i] = __hiloint2double(hi, __double2loint(d2[i]));
+  }
+#pragma unroll
+  for (int i = 0; i < N; i++)
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(z[i]) : "d"(dc[i]));
+#pragma unroll
+  for (int i = 0; i < N; i++) W[i] = dc[i] * z[i];
+#pragma unroll
+  for (int i = 0; i < N; i++) T[i] = fma(-W[i], z[i], 3.0);
+#pragma unroll
+  for (int i = 0; i < N; i++) W[i] = W[i] * T[i];
+#pragma unroll
+  for (int i = 0; i < N; i++) r[i] = fma(-W[i], P.inv_eps, P.alpha2);
+#pragma unroll
+  for (int i = 0; i < N; i++) r2[i] = r[i] * r[i];
+#pragma unroll
+  for (int i = 0; i < N; i++) p[i] = fma(0.068359375, r2[i], -1.40625);
+#pragma unroll
+  for (int i = 0; i < N; i++) p[i] = fma(p[i], r2[i], 11.8125);
+#pragma unroll
+  for (int i = 0; i < N; i++) p[i] = fma(p[i], r2[i], -52.5);
+#pragma unroll
+  for (int i = 0; i < N; i++) p[i] = fma(p[i], r2[i], 157.5);
 #pragma unroll
   for (int i = 0; i < N; i++) out[i] = fma(p[i], r[i], 128.0);
 }

@@ -125,6 +125,11 @@ struct OuterTet {
   MF_DEV double inv(int k) const { return p[(ST_INV + k) * kTetThreads]; }
 };
 
+// mollifier chains written together in a full event
+#ifndef MF_TET_CHAINS
+#define MF_TET_CHAINS 4
+#endif
+
 // full event on sub-tet g (oracle event_tet)
 template <int NQO, int NQ1, bool SHARP>
 MF_DEV void tet_full(const AsmParams &P, const double *g, const OuterTet &O,
@@ -150,42 +155,47 @@ MF_DEV void tet_full(const AsmParams &P, const double *g, const OuterTet &O,
     const double rz = O.inv(6) * d0 + O.inv(7) * d1 + O.inv(8) * d2;
     const double s1 = rx * w2, s2 = ry * w2, s3 = rz * w2;
     const double s0 = w2 - s1 - s2 - s3;
-    double mu[NQ1];
-    bool anysh = false;
-    unsigned shm = 0;
-#pragma unroll
-    for (int q1 = 0; q1 < NQ1; q1++) {
-      const double dx = xsub(x[0], y[q1][0][lane]),
-                   dy = xsub(x[1], y[q1][1][lane]),
-                   dz = xsub(x[2], y[q1][2][lane]);
-      const double dd = xadd(xadd(xmul(dx, dx), xmul(dy, dy)), xmul(dz, dz));
-      if (SHARP) {
-        mu[q1] = dd < P.dp2 ? 256.0 : 0.0;
-      } else {
-        const int hi = __double2hiint(dd);
-        const bool pl = hi < P.hi_dm2, sk = hi > P.hi_dp2;
-        const bool sh = !(pl || sk);
-        mu[q1] = sh ? dd : (pl ? 256.0 : 0.0);
-        shm |= (unsigned)sh << q1;
-        anysh |= sh;
-      }
-    }
-    if (!SHARP && __any_sync(__activemask(), anysh)) {
-      // one chain at a time (the batched form keeps NQ1 chains live and
-      // spills more at 168 registers; measured no faster)
+    if (SHARP) {
 #pragma unroll
       for (int q1 = 0; q1 < NQ1; q1++) {
-        double v;
-        xi256_fast_n<1>(P, &mu[q1], &v);
-        if ((shm >> q1) & 1u) mu[q1] = v;
+        const double dx = xsub(x[0], y[q1][0][lane]),
+                     dy = xsub(x[1], y[q1][1][lane]),
+                     dz = xsub(x[2], y[q1][2][lane]);
+        const double dd = xadd(xadd(xmul(dx, dx), xmul(dy, dy)), xmul(dz, dz));
+        const double mu = dd < P.dp2 ? 256.0 : 0.0;
+        V[q1][0] = fma(mu, s0, V[q1][0]);
+        V[q1][1] = fma(mu, s1, V[q1][1]);
+        V[q1][2] = fma(mu, s2, V[q1][2]);
+        V[q1][3] = fma(mu, s3, V[q1][3]);
       }
-    }
+    } else {
+      // eps > 0: mu is continuous, so fused distances and the clamped
+      // mollifier (no classification, no vote), contracted at once
+      constexpr int GB = MF_TET_CHAINS;
 #pragma unroll
-    for (int q1 = 0; q1 < NQ1; q1++) {
-      V[q1][0] = fma(mu[q1], s0, V[q1][0]);
-      V[q1][1] = fma(mu[q1], s1, V[q1][1]);
-      V[q1][2] = fma(mu[q1], s2, V[q1][2]);
-      V[q1][3] = fma(mu[q1], s3, V[q1][3]);
+      for (int q0 = 0; q0 < NQ1; q0 += GB) {
+        double dd[GB], v[GB];
+#pragma unroll
+        for (int i = 0; i < GB; i++) {
+          const int q1 = (q0 + i < NQ1) ? q0 + i : NQ1 - 1;
+          const double dx = x[0] - y[q1][0][lane], dy = x[1] - y[q1][1][lane],
+                       dz = x[2] - y[q1][2][lane];
+          dd[i] = fma(dz, dz, fma(dy, dy, dx * dx));
+        }
+        // compiler-only barrier: without it the shared-memory point loads
+        // of every group are hoisted above the chains and k_tet spills
+        // 504 bytes instead of 164 (R4-tet 17.5 -> 23.6 s)
+        asm volatile("" ::: "memory");
+        xi256_clamped_n<GB>(P, dd, v);
+#pragma unroll
+        for (int i = 0; i < GB; i++)
+          if (q0 + i < NQ1) {
+            V[q0 + i][0] = fma(v[i], s0, V[q0 + i][0]);
+            V[q0 + i][1] = fma(v[i], s1, V[q0 + i][1]);
+            V[q0 + i][2] = fma(v[i], s2, V[q0 + i][2]);
+            V[q0 + i][3] = fma(v[i], s3, V[q0 + i][3]);
+          }
+      }
     }
   }
 }
@@ -378,6 +388,39 @@ __global__ void __launch_bounds__(32 * kTetWarps, MF_TET_MINB(NQ1))
               if (d2 > gap) gap = d2;
             }
             if (!(gap < P.dpe)) continue;
+            // Whole-pair dead proof.  Every descendant of the root lies in
+            // its vertex box (Bey midpoints round inside their edge), so
+            // (a) if the box's FAR sides are within delta+eps of the inner
+            // box on every axis, every descendant passes the _aprx_min
+            // test (rounded subtraction is monotone) and none is UPPER:
+            // Algorithm 1 splits down to 8^(L_max-1) leaves, and (b) if
+            // the box is farther than delta+eps from the inner POINT box,
+            // every leaf is dead (its point box lies inside).  The leaves
+            // are counted; nothing is integrated (the reference skips
+            // every point pair too, _kernels.py:134-135).
+            if (P.shortcuts && P.L_max >= 2) {
+              bool all = true;
+              double sg = 0.0;
+#pragma unroll
+              for (int k = 0; k < 3; k++) {
+                all = all &&
+                      xsub(hi[k], st[(ST_IHI + k) * kTetThreads]) < P.dpe &&
+                      xsub(st[(ST_ILO + k) * kTetThreads], lo[k]) < P.dpe;
+                const double mg = 1e-9 * (hi[k] - lo[k]);
+                const double gk =
+                    fmax(fmax(lo[k] - mg - st[(ST_PIHI + k) * kTetThreads],
+                              st[(ST_PILO + k) * kTetThreads] - hi[k] - mg),
+                         0.0);
+                sg += gk * gk;
+              }
+              if (all && sg >= P.dp2 * (1.0 + 2e-9)) {
+                const unsigned nleaf = 1u << (3 * (P.L_max - 1));
+                c_pairs++;
+                c_ev += nleaf;
+                c_dead += nleaf;
+                continue;
+              }
+            }
           }
           c_pairs++;
           const int tout = (int)(l % 6);
