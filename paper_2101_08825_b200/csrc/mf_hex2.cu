@@ -70,6 +70,9 @@ struct Ctx2 {
 // Newton step for sqrt(q) with every constant folded: 3 DP operations, no
 // integer exponent fix-up), then xi as a polynomial in rho = 2 r (the
 // coefficients 315/2, -420/8, 378/32, -180/128, 35/512 are exact).
+// (Dropping one clamp side for events proven to have no point pair beyond
+// delta+eps, or none inside delta-eps, was measured: 860.6 vs 855.4 ms on
+// R4-half with four event instantiations -- no gain, not kept.)
 template <int N>
 MF_DEV void xi256_scaled_n(const AsmParams &P, const double *q, double *out) {
   double qc[N], z[N], W[N], T[N], r[N], r2[N], p[N];
@@ -209,15 +212,16 @@ __global__ void __launch_bounds__(kWarps2 * 32, MF_HEX2_MINB)
     C.jac_in = (0.5 * (C.ihi[0] - C.ilo[0])) * (0.5 * (C.ihi[1] - C.ilo[1])) *
                (0.5 * (C.ihi[2] - C.ilo[2]));
   const bool active = lane < NQ1;
-  // this lane's inner point, scaled by 1/eps; inactive lanes sit far away
-  // (their q clamps to the outer shell edge: mu = 0)
-  double ys[3] = {1e100, 1e100, 1e100};
-  if (active) {
+  // this lane's inner point, scaled by 1/eps; inactive lanes mirror a
+  // real point (their results are never read)
+  double ys[3];
+  {
+    const int pq = lane % NQ1;
 #pragma unroll
     for (int k = 0; k < 3; k++)
       ys[k] = P.inv_eps *
               xadd(C.ilo[k],
-                   xmul(xmul(xadd(Rr.box_in_pts[lane * 3 + k], 1.0), 0.5),
+                   xmul(xmul(xadd(Rr.box_in_pts[pq * 3 + k], 1.0), 0.5),
                         xsub(C.ihi[k], C.ilo[k])));
   }
   // point-set bounding boxes (outer rule nodes are sorted ascending)
@@ -438,8 +442,9 @@ __global__ void __launch_bounds__(kWarps2 * 32, MF_HEX2_MINB)
           for (int j = 0; j < 8; j++) V[j] = 0.0;
           for (unsigned mm = mfull; mm; mm &= mm - 1) {
             const int c = __ffs(mm) - 1;
-            event_full2<NO>(P, C, c & 1, 3 + ((c >> 1) & 1),
-                            6 + ((c >> 2) & 1), ys, V);
+            const int ix = c & 1, iy = 3 + ((c >> 1) & 1),
+                      iz = 6 + ((c >> 2) & 1);
+            event_full2<NO>(P, C, ix, iy, iz, ys, V);
           }
           // b21[i][j] = -jac_in * sum_q1 phiw[q1][i] V[q1][j]
           if (active) {

@@ -24,9 +24,9 @@ def _assemble(name, flags=0):
 
 
 @pytest.mark.parametrize("name", golden_names())
-@pytest.mark.parametrize("flags", [0, 1, 2, 4], ids=["auto", "generic",
-                                                      "noshortcut",
-                                                      "elemthreads"])
+@pytest.mark.parametrize("flags", [0, 1, 2, 4, 8],
+                         ids=["auto", "generic", "noshortcut", "elemthreads",
+                              "hexlevels"])
 def test_assemble_matches_reference(name, flags):
     g, A = _assemble(name, flags)
     assert np.array_equal(A.rowptr, g["rowptr"]) and A.K == int(g["K"])
@@ -154,3 +154,33 @@ def test_blocked_rejects_mixed():
     mesh, space, kp, cfg = g.build()
     with pytest.raises(ValueError):
         assemble(mesh, space, kp, AssemblyConfig(strategy="blocked"))
+
+
+@pytest.mark.parametrize("outer,inner", [("gauss2", "gauss2"),
+                                         ("gauss3", "gauss2"),
+                                         ("gauss4", "gauss3"),
+                                         ("default", "default")])
+@pytest.mark.parametrize("L_min", [1, 2])
+def test_hex_separable_kernel_rules_and_lmin(outer, inner, L_min):
+    """k_hex2 (the L_max = 2 kernel: per-axis classification terms, lanes
+    classify their own pairs, clamped mollifier) for every rule size it
+    is instantiated for and both L_min, against the oracle and against the
+    level-synchronous k_hex (MF_FLAG_HEX_LEVELS): identical events, values
+    within the tolerance."""
+    import oracle
+    from paper_2101_08825_b200 import (AssemblyConfig, FESpace, KernelParams,
+                                       assemble, build_mesh)
+    h = 1 / 16
+    kp = KernelParams(3, 2.4 * h, h / 2, kappa=2.0)
+    mesh = build_mesh(3, ((0.0, 0.25),) * 3, h, kp.delta + kp.eps, "hex")
+    space = FESpace(mesh, 1)
+    cfg = AssemblyConfig(L_min=L_min, L_max=2, outer_rule=outer,
+                         inner_rule=inner, strategy="general")
+    A = assemble(mesh, space, kp, cfg)
+    B = assemble(mesh, space, kp, cfg, flags=8)
+    R = oracle.assemble_general(mesh, space, kp, cfg)
+    assert A.events == R.events == B.events
+    assert rel_frob(A.vals, R.vals) <= TOL
+    assert rel_frob(A.vals, B.vals) <= 1e-12
+    assert abs(A.presym_asymmetry - R.presym_asymmetry) <= 1e-9 * np.abs(
+        R.vals).max()
