@@ -43,6 +43,23 @@ struct Cfg<0> {  // quad Q1
   static constexpr int NCHILD = 4;
 };
 
+// position of the n-th (n >= 1) set bit of m, which must have at least n
+// set bits: popc binary search (5 steps; the __fns intrinsic is a long
+// generic loop and was 7% of k_tri_q's instructions)
+MF_DEV int nth_set_bit(unsigned m, int n) {
+  int pos = 0;
+#pragma unroll
+  for (int h = 16; h >= 1; h >>= 1) {
+    const int c = __popc(m & ((1u << h) - 1u));
+    if (n > c) {
+      n -= c;
+      pos += h;
+      m >>= h;
+    }
+  }
+  return pos;
+}
+
 // sub-cell bbox (_kernels.py:214-222)
 template <int KIND>
 MF_DEV void sub_bbox(const double *g, double *lo, double *hi) {
@@ -958,9 +975,11 @@ __global__ void __launch_bounds__(32 * kTriQWarps, MINB)
   // per-event V of a phase-B round; phase W reuses the first 11 rows for
   // the owners' inner boxes, plateau sums and point-set boxes
   constexpr int NRES = NV > 11 ? NV : 11;
-  __shared__ double s_res[kTriQWarps][NRES][32];
+  // (row pitch 33: the segment sums below read one ROW per lane)
+  __shared__ double s_res[kTriQWarps][NRES][33];
   __shared__ int s_off[kTriQWarps][33];
   __shared__ unsigned s_mask[kTriQWarps][32];
+  __shared__ int s_own[kTriQWarps][32];      // owner lane of a round's event
   // the lane's 3 pattern rows: rowptr base shifted to (ylo, xlo), width
   __shared__ long long s_rb[kTriQWarps][NL][32];
   __shared__ int s_wx[kTriQWarps][NL][32];
@@ -1118,9 +1137,9 @@ __global__ void __launch_bounds__(32 * kTriQWarps, MINB)
     if (wmask) {
       const int nper = 1 << nleaf_bits;  // 4 (L_max 2) or 16 (L_max 3)
       const int grp = lane / nper, sl = lane % nper;
-      double(*s_ib)[32] = s_res[w];         // owner inner boxes (4 rows)
-      double(*s_sp)[32] = s_res[w] + 4;     // owner plateau sums (3 rows)
-      double(*s_pb)[32] = s_res[w] + 7;     // owner point-set boxes (4)
+      double(*s_ib)[33] = s_res[w];         // owner inner boxes (4 rows)
+      double(*s_sp)[33] = s_res[w] + 4;     // owner plateau sums (3 rows)
+      double(*s_pb)[33] = s_res[w] + 7;     // owner point-set boxes (4)
       s_ib[0][lane] = ilo[0];
       s_ib[1][lane] = ilo[1];
       s_ib[2][lane] = ihi[0];
@@ -1132,7 +1151,7 @@ __global__ void __launch_bounds__(32 * kTriQWarps, MINB)
       __syncwarp();
       while (wmask) {
         const int cnt = __popc(wmask);
-        const int o = grp < cnt ? (int)__fns(wmask, 0, grp + 1) : -1;
+        const int o = grp < cnt ? nth_set_bit(wmask, grp + 1) : -1;
         double spi[NL] = {0.0, 0.0, 0.0};
         bool fl = false, lv = false;
         if (o >= 0) {
@@ -1244,7 +1263,7 @@ __global__ void __launch_bounds__(32 * kTriQWarps, MINB)
         for (int step = 16; step >= 1; step >>= 1)
           if (s_off[w][o + step] <= g) o += step;
         const unsigned om = s_mask[w][o];
-        const int leaf = __fns(om, 0, g - s_off[w][o] + 1);
+        const int leaf = nth_set_bit(om, g - s_off[w][o] + 1);
         double gg[6];
 #pragma unroll
         for (int u = 0; u < 6; u++) gg[u] = s_root[w][u][o];
@@ -1284,15 +1303,40 @@ __global__ void __launch_bounds__(32 * kTriQWarps, MINB)
         for (int q = 0; q < NQ1; q++)
 #pragma unroll
           for (int j = 0; j < NL; j++) s_res[w][q * NL + j][lane] = Ve[q][j];
+        s_own[w][lane] = o;
       }
       __syncwarp();
-      // owner: add this round's results of its own events, queue order
+      // Segment sums: lane v < NV walks row v of the round's results and
+      // sums each owner's run of events in queue order, leaving the sum in
+      // the run's first column; then every owner adds ONE value per row.
+      // (Each owner used to walk its own events: the warp then ran the
+      // longest owner's loop with 2 NV instructions per event -- 12% of
+      // the kernel's instructions.)  Fixed order: deterministic.
+      const int nround = min(32, total - base);
+      if (lane < NV) {
+        double *row = s_res[w][lane];
+        int cur = s_own[w][0], first = 0;
+        double acc = row[0];
+        for (int k = 1; k < nround; k++) {
+          const int ok = s_own[w][k];
+          const double v = row[k];
+          if (ok != cur) {
+            row[first] = acc;
+            acc = 0.0;
+            cur = ok;
+            first = k;
+          }
+          acc += v;
+        }
+        row[first] = acc;
+      }
+      __syncwarp();
       const int a = max(off, base), b = min(off + cnt, base + 32);
-      for (int k = a; k < b; k++) {
+      if (a < b) {
 #pragma unroll
         for (int q = 0; q < NQ1; q++)
 #pragma unroll
-          for (int j = 0; j < NL; j++) V[q][j] += s_res[w][q * NL + j][k - base];
+          for (int j = 0; j < NL; j++) V[q][j] += s_res[w][q * NL + j][a - base];
       }
       __syncwarp();
     }

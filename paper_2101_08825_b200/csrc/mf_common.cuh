@@ -111,8 +111,10 @@ MF_DEV bool box_dead(const AsmParams &P, const double *alo, const double *ahi,
   double s = 0.0;
 #pragma unroll
   for (int k = 0; k < DIM; k++) {
-    double g = fmax(alo[k] - bhi[k], blo[k] - ahi[k]);
-    g = fmax(g, 0.0);
+    // compare-and-select, not fmax: its NaN handling doubles the
+    // instruction count on sm_100a and no NaN can occur here
+    double g = pmax(alo[k] - bhi[k], blo[k] - ahi[k]);
+    g = pmax(g, 0.0);
     s += g * g;
   }
   return s >= P.dp2 * (1.0 + 1e-9);

@@ -312,9 +312,9 @@ __global__ void __launch_bounds__(kWarps2 * 32, MF_HEX2_MINB)
             const double w = hi - lo;
             const double qlo = lo + s_rt[0] * w, qhi = lo + s_rt[NO - 1] * w;
             const double e1 = qlo - C.pihi[k], e2 = C.pilo[k] - qhi;
-            const double gd = fmax(fmax(e1, e2), 0.0);
+            const double gd = pmax(pmax(e1, e2), 0.0);
             pd[k][h] = gd * gd;
-            pp[k][h] = fmax(e1 * e1, e2 * e2);
+            pp[k][h] = pmax(e1 * e1, e2 * e2);
           }
         }
         if (gap < P.dpe) {

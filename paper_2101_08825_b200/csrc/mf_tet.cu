@@ -408,7 +408,7 @@ __global__ void __launch_bounds__(32 * kTetWarps, MF_TET_MINB(NQ1))
                       xsub(st[(ST_ILO + k) * kTetThreads], lo[k]) < P.dpe;
                 const double mg = 1e-9 * (hi[k] - lo[k]);
                 const double gk =
-                    fmax(fmax(lo[k] - mg - st[(ST_PIHI + k) * kTetThreads],
+                    pmax(pmax(lo[k] - mg - st[(ST_PIHI + k) * kTetThreads],
                               st[(ST_PILO + k) * kTetThreads] - hi[k] - mg),
                          0.0);
                 sg += gk * gk;
