@@ -795,6 +795,19 @@ def run_ours(args):
                 "executed_flops": executed,
                 "executed_tflops": achieved,
                 "executed_frac": achieved / peak}
+        cfgk = CONFIGS[name]
+        if cfgk[0] == 3 and cfgk[6] == "hex" and cfgk[7] == 2:
+            # k_hex2 issues 3 NO + 9 NO + 5 NO^2 + 12 NO^3 FP64 warp
+            # instructions per full event (mf_hex2.cu event_full2: 405 for
+            # NO = 3); the DFMA probe's peak is 64 flops per warp
+            # instruction.  This is the share of the FP64 pipe's issue
+            # slots the full events alone fill (ncu's FP64 pipe % of the
+            # same launch is a few points higher: classification, axes).
+            no = 2 if cfgk[8] == "gauss2" else 3
+            per_ev = 12 * no + 5 * no * no + 12 * no ** 3
+            rate = int(cnt[N.CNT_EV_FULL]) * per_ev / (kms * 1e-3)
+            roof["fp64_issue_frac_full_events"] = rate / (peak * 1e12 / 64)
+            roof["fp64_warp_instr_per_full_event"] = per_ev
     line = {
         "metric": METRIC, "value": value, "unit": "pairs/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
