@@ -623,38 +623,59 @@ class AssemblyContext:
         mesh, space = self.mesh, self.space
         axis = mesh.dim - 1
         nl = int(mesh.grid_ncells[axis])
-        work = pair_counts(mesh, self.params, self.dmesh)
+        gather = strategy == "blocked" and space.degree == 1
         fr = os.environ.get("MF_STREAM_FRACS")
-        if nslabs is not None:
-            layers = slab_layers(mesh, nslabs, work)
-        else:
-            # few ranges (every range adds a launch tail per colour), the
-            # last one small (its copy is exposed).
-            # cuts are fractions of the top-axis LAYERS (rows), not of the
-            # pair work: the time per pair varies across the domain, and
-            # what must be small is the byte count of the ranges that
-            # finish last (traced on R4: work-based cuts left 6.5 GB to
-            # copy after the kernels)
-            # With the copies running during the kernels (finish waits on
-            # an event), two ranges suffice.  Measured end to end: R4
-            # (16 GB) 7.96 s with [0.5, 0.8, 0.93, 1] -> 7.78 s with
-            # [0.9, 1]; R3-16h (3.2 GB) 0.90 s with [0.5, 1], 1.12 s with
-            # [0.75, 1], 1.18 s with [0.9, 1] (its thread-per-element
-            # launches pay a long per-thread tail on a thin range); R2 is
-            # indifferent (1.55 s).
+        if gather:
+            # The entry-wise gather writes whole rows, has no colours (no
+            # launch tails) and runs about as long as the copy of what it
+            # writes, so it streams in many even ranges: the copy of range
+            # s overlaps the gather of range s+1 (R4 default path, host in
+            # to host out: 0.82 s with the general path's [0.9, 1] cut,
+            # which copied 90% of the matrix after computing it).  No pair
+            # counts and no colour plan are needed here.
+            work = None
             if fr:
                 fracs = [float(x) for x in fr.split(",")]
-            elif A.nnz * 8 > 2**33:
-                fracs = [0.9, 1.0]
-            elif A.nnz * 8 > 2**30:
-                fracs = [0.5, 1.0]
             else:
-                fracs = [1.0]
+                n = 8 if A.nnz * 8 > 2**30 else (2 if A.nnz * 8 > 2**28
+                                                  else 1)
+                fracs = [(k + 1) / n for k in range(n)]
             fracs = fracs[-max(1, min(len(fracs), nl // 4)):]
             fracs[-1] = 1.0
             layers = slab_layers_fracs(mesh, fracs, None)
-        plan = ColorPlan(mesh, None, self.device, work=work, layers=layers)
-        gather = strategy == "blocked" and space.degree == 1
+            plan = None
+        else:
+            work = pair_counts(mesh, self.params, self.dmesh)
+            if nslabs is not None:
+                layers = slab_layers(mesh, nslabs, work)
+            else:
+                # few ranges (every range adds a launch tail per colour),
+                # the last one small (its copy is exposed).
+                # cuts are fractions of the top-axis LAYERS (rows), not of
+                # the pair work: the time per pair varies across the
+                # domain, and what must be small is the byte count of the
+                # ranges that finish last (traced on R4: work-based cuts
+                # left 6.5 GB to copy after the kernels)
+                # With the copies running during the kernels (finish waits
+                # on an event), two ranges suffice.  Measured end to end:
+                # R4 (16 GB) 7.96 s with [0.5, 0.8, 0.93, 1] -> 7.78 s with
+                # [0.9, 1]; R3-16h (3.2 GB) 0.90 s with [0.5, 1], 1.12 s
+                # with [0.75, 1], 1.18 s with [0.9, 1] (its
+                # thread-per-element launches pay a long per-thread tail on
+                # a thin range); R2 is indifferent (1.55 s).
+                if fr:
+                    fracs = [float(x) for x in fr.split(",")]
+                elif A.nnz * 8 > 2**33:
+                    fracs = [0.9, 1.0]
+                elif A.nnz * 8 > 2**30:
+                    fracs = [0.5, 1.0]
+                else:
+                    fracs = [1.0]
+                fracs = fracs[-max(1, min(len(fracs), nl // 4)):]
+                fracs[-1] = 1.0
+                layers = slab_layers_fracs(mesh, fracs, None)
+            plan = ColorPlan(mesh, None, self.device, work=work,
+                             layers=layers)
         counters = torch.zeros(N.MF_NCOUNTERS, dtype=torch.int64,
                                device=self.device)
         if strategy == "blocked":
@@ -670,7 +691,8 @@ class AssemblyContext:
         ranges = []
         done_plane = 0
         for s_, (lo, hi) in enumerate(layers):
-            g0, g1 = plan.group_range(s_)
+            if plan is not None:
+                g0, g1 = plan.group_range(s_)
             final = nplanes if s_ == len(layers) - 1 else d * hi
             if gather:
                 self.gather_blocks(A, done_plane * plane, final * plane)
@@ -691,12 +713,23 @@ class AssemblyContext:
         prefault = os.environ.get("MF_PREFAULT", "1") != "0"
 
         def worker():
+            pf = None
             if prefault:
                 # first-touch the fresh result pages while the first
                 # range computes, so the staged copies (and the exposed
-                # tail copy) write into mapped memory
-                stager.prefault(host)
+                # tail copy) write into mapped memory.  MF_PREFAULT=2 /
+                # the gather path: in a thread of its own, running ahead
+                # of the copies instead of before them (the gather is as
+                # short as the prefault itself)
+                if gather or os.environ.get("MF_PREFAULT") == "2":
+                    pf = threading.Thread(target=stager.prefault,
+                                          args=(host,), daemon=True)
+                    pf.start()
+                else:
+                    stager.prefault(host)
             stager.run(src, host, ranges)
+            if pf is not None:
+                pf.join()
 
         self._stream_thread = threading.Thread(target=worker, daemon=True)
         self._stream_thread.start()
