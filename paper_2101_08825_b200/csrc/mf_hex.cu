@@ -593,6 +593,8 @@ bool mf_hex_supported(const AsmParams &P) {
   const MfMesh &M = P.mesh;
   if (M.dim != 3 || M.degree != 1 || M.nloc_max != 8) return false;
   if (P.L_max > 4) return false;
+  // candidate cells are packed x | y << 10 | z << 20 in one register
+  if (M.ncx > 1023 || M.ncy > 1023 || M.ncz > 2047) return false;
   const MfRules &R = P.rules;
   if (R.n1d_box_in < 2 || R.n1d_box_in > 3) return false;
   if (R.n1d_box_out < 2 || R.n1d_box_out > 4) return false;
