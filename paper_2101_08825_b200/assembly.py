@@ -713,23 +713,16 @@ class AssemblyContext:
         prefault = os.environ.get("MF_PREFAULT", "1") != "0"
 
         def worker():
-            pf = None
-            if prefault:
-                # first-touch the fresh result pages while the first
-                # range computes, so the staged copies (and the exposed
-                # tail copy) write into mapped memory.  MF_PREFAULT=2 /
-                # the gather path: in a thread of its own, running ahead
-                # of the copies instead of before them (the gather is as
-                # short as the prefault itself)
-                if gather or os.environ.get("MF_PREFAULT") == "2":
-                    pf = threading.Thread(target=stager.prefault,
-                                          args=(host,), daemon=True)
-                    pf.start()
-                else:
-                    stager.prefault(host)
+            # first-touch the fresh result pages while the first range
+            # computes, so the staged copies (and the exposed tail copy)
+            # write into mapped memory.  Not on the gather path: its
+            # kernels are as short as the prefault itself, so the copy
+            # threads fault their own pages (measured the same 0.67 s on
+            # R4 either way), and a prefault running beside the copies
+            # would zero what they have already written.
+            if prefault and not gather:
+                stager.prefault(host)
             stager.run(src, host, ranges)
-            if pf is not None:
-                pf.join()
 
         self._stream_thread = threading.Thread(target=worker, daemon=True)
         self._stream_thread.start()
