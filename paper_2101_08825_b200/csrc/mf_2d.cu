@@ -1070,30 +1070,10 @@ __global__ void __launch_bounds__(32 * kTriQWarps, MINB)
     // ---- phase A: next candidate pair of this lane, walked alone ----
     bool have = false;
     while (l < l1) {
-#ifdef MF_TRIQ_SCAN_REGS
-      // candidate test of _count_candidates (_kernels.py:1225-1233) with
-      // the inner box from registers (elem_gap reloads it every time)
-      if (P.outer_mask[l]) {
-        const double2 lo = *reinterpret_cast<const double2 *>(M.elem_lo + 2 * l);
-        const double2 hi = *reinterpret_cast<const double2 *>(M.elem_hi + 2 * l);
-        double gap = 0.0;
-        const double a0 = xsub(lo.x, ihi[0]), b0 = xsub(ilo[0], hi.x);
-        const double a1 = xsub(lo.y, ihi[1]), b1 = xsub(ilo[1], hi.y);
-        if (a0 > gap) gap = a0;
-        if (b0 > gap) gap = b0;
-        if (a1 > gap) gap = a1;
-        if (b1 > gap) gap = b1;
-        if (gap < P.dpe) {
-          have = true;
-          break;
-        }
-      }
-#else
       if (P.outer_mask[l] && elem_gap<2>(M.elem_lo, M.elem_hi, l, m) < P.dpe) {
         have = true;
         break;
       }
-#endif
       l++;
     }
     if (!__any_sync(0xffffffffu, have)) break;
