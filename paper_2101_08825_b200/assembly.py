@@ -666,7 +666,10 @@ class AssemblyContext:
                 if fr:
                     fracs = [float(x) for x in fr.split(",")]
                 elif A.nnz * 8 > 2**33:
-                    fracs = [0.9, 1.0]
+                    # k_hex2 runs one warp per block, so a range's launch
+                    # tails are short now: R4 e2e 4.652 s with [0.9, 1],
+                    # 4.615 s with these four, 4.86 s with [0.95, 1]
+                    fracs = [0.5, 0.9, 0.98, 1.0]
                 elif A.nnz * 8 > 2**30:
                     fracs = [0.5, 1.0]
                 else:
