@@ -669,7 +669,10 @@ class AssemblyContext:
                     # k_hex2 runs one warp per block, so a range's launch
                     # tails are short now: R4 e2e 4.652 s with [0.9, 1],
                     # 4.615 s with these four, 4.86 s with [0.95, 1]
-                    fracs = [0.5, 0.9, 0.98, 1.0]
+                    # (the thread-level kernels keep two ranges: every
+                    # range costs them a tail per colour launch)
+                    fracs = ([0.5, 0.9, 0.98, 1.0] if mesh.kind == "hex"
+                             else [0.9, 1.0])
                 elif A.nnz * 8 > 2**30:
                     fracs = [0.5, 1.0]
                 else:
