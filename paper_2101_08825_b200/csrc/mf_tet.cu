@@ -239,10 +239,16 @@ enum : int { ACT_NONE = 0, ACT_SPLIT = 1, ACT_UPPER = 2, ACT_PLAT = 3,
 // folds A22.  Warps are independent (no block barrier after the start), so
 // the short planes at |dz| ~ R do not idle behind the long central ones.
 constexpr int kTetWarps = kTetThreads / 32;
-// blocks per SM: 3 for tet1/tet4 (<= 168 registers, small spill, measured
-// R4-tet 21.7 -> 20.5 s), 2 for tet11 (its V[11][4] would spill heavily)
+// blocks per SM: 2 for every rule (tet4: 235 registers, no spills).  With
+// the clamped mollifier the spill-free build wins: R4-tet 17.1 s at 3
+// blocks (168 registers, 164 B spilled), 15.7 s at 2, 28.4 s at 4 (128
+// registers).  (Round 1, classified mollifier: 3 blocks were faster.)
 #ifndef MF_TET_MINB
-#define MF_TET_MINB(NQ1) ((NQ1) > 4 ? 2 : 3)
+#ifdef MF_TET_MINB_ALL  // A/B builds: one value for every rule
+#define MF_TET_MINB(NQ1) (MF_TET_MINB_ALL)
+#else
+#define MF_TET_MINB(NQ1) 2
+#endif
 #endif
 
 template <int NQO, int NQ1>
