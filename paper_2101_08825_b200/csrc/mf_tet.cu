@@ -42,11 +42,14 @@ constexpr int kTetLevels = 6;
 // size, conflict-free): outer root vertices, the outer inverse map and the
 // inner box -- read rarely, so they need not occupy registers
 constexpr int kTetThreads = 128;
-// (ST_N sets the dynamic shared memory per block, 36 KB at 128 threads,
-// and with it the occupancy: 54 doubles per thread measured R4-tet 17.5 ->
-// 22.8 s)
+// (ST_N sets the dynamic shared memory per block: 54 KB at 128 threads.
+// At 3 blocks/SM the 18 midpoint rows cost occupancy, R4-tet 17.5 -> 22.8
+// s; at the 2 blocks/SM the kernel runs with now they are free.)
+// ST_MID: the root's edge midpoints m01 m02 m03 m12 m13 m23, cached when
+// the root splits, so a level-2 node is 12 loads instead of 18 midpoint
+// computations and a 8-way switch.
 enum : int { ST_ROOT = 0, ST_V0 = 12, ST_INV = 15, ST_ILO = 24, ST_IHI = 27,
-             ST_PILO = 30, ST_PIHI = 33, ST_N = 36 };
+             ST_PILO = 30, ST_PIHI = 33, ST_MID = 36, ST_N = 54 };
 
 // cube corners (bit k = axis k) of Kuhn tet p (mesh.py kuhn_corners)
 __constant__ int8_t c_tet_corner[6][4] = {{0, 1, 3, 7}, {0, 5, 1, 7},
@@ -92,12 +95,30 @@ MF_DEV void tet_child(const double *g, int b, double *c) {
 #undef MF_V
 }
 
-// node with path `code` (3 bits per level below the root), recomputed from
-// the root (shared-memory state st) with exact midpoints
+// state rows of the 4 vertices of Bey child b (tet_child's table): root
+// vertex i at ST_ROOT + 3 i, edge midpoint j at ST_MID + 3 j
+#define MF_M(j) (ST_MID + 3 * (j))
+__constant__ int8_t c_bey_row[8][4] = {
+    {0, MF_M(0), MF_M(1), MF_M(2)},       {MF_M(0), 3, MF_M(3), MF_M(4)},
+    {MF_M(1), MF_M(3), 6, MF_M(5)},       {MF_M(2), MF_M(4), MF_M(5), 9},
+    {MF_M(0), MF_M(1), MF_M(2), MF_M(4)}, {MF_M(0), MF_M(1), MF_M(3), MF_M(4)},
+    {MF_M(1), MF_M(2), MF_M(4), MF_M(5)}, {MF_M(1), MF_M(3), MF_M(4), MF_M(5)}};
+#undef MF_M
+
+// node with path `code` (3 bits per level below the root, L >= 2): the
+// level-2 node from the cached root vertices and edge midpoints, deeper
+// levels recomputed with exact midpoints
 MF_DEV void tet_path(const double *st, uint32_t code, int L, double *g) {
+  {
+    const int b = code & 7;
 #pragma unroll
-  for (int u = 0; u < 12; u++) g[u] = st[(ST_ROOT + u) * kTetThreads];
-  for (int l = 2; l <= L; l++) {
+    for (int v = 0; v < 4; v++) {
+      const int row = c_bey_row[b][v];
+#pragma unroll
+      for (int k = 0; k < 3; k++) g[3 * v + k] = st[(row + k) * kTetThreads];
+    }
+  }
+  for (int l = 3; l <= L; l++) {
     double c[12];
     tet_child(g, (code >> (3 * (l - 2))) & 7, c);
 #pragma unroll
@@ -527,6 +548,31 @@ __global__ void __launch_bounds__(32 * kTetWarps, MF_TET_MINB(NQ1))
                 tet_full<NQO, NQ1, true>(P, g, O, y, lane, s_opts, s_ow, V);
             }
             if (act == ACT_SPLIT) {
+              if (L == 1) {
+                // the root splits: cache its edge midpoints (exact, as
+                // tet_child computes them) for every level-2 node; the
+                // first child is (v0, m01, m02, m03)
+#pragma unroll
+                for (int k = 0; k < 3; k++) {
+                  const double m01 = xmul(0.5, xadd(g[k], g[3 + k]));
+                  const double m02 = xmul(0.5, xadd(g[k], g[6 + k]));
+                  const double m03 = xmul(0.5, xadd(g[k], g[9 + k]));
+                  st[(ST_MID + 9 + k) * kTetThreads] =
+                      xmul(0.5, xadd(g[3 + k], g[6 + k]));
+                  st[(ST_MID + 12 + k) * kTetThreads] =
+                      xmul(0.5, xadd(g[3 + k], g[9 + k]));
+                  st[(ST_MID + 15 + k) * kTetThreads] =
+                      xmul(0.5, xadd(g[6 + k], g[9 + k]));
+                  st[(ST_MID + k) * kTetThreads] = m01;
+                  st[(ST_MID + 3 + k) * kTetThreads] = m02;
+                  st[(ST_MID + 6 + k) * kTetThreads] = m03;
+                  g[3 + k] = m01;
+                  g[6 + k] = m02;
+                  g[9 + k] = m03;
+                }
+                L = 2;
+                continue;
+              }
               ++L;  // first child: code bits of level L stay 0
               double c[12];
               tet_child(g, 0, c);
