@@ -161,8 +161,11 @@ MF_DEV void tri_full(const AsmParams &P, const double *g, const OuterTri &O,
 #pragma unroll 1
   for (int q2 = 0; q2 < NQO; q2++) {
     const double px = s_pts[2 * q2], py = s_pts[2 * q2 + 1];
-    const double x0 = xadd(xadd(g[0], xmul(px, e10)), xmul(py, e20));
-    const double x1 = xadd(xadd(g[1], xmul(px, e11)), xmul(py, e21));
+    // eps = 0: the reference's unfused order (ties); else two FMAs
+    const double x0 = SHARP ? xadd(xadd(g[0], xmul(px, e10)), xmul(py, e20))
+                            : fma(py, e20, fma(px, e10, g[0]));
+    const double x1 = SHARP ? xadd(xadd(g[1], xmul(px, e11)), xmul(py, e21))
+                            : fma(py, e21, fma(px, e11, g[1]));
     const double w2 = s_w[q2] * f;
     const double dx0 = x0 - O.v0[0], dx1 = x1 - O.v0[1];
     const double rx = O.inv[0] * dx0 + O.inv[1] * dx1;

@@ -165,9 +165,13 @@ MF_DEV void tet_full(const AsmParams &P, const double *g, const OuterTet &O,
                  p2 = s_pts[3 * q2 + 2];
     double x[3];
 #pragma unroll
-    for (int k = 0; k < 3; k++)
-      x[k] = xadd(xadd(xadd(g[k], xmul(p0, e[0][k])), xmul(p1, e[1][k])),
-                  xmul(p2, e[2][k]));
+    for (int k = 0; k < 3; k++) {
+      if (SHARP)  // eps = 0: the reference's unfused order (ties)
+        x[k] = xadd(xadd(xadd(g[k], xmul(p0, e[0][k])), xmul(p1, e[1][k])),
+                    xmul(p2, e[2][k]));
+      else        // mu is continuous: three FMAs
+        x[k] = fma(p2, e[2][k], fma(p1, e[1][k], fma(p0, e[0][k], g[k])));
+    }
     const double w2 = s_w[q2] * f;
     const double d0 = x[0] - O.v0(0), d1 = x[1] - O.v0(1),
                  d2 = x[2] - O.v0(2);
