@@ -42,14 +42,50 @@ constexpr int kTetLevels = 6;
 // size, conflict-free): outer root vertices, the outer inverse map and the
 // inner box -- read rarely, so they need not occupy registers
 constexpr int kTetThreads = 128;
-// (ST_N sets the dynamic shared memory per block: 54 KB at 128 threads.
-// At 3 blocks/SM the 18 midpoint rows cost occupancy, R4-tet 17.5 -> 22.8
-// s; at the 2 blocks/SM the kernel runs with now they are free.)
+// Per-rule variants (A/B on the B200, profiles/r2/s4/ab_tet_*.log; all of
+// them bit-identical in values and events):
+// * lean (inner rules above MF_TET_LEAN_MINNQ points, i.e. tet11): the
+//   scatter geometry of the inner element's 4 rows and the G accumulators
+//   are not held in registers across the stencil walk.  The row bases and
+//   G live in the state rows, the x/y windows are recomputed per live pair
+//   (~40 integer instructions against ~5000 per pair).  tet11 spills 96
+//   bytes instead of 416: R5-tet-small 1970 -> 1767 ms.  tet4 has no
+//   spills to remove and loses L1 to the extra rows (R4-tet 14.96 ->
+//   15.04 s), so it keeps the register version.
+// * batch (same rules): see bey_row / the root split in k_tet.
+// * q2u: outer points of a full event unrolled together; 2 for inner rules
+//   of up to 4 points (8 independent mollifier chains, 242 registers, no
+//   spills: R4-tet 15.04 -> 14.66 s), 1 for tet11 (2 spills more).
+#ifndef MF_TET_LEAN_MINNQ
+#define MF_TET_LEAN_MINNQ 5
+#endif
+#ifndef MF_TET_BATCH_MINNQ
+#define MF_TET_BATCH_MINNQ 5
+#endif
+#ifndef MF_TET_Q2U_MAXNQ
+#define MF_TET_Q2U_MAXNQ 4
+#endif
+template <int NQ1>
+struct TetCfg {
+  static constexpr bool lean = NQ1 >= MF_TET_LEAN_MINNQ;
+  static constexpr bool batch = NQ1 >= MF_TET_BATCH_MINNQ;
+  static constexpr int q2u = NQ1 <= MF_TET_Q2U_MAXNQ ? 2 : 1;
+};
+// (tet_state_rows sets the dynamic shared memory per block: 51 KB at 128
+// threads for tet4, 66 KB for tet11.  3 blocks/SM lose even without spills
+// -- R4-tet 19.6 s, R5-tet-small 4973 ms with the lean state: three blocks
+// of state leave no L1 for the coordinate and value gathers.)
 // ST_MID: the root's edge midpoints m01 m02 m03 m12 m13 m23, cached when
 // the root splits, so a level-2 node is 12 loads instead of 18 midpoint
 // computations and a 8-way switch.
-enum : int { ST_ROOT = 0, ST_V0 = 12, ST_INV = 15, ST_ILO = 24, ST_IHI = 27,
-             ST_PILO = 30, ST_PIHI = 33, ST_MID = 36, ST_N = 54 };
+// (vertex 0 of the root is rows 0-2 of ST_ROOT; ST_ROWZ and the NQ1 rows of
+// ST_G exist for the lean rules only)
+enum : int { ST_ROOT = 0, ST_INV = 12, ST_ILO = 21, ST_IHI = 24, ST_PILO = 27,
+             ST_PIHI = 30, ST_MID = 33, ST_ROWZ = 51, ST_G = 55 };
+template <int NQ1>
+constexpr int tet_state_rows() {
+  return TetCfg<NQ1>::lean ? ST_G + NQ1 : ST_ROWZ;
+}
 
 // cube corners (bit k = axis k) of Kuhn tet p (mesh.py kuhn_corners)
 __constant__ int8_t c_tet_corner[6][4] = {{0, 1, 3, 7}, {0, 5, 1, 7},
@@ -105,6 +141,23 @@ __constant__ int8_t c_bey_row[8][4] = {
     {MF_M(1), MF_M(2), MF_M(4), MF_M(5)}, {MF_M(1), MF_M(3), MF_M(4), MF_M(5)}};
 #undef MF_M
 
+// the same table for unrolled code (static shared-memory offsets)
+MF_DEV constexpr int bey_row(int b, int v) {
+  constexpr int M0 = ST_MID, M1 = ST_MID + 3, M2 = ST_MID + 6,
+                M3 = ST_MID + 9, M4 = ST_MID + 12, M5 = ST_MID + 15;
+  constexpr int t[8][4] = {{0, M0, M1, M2},   {M0, 3, M3, M4},
+                           {M1, M3, 6, M5},   {M2, M4, M5, 9},
+                           {M0, M1, M2, M4},  {M0, M1, M3, M4},
+                           {M1, M2, M4, M5},  {M1, M3, M4, M5}};
+  return t[b][v];
+}
+
+// batch: when the root splits and L_max == 2, the 8 leaves are
+// classified in one unrolled, branch-free batch (independent chains,
+// static state rows), and only the plateau / full leaves are revisited
+// (tet11: R5-tet-small 1767 -> 1702 ms.  tet4: 255 registers and 56 bytes
+// spilled, R4-tet 15.04 -> 16.02 s, so it keeps the depth-first walk.)
+
 // node with path `code` (3 bits per level below the root, L >= 2): the
 // level-2 node from the cached root vertices and edge midpoints, deeper
 // levels recomputed with exact midpoints
@@ -142,7 +195,7 @@ MF_DEV double tet_edges(const double *g, double (*e)[3]) {
 
 struct OuterTet {
   const double *p;  // &s_state[0][threadIdx.x]
-  MF_DEV double v0(int k) const { return p[(ST_V0 + k) * kTetThreads]; }
+  MF_DEV double v0(int k) const { return p[(ST_ROOT + k) * kTetThreads]; }
   MF_DEV double inv(int k) const { return p[(ST_INV + k) * kTetThreads]; }
 };
 
@@ -159,7 +212,7 @@ MF_DEV void tet_full(const AsmParams &P, const double *g, const OuterTet &O,
   double e[3][3];
   const double det = fabs(tet_edges(g, e));
   const double f = det * P.cde * (1.0 / 256.0);
-#pragma unroll 1
+#pragma unroll(TetCfg<NQ1>::q2u)
   for (int q2 = 0; q2 < NQO; q2++) {
     const double p0 = s_pts[3 * q2], p1 = s_pts[3 * q2 + 1],
                  p2 = s_pts[3 * q2 + 2];
@@ -282,7 +335,7 @@ __global__ void __launch_bounds__(32 * kTetWarps, MF_TET_MINB(NQ1))
   __shared__ double s_phiw[NQ1][4];
   __shared__ double s_opts[3 * NQO], s_ow[NQO];
   __shared__ double s_y[kTetWarps][NQ1][3][32];  // inner points, lane-major
-  extern __shared__ double s_dyn[];  // s_state[ST_N][kTetThreads]
+  extern __shared__ double s_dyn[];  // s_state[tet_state_rows][kTetThreads]
   double(*s_state)[kTetThreads] =
       reinterpret_cast<double(*)[kTetThreads]>(s_dyn);
   const MfMesh &M = P.mesh;
@@ -352,10 +405,14 @@ __global__ void __launch_bounds__(32 * kTetWarps, MF_TET_MINB(NQ1))
     st[(ST_PIHI + k) * kTetThreads] = pmx + 1e-9 * (hi - lo);
   }
   const double fo = s_fo;
-  double G[NQ1];
+  constexpr bool kLean = TetCfg<NQ1>::lean;
+  double G[NQ1];  // (lean: unused, the sums live in the ST_G rows)
 #pragma unroll
-  for (int q = 0; q < NQ1; q++) G[q] = 0.0;
-  unsigned c_ev = 0, c_pairs = 0, c_up = 0, c_pl = 0, c_dead = 0, c_full = 0;
+  for (int q = 0; q < NQ1; q++) {
+    G[q] = 0.0;
+    if constexpr (kLean) st[(ST_G + q) * kTetThreads] = 0.0;
+  }
+  unsigned c_ev = 0, c_pairs = 0, c_up = 0, c_pl = 0, c_full = 0;
   int cx, cy, cz;
   cell_coords(M.elem_cell[m], M.ncx, M.ncy, cx, cy, cz);
   const int64_t *mdofs = M.elem_dofs + m * M.nloc_max;
@@ -378,6 +435,8 @@ __global__ void __launch_bounds__(32 * kTetWarps, MF_TET_MINB(NQ1))
       // row base shifted to the z layer of this plane's outer cubes
       rowz[i] = P.pat.rowptr[mdofs[i]] +
                 (int64_t)(z2 - rzlo) * rwy[i] * rwx[i];
+      if constexpr (kLean)
+        st[(ST_ROWZ + i) * kTetThreads] = __longlong_as_double(rowz[i]);
     }
     const double(*y)[3][32] = s_y[w];
     for (int dy = -Rs; dy <= Rs; dy++) {
@@ -448,7 +507,6 @@ __global__ void __launch_bounds__(32 * kTetWarps, MF_TET_MINB(NQ1))
                 const unsigned nleaf = 1u << (3 * (P.L_max - 1));
                 c_pairs++;
                 c_ev += nleaf;
-                c_dead += nleaf;
                 continue;
               }
             }
@@ -473,8 +531,6 @@ __global__ void __launch_bounds__(32 * kTetWarps, MF_TET_MINB(NQ1))
               st[(ST_INV + 3 * r + 2) * kTetThreads] =
                   (u[0] * v[1] - u[1] * v[0]) * idet;
             }
-#pragma unroll
-            for (int k = 0; k < 3; k++) st[(ST_V0 + k) * kTetThreads] = g[k];
           }
           double V[NQ1][4];
 #pragma unroll
@@ -536,7 +592,6 @@ __global__ void __launch_bounds__(32 * kTetWarps, MF_TET_MINB(NQ1))
             if (act >= ACT_UPPER) {
               ev++;
               if (act == ACT_UPPER) c_up++;
-              if (act == ACT_DEAD) c_dead++;
               if (act == ACT_PLAT) c_pl++;
               if (act == ACT_FULL) c_full++;
               const bool plateau =
@@ -574,6 +629,63 @@ __global__ void __launch_bounds__(32 * kTetWarps, MF_TET_MINB(NQ1))
                   g[6 + k] = m02;
                   g[9 + k] = m03;
                 }
+                if (TetCfg<NQ1>::batch && P.L_max == 2 && P.shortcuts) {
+                  double ilo[3], ihi[3], plo[3], phi[3];
+#pragma unroll
+                  for (int k = 0; k < 3; k++) {
+                    ilo[k] = st[(ST_ILO + k) * kTetThreads];
+                    ihi[k] = st[(ST_IHI + k) * kTetThreads];
+                    plo[k] = st[(ST_PILO + k) * kTetThreads];
+                    phi[k] = st[(ST_PIHI + k) * kTetThreads];
+                  }
+                  unsigned m_pl = 0, m_full = 0, n_ev = 0;
+#pragma unroll
+                  for (int b = 0; b < 8; b++) {
+                    double c[12], slo[3], shi[3], qlo[3], qhi[3];
+#pragma unroll
+                    for (int v = 0; v < 4; v++)
+#pragma unroll
+                      for (int k = 0; k < 3; k++)
+                        c[3 * v + k] = st[(bey_row(b, v) + k) * kTetThreads];
+                    tet_bbox(c, slo, shi);
+                    const bool near = aprx_min_d<3>(slo, shi, ilo, ihi) < P.dpe;
+#pragma unroll
+                    for (int k = 0; k < 3; k++) {
+                      const double cc =
+                          0.25 * ((c[k] + c[3 + k]) + (c[6 + k] + c[9 + k]));
+                      const double mg = 1e-9 * (shi[k] - slo[k]);
+                      qlo[k] = cc + fo * (slo[k] - cc) - mg;
+                      qhi[k] = cc + fo * (shi[k] - cc) + mg;
+                    }
+                    const bool dead = box_dead<3>(P, qlo, qhi, plo, phi);
+                    const bool plat = aprx_max_sq<3>(qlo, qhi, plo, phi) <
+                                      P.dm2 * (1.0 - 4e-9);
+                    const bool ev_pl = near && !dead && plat;
+                    const bool ev_fu = near && !dead && !plat;
+                    n_ev += near ? 1u : 0u;
+                    m_pl |= (ev_pl ? 1u : 0u) << b;
+                    m_full |= (ev_fu ? 1u : 0u) << b;
+                  }
+                  ev += n_ev;
+                  c_pl += __popc(m_pl);
+                  c_full += __popc(m_full);
+                  unsigned todo = m_pl | m_full;
+                  live |= todo != 0;
+                  while (todo) {
+                    const int b = __ffs(todo) - 1;
+                    todo &= todo - 1;
+                    tet_path(st, (uint32_t)b, 2, g);
+                    if ((m_pl >> b) & 1)
+                      tet_plateau<NQO>(P, g, O, s_opts, s_ow, SP);
+                    else if (P.eps > 0.0)
+                      tet_full<NQO, NQ1, false>(P, g, O, y, lane, s_opts, s_ow,
+                                                V);
+                    else
+                      tet_full<NQO, NQ1, true>(P, g, O, y, lane, s_opts, s_ow,
+                                               V);
+                  }
+                  break;
+                }
                 L = 2;
                 continue;
               }
@@ -599,6 +711,20 @@ __global__ void __launch_bounds__(32 * kTetWarps, MF_TET_MINB(NQ1))
           if (live) {
             double spsum = (SP[0] + SP[1]) + (SP[2] + SP[3]);
             const double sc = -P.scale * scale_in;
+            if constexpr (kLean) {
+              // (the values computed above are dead across the walk)
+#pragma unroll
+              for (int i = 0; i < 4; i++) {
+                const int v = c_tet_corner[tin][i];
+                const int gx = cx + (v & 1), gy = cy + ((v >> 1) & 1);
+                rxlo[i] = max(gx - P.pat.K, 0);
+                rwx[i] = min(gx + P.pat.K, P.pat.NX - 1) - rxlo[i] + 1;
+                rylo[i] = max(gy - P.pat.K, 0);
+                rwy[i] = min(gy + P.pat.K, P.pat.NY - 1) - rylo[i] + 1;
+                rowz[i] =
+                    __double_as_longlong(st[(ST_ROWZ + i) * kTetThreads]);
+              }
+            }
 #if MF_TET_LOADS_FIRST
             // the 16 old values are loaded together before any store, so
             // their latencies overlap (the compiler cannot hoist them past
@@ -651,7 +777,10 @@ __global__ void __launch_bounds__(32 * kTetWarps, MF_TET_MINB(NQ1))
               double s = spsum;
 #pragma unroll
               for (int j = 0; j < 4; j++) s += V[q][j];
-              G[q] += s;
+              if constexpr (kLean)
+                st[(ST_G + q) * kTetThreads] += s;
+              else
+                G[q] += s;
             }
           }
         }
@@ -660,8 +789,11 @@ __global__ void __launch_bounds__(32 * kTetWarps, MF_TET_MINB(NQ1))
   }
   double *gp = gscr + ((int64_t)pidx * P.n_inner + t) * NQ1;
 #pragma unroll
-  for (int q = 0; q < NQ1; q++) gp[q] = G[q];
+  for (int q = 0; q < NQ1; q++)
+    gp[q] = kLean ? st[(ST_G + q) * kTetThreads] : G[q];
   const unsigned mask = __activemask();
+  // every event is upper, plateau, dead or full
+  const unsigned c_dead = c_ev - c_up - c_pl - c_full;
   const unsigned v[6] = {c_ev, c_pairs, c_up, c_pl, c_dead, c_full};
   const int slot[6] = {MF_CNT_EVENTS, MF_CNT_PAIRS, MF_CNT_EV_UPPER,
                        MF_CNT_EV_PLATEAU, MF_CNT_EV_DEAD, MF_CNT_EV_FULL};
@@ -716,7 +848,7 @@ template <int NQO, int NQ1>
 cudaError_t launch(const AsmParams &P, double *gscr, cudaStream_t s) {
   const unsigned gx = (unsigned)((P.n_inner + 32 * kTetWarps - 1) /
                                  (32 * kTetWarps));
-  const size_t dyn = sizeof(double) * ST_N * kTetThreads;
+  const size_t dyn = sizeof(double) * tet_state_rows<NQ1>() * kTetThreads;
   cudaError_t ea = cudaFuncSetAttribute(
       k_tet<NQO, NQ1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
   if (ea != cudaSuccess) return ea;

@@ -68,6 +68,7 @@ def main():
             continue
         d = json.loads(r.stdout.strip().splitlines()[-1])
         v = np.load(out)
+        os.remove(out)   # R4-tet values are 16 GB per variant
         if base is None:
             base = v
         rel = float(np.linalg.norm(v - base) / np.linalg.norm(base))
