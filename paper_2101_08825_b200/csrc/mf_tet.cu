@@ -62,6 +62,9 @@ constexpr int kTetThreads = 128;
 #ifndef MF_TET_BATCH_MINNQ
 #define MF_TET_BATCH_MINNQ 5
 #endif
+#ifndef MF_TET_BATCH_HALF_MAXNQ
+#define MF_TET_BATCH_HALF_MAXNQ 0
+#endif
 #ifndef MF_TET_Q2U_MAXNQ
 #define MF_TET_Q2U_MAXNQ 4
 #endif
@@ -70,9 +73,11 @@ struct TetCfg {
   static constexpr bool lean = NQ1 >= MF_TET_LEAN_MINNQ;
   static constexpr bool batch = NQ1 >= MF_TET_BATCH_MINNQ;
   static constexpr int q2u = NQ1 <= MF_TET_Q2U_MAXNQ ? 2 : 1;
+  // (A/B knob: the batch in two halves of 4 leaves)
+  static constexpr bool batch_half = NQ1 <= MF_TET_BATCH_HALF_MAXNQ;
 };
 // (tet_state_rows sets the dynamic shared memory per block: 51 KB at 128
-// threads for tet4, 66 KB for tet11.  3 blocks/SM lose even without spills
+// threads for tet4, 72 KB for tet11.  3 blocks/SM lose even without spills
 // -- R4-tet 19.6 s, R5-tet-small 4973 ms with the lean state: three blocks
 // of state leave no L1 for the coordinate and value gathers.)
 // ST_MID: the root's edge midpoints m01 m02 m03 m12 m13 m23, cached when
@@ -80,11 +85,32 @@ struct TetCfg {
 // computations and a 8-way switch.
 // (vertex 0 of the root is rows 0-2 of ST_ROOT; ST_ROWZ and the NQ1 rows of
 // ST_G exist for the lean rules only)
+// ST_RBOX: the root's vertex box (lo, hi), written when the root splits.
+// The vertex box of CORNER child b of Bey's refinement (v_b and the three
+// midpoints of its edges) follows from it without min/max: rounding is
+// monotone, so min_j rn((v_b + v_j) / 2) = rn((v_b + min_j v_j) / 2), and
+// j = b gives v_b itself -- lo = mid(v_b, root lo), hi = mid(v_b, root
+// hi), the same bits as the min/max over the child's vertices, in 4
+// FP64 instructions per axis instead of 6 compare-and-selects (18
+// instructions; ncu: DSETP + FSEL were 20% of k_tet's instructions).
 enum : int { ST_ROOT = 0, ST_INV = 12, ST_ILO = 21, ST_IHI = 24, ST_PILO = 27,
-             ST_PIHI = 30, ST_MID = 33, ST_ROWZ = 51, ST_G = 55 };
+             ST_PIHI = 30, ST_MID = 33, ST_RBOX = 51, ST_ROWZ = 57, ST_G = 61 };
+// Measured (profiles/r2/s4/ab_tet_cornerbox_*.log, bit-identical): in the
+// batched classification (tet11) R5-tet-small 1722 -> 1688 ms; in the
+// depth-first walk (tet4) the dynamic child index and the 6 extra state
+// rows cost more than the selects saved (R4-tet 14.79 -> 15.07 s), so the
+// walk keeps tet_bbox and tet4 has no ST_RBOX rows.
+#ifndef MF_TET_CORNER_BOX
+#define MF_TET_CORNER_BOX 0
+#endif
+#ifndef MF_TET_CORNER_BOX_BATCH
+#define MF_TET_CORNER_BOX_BATCH 1
+#endif
 template <int NQ1>
 constexpr int tet_state_rows() {
-  return TetCfg<NQ1>::lean ? ST_G + NQ1 : ST_ROWZ;
+  return TetCfg<NQ1>::lean ? ST_G + NQ1
+         : (TetCfg<NQ1>::batch || MF_TET_CORNER_BOX) ? ST_ROWZ
+                                                      : ST_RBOX;
 }
 
 // cube corners (bit k = axis k) of Kuhn tet p (mesh.py kuhn_corners)
@@ -157,6 +183,52 @@ MF_DEV constexpr int bey_row(int b, int v) {
 // static state rows), and only the plateau / full leaves are revisited
 // (tet11: R5-tet-small 1767 -> 1702 ms.  tet4: 255 registers and 56 bytes
 // spilled, R4-tet 15.04 -> 16.02 s, so it keeps the depth-first walk.)
+
+// leaves B0 .. B0+NB-1 of a split root (L_max = 2): event or not, and
+// dead / plateau / full by the point-set proofs, as in the walk
+template <int B0, int NB>
+MF_DEV void tet_classify_leaves(const AsmParams &P, const double *st,
+                                double fo, const double *ilo,
+                                const double *ihi, const double *plo,
+                                const double *phi, unsigned &n_ev,
+                                unsigned &m_pl, unsigned &m_full) {
+#pragma unroll
+  for (int b = B0; b < B0 + NB; b++) {
+    double c[12], slo[3], shi[3], qlo[3], qhi[3];
+#pragma unroll
+    for (int v = 0; v < 4; v++)
+#pragma unroll
+      for (int k = 0; k < 3; k++)
+        c[3 * v + k] = st[(bey_row(b, v) + k) * kTetThreads];
+    if (MF_TET_CORNER_BOX_BATCH && b < 4) {
+#pragma unroll
+      for (int k = 0; k < 3; k++) {
+        slo[k] = xmul(0.5, xadd(c[3 * b + k],
+                                st[(ST_RBOX + k) * kTetThreads]));
+        shi[k] = xmul(0.5, xadd(c[3 * b + k],
+                                st[(ST_RBOX + 3 + k) * kTetThreads]));
+      }
+    } else {
+      tet_bbox(c, slo, shi);
+    }
+    const bool near = aprx_min_d<3>(slo, shi, ilo, ihi) < P.dpe;
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+      const double cc = 0.25 * ((c[k] + c[3 + k]) + (c[6 + k] + c[9 + k]));
+      const double mg = 1e-9 * (shi[k] - slo[k]);
+      qlo[k] = cc + fo * (slo[k] - cc) - mg;
+      qhi[k] = cc + fo * (shi[k] - cc) + mg;
+    }
+    const bool dead = box_dead<3>(P, qlo, qhi, plo, phi);
+    const bool plat =
+        aprx_max_sq<3>(qlo, qhi, plo, phi) < P.dm2 * (1.0 - 4e-9);
+    const bool ev_pl = near && !dead && plat;
+    const bool ev_fu = near && !dead && !plat;
+    n_ev += near ? 1u : 0u;
+    m_pl |= (ev_pl ? 1u : 0u) << b;
+    m_full |= (ev_fu ? 1u : 0u) << b;
+  }
+}
 
 // node with path `code` (3 bits per level below the root, L >= 2): the
 // level-2 node from the cached root vertices and edge midpoints, deeper
@@ -546,7 +618,18 @@ __global__ void __launch_bounds__(32 * kTetWarps, MF_TET_MINB(NQ1))
           int L = 1;
           for (;;) {
             double slo[3], shi[3], ilo[3], ihi[3];
-            tet_bbox(g, slo, shi);
+            if (MF_TET_CORNER_BOX && L == 2 && (code & 4) == 0) {
+              const int b = code & 3;  // corner child: see ST_RBOX
+#pragma unroll
+              for (int k = 0; k < 3; k++) {
+                const double vb = st[(ST_ROOT + 3 * b + k) * kTetThreads];
+                slo[k] = xmul(0.5, xadd(vb, st[(ST_RBOX + k) * kTetThreads]));
+                shi[k] =
+                    xmul(0.5, xadd(vb, st[(ST_RBOX + 3 + k) * kTetThreads]));
+              }
+            } else {
+              tet_bbox(g, slo, shi);
+            }
 #pragma unroll
             for (int k = 0; k < 3; k++) {
               ilo[k] = st[(ST_ILO + k) * kTetThreads];
@@ -613,6 +696,10 @@ __global__ void __launch_bounds__(32 * kTetWarps, MF_TET_MINB(NQ1))
                 // first child is (v0, m01, m02, m03)
 #pragma unroll
                 for (int k = 0; k < 3; k++) {
+                  if constexpr (TetCfg<NQ1>::batch || MF_TET_CORNER_BOX) {
+                    st[(ST_RBOX + k) * kTetThreads] = slo[k];
+                    st[(ST_RBOX + 3 + k) * kTetThreads] = shi[k];
+                  }
                   const double m01 = xmul(0.5, xadd(g[k], g[3 + k]));
                   const double m02 = xmul(0.5, xadd(g[k], g[6 + k]));
                   const double m03 = xmul(0.5, xadd(g[k], g[9 + k]));
@@ -639,32 +726,15 @@ __global__ void __launch_bounds__(32 * kTetWarps, MF_TET_MINB(NQ1))
                     phi[k] = st[(ST_PIHI + k) * kTetThreads];
                   }
                   unsigned m_pl = 0, m_full = 0, n_ev = 0;
-#pragma unroll
-                  for (int b = 0; b < 8; b++) {
-                    double c[12], slo[3], shi[3], qlo[3], qhi[3];
-#pragma unroll
-                    for (int v = 0; v < 4; v++)
-#pragma unroll
-                      for (int k = 0; k < 3; k++)
-                        c[3 * v + k] = st[(bey_row(b, v) + k) * kTetThreads];
-                    tet_bbox(c, slo, shi);
-                    const bool near = aprx_min_d<3>(slo, shi, ilo, ihi) < P.dpe;
-#pragma unroll
-                    for (int k = 0; k < 3; k++) {
-                      const double cc =
-                          0.25 * ((c[k] + c[3 + k]) + (c[6 + k] + c[9 + k]));
-                      const double mg = 1e-9 * (shi[k] - slo[k]);
-                      qlo[k] = cc + fo * (slo[k] - cc) - mg;
-                      qhi[k] = cc + fo * (shi[k] - cc) + mg;
-                    }
-                    const bool dead = box_dead<3>(P, qlo, qhi, plo, phi);
-                    const bool plat = aprx_max_sq<3>(qlo, qhi, plo, phi) <
-                                      P.dm2 * (1.0 - 4e-9);
-                    const bool ev_pl = near && !dead && plat;
-                    const bool ev_fu = near && !dead && !plat;
-                    n_ev += near ? 1u : 0u;
-                    m_pl |= (ev_pl ? 1u : 0u) << b;
-                    m_full |= (ev_fu ? 1u : 0u) << b;
+                  if constexpr (TetCfg<NQ1>::batch_half) {
+                    tet_classify_leaves<0, 4>(P, st, fo, ilo, ihi, plo, phi,
+                                              n_ev, m_pl, m_full);
+                    asm volatile("" ::: "memory");
+                    tet_classify_leaves<4, 4>(P, st, fo, ilo, ihi, plo, phi,
+                                              n_ev, m_pl, m_full);
+                  } else {
+                    tet_classify_leaves<0, 8>(P, st, fo, ilo, ihi, plo, phi,
+                                              n_ev, m_pl, m_full);
                   }
                   ev += n_ev;
                   c_pl += __popc(m_pl);
