@@ -215,6 +215,29 @@ def test_tet_oracle_linear_patch():
 
 # ---------------------------------------------------------------- GPU
 
+def test_bey_corner_child_box_from_root_box():
+    """k_tet's batched leaf classification (mf_tet.cu, ST_RBOX) takes the
+    vertex box of corner child b of Bey's refinement as mid(v_b, root box)
+    instead of the min/max over the child's 4 vertices.  Rounding is
+    monotone, so the two are the same bits: checked here on random,
+    jitter-like and degenerate-tie coordinates."""
+    rng = np.random.default_rng(7)
+    for trial in range(2000):
+        if trial % 3 == 0:       # lattice + jitter, many equal coordinates
+            v = (rng.integers(0, 3, (4, 3)) / 64.0
+                 + (trial % 2) * rng.uniform(-0.1, 0.1, (4, 3)) / 64.0 + 0.3)
+        elif trial % 3 == 1:     # wide dynamic range, both signs
+            v = rng.standard_normal((4, 3)) * 10.0 ** rng.integers(-8, 8)
+        else:
+            v = rng.uniform(-1.0, 2.0, (4, 3))
+        lo, hi = v.min(axis=0), v.max(axis=0)
+        for b in range(4):
+            child = np.array([v[b] if j == b else 0.5 * (v[b] + v[j])
+                              for j in range(4)])
+            assert np.array_equal(child.min(axis=0), 0.5 * (v[b] + lo))
+            assert np.array_equal(child.max(axis=0), 0.5 * (v[b] + hi))
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", sorted(CASES))
 def test_tet_gpu_matches_oracle(name):
