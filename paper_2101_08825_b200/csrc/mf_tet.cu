@@ -914,6 +914,13 @@ __global__ void __launch_bounds__(128) k_tet_a22(AsmParams P,
   }
 }
 
+// (A/B knob: an explicit minimal shared-memory carve-out changes nothing,
+// R4-tet 14381.6 vs 14382.5 ms, profiles/r2/s4/ab_tet_carveout_*.log: the
+// driver already picks the smallest carve-out that holds 2 blocks.)
+#ifndef MF_TET_CARVEOUT
+#define MF_TET_CARVEOUT 0
+#endif
+
 template <int NQO, int NQ1>
 cudaError_t launch(const AsmParams &P, double *gscr, cudaStream_t s) {
   const unsigned gx = (unsigned)((P.n_inner + 32 * kTetWarps - 1) /
@@ -922,6 +929,22 @@ cudaError_t launch(const AsmParams &P, double *gscr, cudaStream_t s) {
   cudaError_t ea = cudaFuncSetAttribute(
       k_tet<NQO, NQ1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
   if (ea != cudaSuccess) return ea;
+#if MF_TET_CARVEOUT
+  {
+    // shared-memory carve-out: just enough for the 2 resident blocks, the
+    // rest of the 256 KB stays L1 for the coordinate and value gathers
+    cudaFuncAttributes fa;
+    ea = cudaFuncGetAttributes(&fa, k_tet<NQO, NQ1>);
+    if (ea != cudaSuccess) return ea;
+    const size_t need = 2 * (dyn + fa.sharedSizeBytes + 1024);
+    int pct = (int)((need * 100 + 228 * 1024 - 1) / (228 * 1024));
+    if (pct > 100) pct = 100;
+    ea = cudaFuncSetAttribute(k_tet<NQO, NQ1>,
+                              cudaFuncAttributePreferredSharedMemoryCarveout,
+                              pct);
+    if (ea != cudaSuccess) return ea;
+  }
+#endif
   for (int pass = 0; pass < 2; pass++) {
     const int planes = pass == 0 ? P.R + 1 : P.R;
     if (planes < 1) continue;
