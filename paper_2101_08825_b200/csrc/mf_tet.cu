@@ -379,6 +379,25 @@ MF_DEV void tet_plateau(const AsmParams &P, const double *g,
 enum : int { ACT_NONE = 0, ACT_SPLIT = 1, ACT_UPPER = 2, ACT_PLAT = 3,
              ACT_DEAD = 4, ACT_FULL = 5 };
 
+// cache operators of the A21 read-modify-writes (A/B knob: 0 default,
+// 1 = .cg loads and stores (L2 only), 2 = streaming .cs).  Both lose
+// (profiles/r2/s4/ab_tet_valscache_*.log: R4-tet 14.39 -> 15.00 / 14.68 s,
+// R5-tet-small 1688 -> 2680 / 1722 ms): the 6 tets of an outer cube share
+// corner slots, and those re-reads are the L1 hits.
+#ifndef MF_TET_VALS_CACHE
+#define MF_TET_VALS_CACHE 0
+#endif
+#if MF_TET_VALS_CACHE == 1
+#define MF_TET_LDV(p) __ldcg(p)
+#define MF_TET_STV(p, v) __stcg(p, v)
+#elif MF_TET_VALS_CACHE == 2
+#define MF_TET_LDV(p) __ldcs(p)
+#define MF_TET_STV(p, v) __stcs(p, v)
+#else
+#define MF_TET_LDV(p) (*(p))
+#define MF_TET_STV(p, v) (*(p) = (v))
+#endif
+
 // A warp = 32 inner elements (lanes) of the current colour x ONE stencil
 // z-plane dz (blockIdx.y); a launch covers the planes of one parity.  The
 // lanes walk identical offset sequences (converged on unjittered meshes).
@@ -808,10 +827,10 @@ __global__ void __launch_bounds__(32 * kTetWarps, MF_TET_MINB(NQ1))
                           gzo = (v >> 2) & 1;
 #pragma unroll
                 for (int i = 0; i < 4; i++)
-                  old[i][j] = P.vals[rowz[i] +
-                                     ((int64_t)gzo * rwy[i] + (gy - rylo[i])) *
-                                         rwx[i] +
-                                     (gx - rxlo[i])];
+                  old[i][j] = MF_TET_LDV(
+                      P.vals + rowz[i] +
+                      ((int64_t)gzo * rwy[i] + (gy - rylo[i])) * rwx[i] +
+                      (gx - rxlo[i]));
               }
             }
 #endif
@@ -834,7 +853,7 @@ __global__ void __launch_bounds__(32 * kTetWarps, MF_TET_MINB(NQ1))
                     (gx - rxlo[i]);
 #if MF_TET_LOADS_FIRST
                 if constexpr (NQ1 <= MF_TET_LOADS_FIRST_MAXNQ)
-                  P.vals[slot] = old[i][j] + sc * b;
+                  MF_TET_STV(P.vals + slot, old[i][j] + sc * b);
                 else
                   P.vals[slot] += sc * b;
 #else
